@@ -1,0 +1,175 @@
+/*
+ * p2s.h -- C ABI of the B200-native DF-P2S dense-field turbulence simulator.
+ *
+ * Method: Chimitt, Zhang, Mao, Chan, "Real-Time Dense Field Phase-to-Space
+ * Simulation of Imaging through Atmospheric Turbulence", arXiv 2210.06713.
+ * Citations "P:<line>" refer to the paper's text; "Q<n>" to the
+ * readings of SURVEY.md Sec. 8(c) that DESIGN.md lists where the paper is
+ * silent.
+ *
+ * Per frame the library runs five steps on the GPU:
+ *   1. Fourier sampling of per-pixel Zernike coefficient fields: per-mode PSDs of
+ *      the homogeneous auto-correlation slices A_jj filter seeded
+ *      Hermitian white noise, a 2-D inverse DFT yields two real unit-variance
+ *      fields per complex transform, point-wise Noll mixing
+ *      a = L f with L L^T = A_0 (Eq.10).
+ *   2. Tilt warp from a_2, a_3 (bilinear gather, clamp-to-edge; Q12).
+ *   3. The P2S network mapping each pixel's higher-order Zernike vector a_4..a_Z
+ *      to K basis weights (shape Q13).
+ *   4. The spatially varying blur out_c(x) = sum_k w_k(x) (h_k (*) Iw_c)(x)
+ *      (Eq.9; true convolution, centre tap, mirror boundary Q14).
+ *   5. Optional PSF-sum normalisation, additive Gaussian noise, clamp (Q16).
+ *
+ * Conventions for every entry point:
+ *   - Functions never throw or abort; they return a p2s_status and store a
+ *     thread-local message retrievable with p2s_last_error().
+ *   - Argument checks are synchronous and happen before any launch
+ *     (P2S_ERR_INVALID_ARGUMENT).  Launch/driver failures -> P2S_ERR_CUDA.
+ *   - "dev" pointers are CUDA device pointers on the plan's device, "host"
+ *     pointers are ordinary host memory.  All arrays are dense, C order.
+ *   - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Work is enqueued on it and the call returns without synchronising,
+ *     except the *_host entry point, which synchronises before returning.
+ *   - Ownership: the plan owns its device tables and workspace (allocated in
+ *     p2s_plan_create, freed in p2s_plan_destroy).  The caller owns every buffer
+ *     it passes and must keep it alive until the enqueued work completes.  Host
+ *     arrays given to p2s_plan_create are copied.  No caller pointer is kept.
+ *   - Concurrency: a plan serialises its own calls (shared workspace); use one
+ *     plan per device/stream.  Plans on different devices are independent.
+ *   - Noise is counter-based (Philox4x32-10 keyed by the 64-bit seed, counter by
+ *     global frame index and spectral bin), so any frame range, batch split or
+ *     GPU partition reproduces the same bits.
+ */
+#ifndef P2S_H
+#define P2S_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  P2S_OK = 0,
+  P2S_ERR_INVALID_ARGUMENT = 1,
+  P2S_ERR_NUMERIC = 2,       /* Cholesky of A_0 failed after regularisation */
+  P2S_ERR_CUDA = 3,          /* launch / driver error */
+  P2S_ERR_OUT_OF_MEMORY = 4, /* device or host allocation failed */
+  P2S_ERR_UNSUPPORTED = 5    /* e.g. forced FFT grid that is not 5-smooth */
+} p2s_status;
+
+typedef struct p2s_plan_s* p2s_plan;
+
+/* Optional settings; a zero-initialised struct (or NULL) selects defaults,
+ * except `taps`, which is required (the basis is K x T x T). */
+typedef struct {
+  int    taps;              /* T: odd, 3 <= T <= 63, T/2 <= min(H,W)-1 (Q22)        */
+  double aperture_m;        /* D in metres, default 0.1                              */
+  double wavelength_m;      /* lambda, default 525e-9                                */
+  double s_per_px;          /* lag per pixel in units of D; >0 overrides L*lambda/(2 D^2) (Q5) */
+  double tilt_px_per_rad;   /* kappa_t pixels per unit a_2; >0 overrides 4/pi (Q12)  */
+  int    pad;               /* FFT grid P x Q = next 5-smooth >= pad*(H,W); default 1 (Q6) */
+  int    mlp_hidden[2];     /* hidden widths, default {100, 100}; each <= 256        */
+  int    max_batch;         /* frames per internal chunk (workspace sizing); 0 = auto */
+  float  ar_alpha;          /* AR(1) coefficient on the spectral noise in [0,1), default 0 (Q18) */
+  float  noise_sigma;       /* step 5 additive Gaussian noise sigma, default 0       */
+  int    normalize_psf_sum; /* step 5: divide by sum_k w_k sum_u h_k, default 0      */
+  int    clamp01;           /* step 5: clamp output to [0,1], default 0             */
+  int    device;            /* CUDA ordinal the plan is bound to; 0 = current device */
+} p2s_options;
+
+/* Build a plan (P:312-330 generation setup; runs once, off the per-frame clock).
+ *   H, W        image size in pixels (>= T, <= 8192)
+ *   C           channels, 1..4 (channels share field, warp and weights, Q17)
+ *   d_over_r0   D/r0 >= 0 (0 = diffraction limited: A_0 = 0, L = 0)
+ *   L_m         propagation path length in metres (> 0), sets s_px (Q5)
+ *   Z           number of Noll modes N ("we set N = 36"); 4 <= Z <= 66
+ *   K           number of PSF basis functions M; 1 <= K <= 128
+ *   basis       host float [K][T][T], h_k on the tap grid, centre tap T/2 (copied)
+ *   mlp_weights host float, packed row-major [out][in]:
+ *                 W1[h1][Z-3], b1[h1], W2[h2][h1], b2[h2], W3[K][h2], b3[K]  (copied)
+ *   opt         nullable; see p2s_options.
+ * Computes A_0 (Noll's closed form), L = chol(A_0[2..Z]) in fp64, the
+ * auto-correlation kernels c_j on the periodic lag grid, S_j = DFT(c_j) clamped
+ * at 0 and renormalised to sum S_j = PQ (Q7), sqrt(S_j), and the packed bf16
+ * tensor-core images of the MLP (with L folded into layer 1) and of the basis.
+ * Errors: INVALID_ARGUMENT, NUMERIC, CUDA, OUT_OF_MEMORY, UNSUPPORTED. */
+p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double d_over_r0, double L_m,
+                           int Z, int K, const float* basis, const float* mlp_weights,
+                           const p2s_options* opt);
+
+/* Free every device and host resource of the plan (synchronises its device). */
+p2s_status p2s_plan_destroy(p2s_plan p);
+
+/* Step 1: zern (dev float [nframes][Z][H][W]) <- a for frames frame0..frame0+nframes-1 of
+ * sequence `seed`.  Plane 0 (piston) is 0; plane j-1 holds Noll mode j.
+ * With ar_alpha != 0 the spectral noise follows eta_t = alpha eta_{t-1} +
+ * sqrt(1-alpha^2) xi_t from t = 0 (replayed on the device when frame0 does not
+ * continue the previous call). */
+p2s_status p2s_sample_zernike(p2s_plan p, uint64_t seed, int64_t frame0, int nframes,
+                              float* zern, void* stream);
+
+/* Step 2: warped (dev float [nframes][C][H][W]) <- bilinear(img, x + kappa (a_2, a_3)).
+ *   img              dev float [..][C][H][W]; frame i uses img + i*img_frame_stride
+ *                    (in floats; 0 = one image broadcast to all frames)
+ *   zern             dev float [nframes][Z][H][W] as written by p2s_sample_zernike */
+p2s_status p2s_warp(p2s_plan p, const float* img, int64_t img_frame_stride, const float* zern,
+                    float* warped, int nframes, void* stream);
+
+/* Steps 3-5: out (dev float [nframes][C][H][W]) <- step5(sum_k w_k(x) (h_k (*) warped_c)(x)),
+ * w = MLP(a_4..a_Z) from zern (dev float [nframes][Z][H][W]).  seed/frame0 key the
+ * step-5 noise (Philox stream 1). */
+p2s_status p2s_blur(p2s_plan p, const float* warped, const float* zern, uint64_t seed,
+                    int64_t frame0, float* out, int nframes, void* stream);
+
+/* Steps 1-5 fused: out (dev float [nframes][C][H][W]) for frames frame0.. of sequence seed.
+ * img as in p2s_warp.  Equivalent to sample_zernike -> warp -> blur up to rounding
+ * (L is folded into the MLP's first layer; tensor-core stages run in bf16 with
+ * fp32 accumulation). */
+p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t img_frame_stride, uint64_t seed,
+                               int64_t frame0, int nframes, float* out, void* stream);
+
+/* Same as p2s_simulate_frames with HOST buffers: img_host [..][C][H][W] (stride as above),
+ * out_host [nframes][C][H][W].  Copies in, runs, copies out, synchronises. */
+p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host, int64_t img_frame_stride,
+                                    uint64_t seed, int64_t frame0, int nframes, float* out_host,
+                                    void* stream);
+
+/* Thread-local message describing the last failure on this thread ("" if none). */
+const char* p2s_last_error(void);
+
+/* ---- introspection / test support (not on the hot path) ---- */
+
+/* FFT grid P x Q, workspace bytes for max_batch frames, max clamped-PSD fraction over modes.
+ * Any output pointer may be NULL. */
+p2s_status p2s_plan_info(p2s_plan p, int* P, int* Q, size_t* workspace_bytes,
+                         double* clamped_psd_fraction, int* max_batch);
+
+/* Copy plan tables to host (each pointer nullable):
+ *   A0    double [Z][Z]    Noll matrix (piston row/col 0)
+ *   chol  double [Z][Z]    lower-triangular L, L L^T = A0
+ *   sqrtS float  [Z-1][P][Q] sqrt(S_j) for j = 2..Z (sum S_j = P*Q) */
+p2s_status p2s_plan_export_tables(p2s_plan p, double* A0, double* chol, float* sqrtS);
+
+/* Replace the plan's sqrt(S_j) (host float [Z-1][P][Q], same layout as export). */
+p2s_status p2s_plan_import_sqrtS(p2s_plan p, const float* sqrtS);
+
+/* Device Philox4x32-10 test fill: out (dev uint32 [n][4]) <- philox(counter =
+ * (i, c1, c2, c3), key = (k0, k1)) for i = 0..n-1. */
+p2s_status p2s_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
+                           int64_t n, uint32_t* out, void* stream);
+
+/* Host-only (no GPU needed): plan tables for the given geometry, for CPU tests.
+ *   A0, chol: double [Z][Z]; sqrtS: double [Z-1][P][Q] with P, Q from p2s_grid_size;
+ *   clamped: double [Z-1] negative-PSD mass fraction per mode. Any output nullable. */
+p2s_status p2s_host_tables(int P, int Q, double s_per_px, double d_over_r0, int Z,
+                           double* A0, double* chol, double* sqrtS, double* clamped);
+
+/* Smallest 5-smooth n >= x (the FFT grid rule of p2s_plan_create). */
+int p2s_grid_size(int x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* P2S_H */

@@ -1,0 +1,7 @@
+"""B200-native DF-P2S dense-field turbulence simulator (arXiv 2210.06713).
+
+The product path is libp2s.so (include/p2s.h): hand-written sm_100a kernels for the
+five per-frame steps.  This package only binds it (p2s.py).
+"""
+from .p2s import (EXPORTS, LIB_PATH, Options, P2SError, Plan, PlanConfig, grid_size, host_tables,  # noqa: F401
+                  lib, philox_fill)

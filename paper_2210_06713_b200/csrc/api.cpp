@@ -1,0 +1,575 @@
+// api.cpp -- the C ABI of include/p2s.h: plan construction (host tables, bf16
+// tensor-core images, workspace) and the per-frame entry points that enqueue the
+// sm_100a kernels of k_fft.cu, k_warp.cu, k_mlp.cu and k_blur.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "p2s_internal.h"
+
+namespace p2s {
+
+static thread_local std::string g_err;
+
+p2s_status set_error(p2s_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+static p2s_status cuda_fail(const char* what, cudaError_t e) {
+  return set_error(e == cudaErrorMemoryAllocation ? P2S_ERR_OUT_OF_MEMORY : P2S_ERR_CUDA,
+                   std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define P2S_CUDA(call, what)                    \
+  do {                                          \
+    cudaError_t e_ = (call);                    \
+    if (e_ != cudaSuccess) return cuda_fail(what, e_); \
+  } while (0)
+
+#define P2S_LAUNCH(call, what)                                   \
+  do {                                                           \
+    int e_ = (call);                                             \
+    if (e_ != 0) return cuda_fail(what, (cudaError_t)e_);         \
+  } while (0)
+
+static inline int round16(int x) { return (x + 15) / 16 * 16; }
+
+static uint16_t host_bf16(float f) {
+  __nv_bfloat16 b = __float2bfloat16_rn(f);
+  uint16_t u;
+  std::memcpy(&u, &b, 2);
+  return u;
+}
+
+static void radix_plan(int N, AxisFFT& a) {
+  a.N = N;
+  a.nrad = 0;
+  int m = N;
+  while (m % 8 == 0) { a.rad[a.nrad++] = 8; m /= 8; }
+  while (m % 4 == 0) { a.rad[a.nrad++] = 4; m /= 4; }
+  while (m % 2 == 0) { a.rad[a.nrad++] = 2; m /= 2; }
+  while (m % 3 == 0) { a.rad[a.nrad++] = 3; m /= 3; }
+  while (m % 5 == 0) { a.rad[a.nrad++] = 5; m /= 5; }
+}
+
+static p2s_status upload_twiddles(AxisFFT& a) {
+  std::vector<float2> tw(a.N);
+  const double pi = 3.14159265358979323846;
+  for (int k = 0; k < a.N; ++k) {
+    double ang = 2.0 * pi * (double)k / a.N;  // inverse transform: e^{+2 pi i k/N}
+    tw[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+  P2S_CUDA(cudaMalloc(&a.tw, sizeof(float2) * a.N), "cudaMalloc twiddles");
+  P2S_CUDA(cudaMemcpy(a.tw, tw.data(), sizeof(float2) * a.N, cudaMemcpyHostToDevice), "copy twiddles");
+  return P2S_OK;
+}
+
+// K-major SWIZZLE_NONE image of a [rows x cols] matrix (rows padded to R, cols to Kp).
+static void kmajor_image(const std::vector<double>& Mtx, int rows, int cols, int R, int Kp, uint8_t* dst) {
+  std::memset(dst, 0, (size_t)R * Kp * 2);
+  const size_t sbo = (size_t)(Kp / 8) * 128;
+  for (int n = 0; n < rows; ++n)
+    for (int k = 0; k < cols; ++k) {
+      size_t off = (n % 8) * 16 + (n / 8) * sbo + (k / 8) * 128 + (k % 8) * 2;
+      uint16_t v = host_bf16((float)Mtx[(size_t)n * cols + k]);
+      std::memcpy(dst + off, &v, 2);
+    }
+}
+
+// Pack W1 (n_in x h1 as [h1][nin]), W2, W3 and biases into the smem image of k_mlp.
+static p2s_status build_mlp_blob(const std::vector<double>& W1, int nin, int h1, const std::vector<double>& b1,
+                                 const std::vector<double>& W2, int h2, const std::vector<double>& b2,
+                                 const std::vector<double>& W3, int K, const std::vector<double>& b3, MlpGeom& g,
+                                 uint8_t** dblob) {
+  g.nin = nin;
+  g.k1 = round16(nin);
+  g.n1 = round16(h1);
+  g.n2 = round16(h2);
+  g.n3 = round16(K);
+  g.kout = K;
+  size_t w1 = (size_t)g.n1 * g.k1 * 2, w2 = (size_t)g.n2 * g.n1 * 2, w3 = (size_t)g.n3 * g.n2 * 2;
+  g.off_w2 = w1;
+  g.off_w3 = w1 + w2;
+  g.off_b1 = w1 + w2 + w3;
+  g.off_b2 = g.off_b1 + (size_t)g.n1 * 4;
+  g.off_b3 = g.off_b2 + (size_t)g.n2 * 4;
+  g.blob_bytes = (g.off_b3 + (size_t)g.n3 * 4 + 15) / 16 * 16;
+  std::vector<uint8_t> blob(g.blob_bytes, 0);
+  kmajor_image(W1, h1, nin, g.n1, g.k1, blob.data());
+  kmajor_image(W2, h2, h1, g.n2, g.n1, blob.data() + g.off_w2);
+  kmajor_image(W3, K, h2, g.n3, g.n2, blob.data() + g.off_w3);
+  float* fb1 = reinterpret_cast<float*>(blob.data() + g.off_b1);
+  float* fb2 = reinterpret_cast<float*>(blob.data() + g.off_b2);
+  float* fb3 = reinterpret_cast<float*>(blob.data() + g.off_b3);
+  for (int i = 0; i < h1; ++i) fb1[i] = (float)b1[i];
+  for (int i = 0; i < h2; ++i) fb2[i] = (float)b2[i];
+  for (int i = 0; i < K; ++i) fb3[i] = (float)b3[i];
+  P2S_CUDA(cudaMalloc(dblob, g.blob_bytes), "cudaMalloc mlp blob");
+  P2S_CUDA(cudaMemcpy(*dblob, blob.data(), g.blob_bytes, cudaMemcpyHostToDevice), "copy mlp blob");
+  return P2S_OK;
+}
+
+// Blur K-step schedule (see k_blur.cu): groups (tx, g) of 8 tap rows, ordered by their
+// shared-memory offset (2c - tx) * SBO_src + 128 g, paired two per K-step.
+static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
+  BlurGeom& g = p->bg;
+  const int T = p->T, K = p->K;
+  g.T = T;
+  g.c = T / 2;
+  g.NC = T + 15;
+  g.RB = 32;
+  const int G = (T + 7) / 8;
+  g.RS = g.RB + 8 * G + 8;
+  g.np = round16(K);
+  const uint32_t sbo = (uint32_t)g.RS * 16;
+  struct Grp { int tx, gi; uint32_t off; };
+  std::vector<Grp> groups;
+  for (int tx = T - 1; tx >= 0; --tx)
+    for (int gi = 0; gi < G; ++gi) groups.push_back({tx, gi, (uint32_t)(2 * g.c - tx) * sbo + 128u * gi});
+  g.nks = (int)(groups.size() + 1) / 2;
+  const size_t bbytes = (size_t)g.np * 32;
+  std::vector<uint8_t> img((size_t)g.nks * bbytes, 0);
+  std::vector<uint32_t> koff(g.nks), klbo(g.nks);
+  for (int t = 0; t < g.nks; ++t) {
+    const Grp& ga = groups[2 * t];
+    const bool has_b = (size_t)(2 * t + 1) < groups.size();
+    koff[t] = ga.off;
+    klbo[t] = has_b ? groups[2 * t + 1].off - ga.off : 128u;
+    uint8_t* dst = img.data() + (size_t)t * bbytes;
+    for (int k = 0; k < 16; ++k) {
+      const bool second = k >= 8;
+      if (second && !has_b) continue;
+      const Grp& gr = second ? groups[2 * t + 1] : ga;
+      const int ty = 2 * g.c - 8 * gr.gi - (k & 7);
+      if (ty < 0 || ty >= T) continue;
+      for (int n = 0; n < K; ++n) {
+        float v = basis[((size_t)n * T + ty) * T + gr.tx];
+        uint16_t b = host_bf16(v);
+        size_t off = (n % 8) * 16 + (n / 8) * 256 + (k / 8) * 128 + (k % 8) * 2;
+        std::memcpy(dst + off, &b, 2);
+      }
+    }
+  }
+  std::vector<float> hs(g.np, 0.f);
+  for (int n = 0; n < K; ++n) {
+    double s = 0;
+    for (int i = 0; i < T * T; ++i) s += basis[(size_t)n * T * T + i];
+    hs[n] = (float)s;
+  }
+  P2S_CUDA(cudaMalloc(&g.bimg, img.size()), "cudaMalloc blur B");
+  P2S_CUDA(cudaMemcpy(g.bimg, img.data(), img.size(), cudaMemcpyHostToDevice), "copy blur B");
+  P2S_CUDA(cudaMalloc(&g.koff, sizeof(uint32_t) * g.nks), "cudaMalloc koff");
+  P2S_CUDA(cudaMemcpy(g.koff, koff.data(), sizeof(uint32_t) * g.nks, cudaMemcpyHostToDevice), "copy koff");
+  P2S_CUDA(cudaMalloc(&g.klbo, sizeof(uint32_t) * g.nks), "cudaMalloc klbo");
+  P2S_CUDA(cudaMemcpy(g.klbo, klbo.data(), sizeof(uint32_t) * g.nks, cudaMemcpyHostToDevice), "copy klbo");
+  P2S_CUDA(cudaMalloc(&g.hsum, sizeof(float) * g.np), "cudaMalloc hsum");
+  P2S_CUDA(cudaMemcpy(g.hsum, hs.data(), sizeof(float) * g.np, cudaMemcpyHostToDevice), "copy hsum");
+  return P2S_OK;
+}
+
+// Device sqrt(S) pairs scaled by sqrt(PQ/2)/PQ (noise amplitude and the 1/PQ of the IDFT).
+static p2s_status upload_sqrtS(p2s_plan_s* p) {
+  const size_t PQ = (size_t)p->P * p->Q;
+  std::vector<float2> dev(PQ * p->npairs);
+  const double sc = 1.0 / std::sqrt(2.0 * (double)PQ);
+  for (int pr = 0; pr < p->npairs; ++pr)
+    for (size_t k = 0; k < PQ; ++k) {
+      int sa = 2 * pr, sb = 2 * pr + 1;
+      float a = (float)(p->sqrtS_host[(size_t)sa * PQ + k] * sc);
+      float b = sb < p->nslots ? (float)(p->sqrtS_host[(size_t)sb * PQ + k] * sc) : 0.f;
+      dev[(size_t)pr * PQ + k] = make_float2(a, b);
+    }
+  if (!p->d_sqrtS) P2S_CUDA(cudaMalloc(&p->d_sqrtS, sizeof(float2) * dev.size()), "cudaMalloc sqrtS");
+  P2S_CUDA(cudaMemcpy(p->d_sqrtS, dev.data(), sizeof(float2) * dev.size(), cudaMemcpyHostToDevice), "copy sqrtS");
+  return P2S_OK;
+}
+
+static size_t frame_bytes(const p2s_plan_s* p) {
+  const size_t HW = (size_t)p->H * p->W, PQ = (size_t)p->P * p->Q;
+  size_t b = 0;
+  b += PQ * p->npairs * sizeof(float2);
+  b += HW * (size_t)std::max(p->nslots, p->Z - 3) * 2;
+  b += 2 * HW * 4;
+  b += (size_t)p->C * HW * 2;
+  b += HW * (size_t)p->mg_fold.n3 * 2;
+  b += 2 * (size_t)p->C * HW * 4;
+  return b + 5 * 256;
+}
+
+static p2s_status alloc_workspace(p2s_plan_s* p) {
+  const size_t HW = (size_t)p->H * p->W, PQ = (size_t)p->P * p->Q, mb = p->max_batch;
+  p->ws_bytes = frame_bytes(p) * mb;
+  P2S_CUDA(cudaMalloc(&p->d_ws, p->ws_bytes), "cudaMalloc workspace");
+  uint8_t* c = reinterpret_cast<uint8_t*>(p->d_ws);
+  auto take = [&](size_t bytes) {
+    uint8_t* r = c;
+    c += (bytes + 255) / 256 * 256;
+    return r;
+  };
+  p->d_Z = reinterpret_cast<float2*>(take(mb * PQ * p->npairs * sizeof(float2)));
+  p->d_X = reinterpret_cast<uint16_t*>(take(mb * HW * (size_t)std::max(p->nslots, p->Z - 3) * 2));
+  p->d_tilt = reinterpret_cast<float*>(take(mb * 2 * HW * 4));
+  p->d_Iw = reinterpret_cast<uint16_t*>(take(mb * (size_t)p->C * HW * 2));
+  p->d_w = reinterpret_cast<uint16_t*>(take(mb * HW * (size_t)p->mg_fold.n3 * 2));
+  p->d_img = reinterpret_cast<float*>(take(mb * (size_t)p->C * HW * 4));
+  p->d_out = reinterpret_cast<float*>(take(mb * (size_t)p->C * HW * 4));
+  return P2S_OK;
+}
+
+static void free_plan(p2s_plan_s* p) {
+  if (!p) return;
+  cudaFree(p->d_sqrtS);
+  cudaFree(p->d_ar);
+  cudaFree(p->d_L);
+  cudaFree(p->d_mlp_fold);
+  cudaFree(p->d_mlp_plain);
+  cudaFree(p->bg.bimg);
+  cudaFree(p->bg.koff);
+  cudaFree(p->bg.klbo);
+  cudaFree(p->bg.hsum);
+  cudaFree(p->fq.tw);
+  cudaFree(p->fp.tw);
+  cudaFree(p->d_ws);
+  delete p;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// AR(1) bookkeeping: 0 = continue from the stored state, 1 = fresh start at frame 0,
+// 2 = replay frames 0..frame0-1 into the state first.
+static int ar_mode_for(p2s_plan_s* p, uint64_t seed, int64_t frame0) {
+  if (p->ar_valid && p->ar_seed == seed && p->ar_next == frame0) return 0;
+  return frame0 == 0 ? 1 : 2;
+}
+
+static p2s_status run_step1(p2s_plan_s* p, uint64_t seed, int64_t f0, int F, cudaStream_t s) {
+  const bool ar = p->ar_alpha != 0.f;
+  int mode = ar ? ar_mode_for(p, seed, f0) : 1;
+  P2S_LAUNCH(launch_rows(p, seed, f0, F, ar, mode, mode == 2 ? 0 : f0, s), "k_rows");
+  if (ar) {
+    p->ar_valid = true;
+    p->ar_seed = seed;
+    p->ar_next = f0 + F;
+  }
+  return P2S_OK;
+}
+
+}  // namespace p2s
+
+using namespace p2s;
+
+extern "C" const char* p2s_last_error(void) { return g_err.c_str(); }
+
+extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double d_over_r0, double L_m, int Z, int K,
+                                      const float* basis, const float* mlp_weights, const p2s_options* opt) {
+  g_err.clear();
+  if (!out) return set_error(P2S_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  p2s_options o;
+  std::memset(&o, 0, sizeof(o));
+  if (opt) o = *opt;
+  const int T = o.taps;
+  if (T < 3 || T > 63 || T % 2 == 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "taps must be odd in [3, 63]");
+  if (H < T || W < T || H > 8192 || W > 8192) return set_error(P2S_ERR_INVALID_ARGUMENT, "H, W must be in [T, 8192]");
+  if (T / 2 > std::min(H, W) - 1) return set_error(P2S_ERR_INVALID_ARGUMENT, "T/2 must be <= min(H,W)-1");
+  if (C < 1 || C > 4) return set_error(P2S_ERR_INVALID_ARGUMENT, "C must be in [1, 4]");
+  if (!(d_over_r0 >= 0) || !std::isfinite(d_over_r0)) return set_error(P2S_ERR_INVALID_ARGUMENT, "D/r0 must be >= 0");
+  if (!(L_m > 0) || !std::isfinite(L_m)) return set_error(P2S_ERR_INVALID_ARGUMENT, "L must be > 0");
+  if (Z < 4 || Z > 66) return set_error(P2S_ERR_INVALID_ARGUMENT, "Z must be in [4, 66]");
+  if (K < 1 || K > 128) return set_error(P2S_ERR_INVALID_ARGUMENT, "K must be in [1, 128]");
+  if (!basis || !mlp_weights) return set_error(P2S_ERR_INVALID_ARGUMENT, "basis / mlp_weights is NULL");
+  const int h1 = o.mlp_hidden[0] > 0 ? o.mlp_hidden[0] : 100;
+  const int h2 = o.mlp_hidden[1] > 0 ? o.mlp_hidden[1] : 100;
+  if (h1 > 256 || h2 > 256) return set_error(P2S_ERR_INVALID_ARGUMENT, "mlp_hidden must be <= 256");
+  if (!(o.ar_alpha >= 0.f && o.ar_alpha < 1.f)) return set_error(P2S_ERR_INVALID_ARGUMENT, "ar_alpha in [0,1)");
+  const double D = o.aperture_m > 0 ? o.aperture_m : 0.1;
+  const double lam = o.wavelength_m > 0 ? o.wavelength_m : 525e-9;
+  const int pad = o.pad > 0 ? o.pad : 1;
+  if (o.device < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "device must be >= 0");
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  if (o.device > 0) dev = o.device;  // 0 selects the calling thread's current device
+
+  p2s_plan_s* p = new (std::nothrow) p2s_plan_s();
+  if (!p) return set_error(P2S_ERR_OUT_OF_MEMORY, "host allocation failed");
+  p->H = H; p->W = W; p->C = C; p->Z = Z; p->K = K; p->T = T;
+  p->h1 = h1; p->h2 = h2;
+  p->d_over_r0 = d_over_r0; p->L_m = L_m;
+  p->s_px = o.s_per_px > 0 ? o.s_per_px : L_m * (lam / (2.0 * D)) / D;
+  p->kappa = o.tilt_px_per_rad > 0 ? o.tilt_px_per_rad : 4.0 / 3.14159265358979323846;
+  p->ar_alpha = o.ar_alpha;
+  p->noise_sigma = o.noise_sigma;
+  p->normalize = o.normalize_psf_sum;
+  p->clamp01 = o.clamp01;
+  p->device = dev;
+  p->P = grid_size(pad * H);
+  p->Q = grid_size(pad * W);
+  if (p->P > 4096 || p->Q > 4096) {
+    delete p;
+    return set_error(P2S_ERR_UNSUPPORTED, "FFT grid larger than 4096 per axis");
+  }
+  p->nslots = Z - 1;
+  p->npairs = (p->nslots + 1) / 2;
+
+  DeviceGuard guard(dev);
+  p2s_status st;
+#define P2S_TRY(expr)              \
+  do {                             \
+    st = (expr);                   \
+    if (st != P2S_OK) {            \
+      free_plan(p);                \
+      return st;                   \
+    }                              \
+  } while (0)
+  {
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) {
+      delete p;
+      return cuda_fail("cudaGetDeviceProperties", e);
+    }
+    p->num_sms = prop.multiProcessorCount;
+    if (prop.major < 10) {
+      delete p;
+      return set_error(P2S_ERR_UNSUPPORTED, "requires an sm_100a (Blackwell B200) device");
+    }
+  }
+  // ---- step-1 tables (host fp64)
+  noll_matrix(Z, d_over_r0, p->A0);
+  if (!noll_cholesky(Z, p->A0, p->Lc)) {
+    delete p;
+    return set_error(P2S_ERR_NUMERIC, "Cholesky of the Noll matrix failed after regularisation");
+  }
+  {
+    std::vector<double> sq, cl;
+    psd_tables(p->P, p->Q, p->s_px, Z, sq, cl);
+    p->sqrtS_host.assign(sq.begin(), sq.end());
+    p->clamped_max = *std::max_element(cl.begin(), cl.end());
+  }
+  P2S_TRY(upload_sqrtS(p));
+  radix_plan(p->Q, p->fq);
+  radix_plan(p->P, p->fp);
+  P2S_TRY(upload_twiddles(p->fq));
+  P2S_TRY(upload_twiddles(p->fp));
+  {
+    const int n = Z - 1;
+    std::vector<float> Lf((size_t)n * n);
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < n; ++k) Lf[(size_t)i * n + k] = (float)p->Lc[(size_t)(i + 1) * Z + (k + 1)];
+    cudaError_t e = cudaMalloc(&p->d_L, sizeof(float) * Lf.size());
+    if (e == cudaSuccess) e = cudaMemcpy(p->d_L, Lf.data(), sizeof(float) * Lf.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      free_plan(p);
+      return cuda_fail("upload L", e);
+    }
+  }
+  // ---- P2S MLP (steps 3): plain (inputs a_4..a_Z) and folded (inputs f_2..f_Z, W1' = W1 L)
+  {
+    const int nin = Z - 3;
+    const size_t need = (size_t)h1 * nin + h1 + (size_t)h2 * h1 + h2 + (size_t)K * h2 + K;
+    p->mlp_host.assign(mlp_weights, mlp_weights + need);
+    const float* q = mlp_weights;
+    std::vector<double> W1(q, q + (size_t)h1 * nin); q += (size_t)h1 * nin;
+    std::vector<double> b1(q, q + h1); q += h1;
+    std::vector<double> W2(q, q + (size_t)h2 * h1); q += (size_t)h2 * h1;
+    std::vector<double> b2(q, q + h2); q += h2;
+    std::vector<double> W3(q, q + (size_t)K * h2); q += (size_t)K * h2;
+    std::vector<double> b3(q, q + K);
+    P2S_TRY(build_mlp_blob(W1, nin, h1, b1, W2, h2, b2, W3, K, b3, p->mg_plain, &p->d_mlp_plain));
+    const int nf = Z - 1;
+    std::vector<double> W1f((size_t)h1 * nf, 0.0);
+    for (int h = 0; h < h1; ++h)
+      for (int s = 0; s < nf; ++s) {
+        double acc = 0;
+        for (int r = 0; r < nin; ++r) acc += W1[(size_t)h * nin + r] * p->Lc[(size_t)(r + 3) * Z + (s + 1)];
+        W1f[(size_t)h * nf + s] = acc;
+      }
+    P2S_TRY(build_mlp_blob(W1f, nf, h1, b1, W2, h2, b2, W3, K, b3, p->mg_fold, &p->d_mlp_fold));
+  }
+  // ---- basis (step 4)
+  p->basis_host.assign(basis, basis + (size_t)K * T * T);
+  P2S_TRY(build_blur(p, basis));
+  // ---- workspace
+  {
+    size_t fb = frame_bytes(p);
+    int mb = o.max_batch > 0 ? o.max_batch : (int)std::min<size_t>(64, std::max<size_t>(1, ((size_t)12 << 30) / fb));
+    p->max_batch = mb;
+  }
+  P2S_TRY(alloc_workspace(p));
+  if (p->ar_alpha != 0.f) {
+    cudaError_t e = cudaMalloc(&p->d_ar, sizeof(float4) * (size_t)p->npairs * p->P * p->Q);
+    if (e != cudaSuccess) {
+      free_plan(p);
+      return cuda_fail("cudaMalloc AR state", e);
+    }
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    free_plan(p);
+    return cuda_fail("plan create", e);
+  }
+  *out = p;
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_plan_destroy(p2s_plan p) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  DeviceGuard guard(p->device);
+  cudaDeviceSynchronize();
+  free_plan(p);
+  return P2S_OK;
+}
+
+#define CHECK_PLAN()                                                         \
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");       \
+  if (nframes < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "nframes < 0"); \
+  if (frame0 < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "frame0 < 0");
+
+extern "C" p2s_status p2s_sample_zernike(p2s_plan p, uint64_t seed, int64_t frame0, int nframes, float* zern,
+                                         void* stream) {
+  CHECK_PLAN();
+  if (nframes == 0) return P2S_OK;
+  if (!zern) return set_error(P2S_ERR_INVALID_ARGUMENT, "zern is NULL");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t per = (size_t)p->Z * p->H * p->W;
+  for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
+    const int F = std::min(p->max_batch, nframes - i0);
+    p2s_status st = run_step1(p, seed, frame0 + i0, F, s);
+    if (st != P2S_OK) return st;
+    P2S_LAUNCH(launch_cols(p, F, 0, zern + per * i0, s), "k_cols");
+    P2S_LAUNCH(launch_mix(p, F, zern + per * i0, s), "k_mix");
+  }
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_warp(p2s_plan p, const float* img, int64_t img_frame_stride, const float* zern,
+                               float* warped, int nframes, void* stream) {
+  const int64_t frame0 = 0;
+  CHECK_PLAN();
+  if (nframes == 0) return P2S_OK;
+  if (!img || !zern || !warped) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (img_frame_stride < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "img_frame_stride < 0");
+  if (nframes > 65535) return set_error(P2S_ERR_INVALID_ARGUMENT, "nframes > 65535 per call");
+  DeviceGuard guard(p->device);
+  P2S_LAUNCH(launch_warp_f32(p, nframes, img, img_frame_stride, zern, warped, (cudaStream_t)stream), "k_warp");
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_blur(p2s_plan p, const float* warped, const float* zern, uint64_t seed, int64_t frame0,
+                               float* out, int nframes, void* stream) {
+  CHECK_PLAN();
+  if (nframes == 0) return P2S_OK;
+  if (!warped || !zern || !out) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t HW = (size_t)p->H * p->W;
+  for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
+    const int F = std::min(p->max_batch, nframes - i0);
+    P2S_LAUNCH(launch_zern_to_x(p, F, zern + (size_t)i0 * p->Z * HW, s), "k_zern_to_x");
+    P2S_LAUNCH(launch_mlp(p, F, false, s), "k_mlp");
+    P2S_LAUNCH(launch_blur(p, F, warped + (size_t)i0 * p->C * HW, true, seed, frame0 + i0,
+                           out + (size_t)i0 * p->C * HW, s),
+               "k_blur");
+  }
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t img_frame_stride, uint64_t seed,
+                                          int64_t frame0, int nframes, float* out, void* stream) {
+  CHECK_PLAN();
+  if (nframes == 0) return P2S_OK;
+  if (!img || !out) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (img_frame_stride < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "img_frame_stride < 0");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t HW = (size_t)p->H * p->W;
+  for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
+    const int F = std::min(p->max_batch, nframes - i0);
+    p2s_status st = run_step1(p, seed, frame0 + i0, F, s);
+    if (st != P2S_OK) return st;
+    P2S_LAUNCH(launch_cols(p, F, 1, nullptr, s), "k_cols");
+    P2S_LAUNCH(launch_warp_sim(p, F, img + (size_t)i0 * img_frame_stride, img_frame_stride, s), "k_warp");
+    P2S_LAUNCH(launch_mlp(p, F, true, s), "k_mlp");
+    P2S_LAUNCH(launch_blur(p, F, p->d_Iw, false, seed, frame0 + i0, out + (size_t)i0 * p->C * HW, s), "k_blur");
+  }
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host, int64_t img_frame_stride,
+                                               uint64_t seed, int64_t frame0, int nframes, float* out_host,
+                                               void* stream) {
+  CHECK_PLAN();
+  if (nframes == 0) return P2S_OK;
+  if (!img_host || !out_host) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (img_frame_stride < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "img_frame_stride < 0");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t img_floats = (size_t)p->C * p->H * p->W;
+  for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
+    const int F = std::min(p->max_batch, nframes - i0);
+    if (img_frame_stride == 0) {
+      P2S_CUDA(cudaMemcpyAsync(p->d_img, img_host, img_floats * 4, cudaMemcpyHostToDevice, s), "H2D img");
+    } else {
+      for (int i = 0; i < F; ++i)
+        P2S_CUDA(cudaMemcpyAsync(p->d_img + i * img_floats, img_host + (size_t)(i0 + i) * img_frame_stride,
+                                 img_floats * 4, cudaMemcpyHostToDevice, s),
+                 "H2D img");
+    }
+    p2s_status st = p2s_simulate_frames(p, p->d_img, img_frame_stride ? (int64_t)img_floats : 0, seed,
+                                        frame0 + i0, F, p->d_out, stream);
+    if (st != P2S_OK) return st;
+    P2S_CUDA(cudaMemcpyAsync(out_host + (size_t)i0 * img_floats, p->d_out, (size_t)F * img_floats * 4,
+                             cudaMemcpyDeviceToHost, s),
+             "D2H out");
+  }
+  P2S_CUDA(cudaStreamSynchronize(s), "stream sync");
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_plan_info(p2s_plan p, int* P, int* Q, size_t* ws, double* clamped, int* max_batch) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (P) *P = p->P;
+  if (Q) *Q = p->Q;
+  if (ws) *ws = p->ws_bytes;
+  if (clamped) *clamped = p->clamped_max;
+  if (max_batch) *max_batch = p->max_batch;
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_plan_export_tables(p2s_plan p, double* A0, double* chol, float* sqrtS) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (A0) std::memcpy(A0, p->A0.data(), sizeof(double) * p->A0.size());
+  if (chol) std::memcpy(chol, p->Lc.data(), sizeof(double) * p->Lc.size());
+  if (sqrtS) std::memcpy(sqrtS, p->sqrtS_host.data(), sizeof(float) * p->sqrtS_host.size());
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_plan_import_sqrtS(p2s_plan p, const float* sqrtS) {
+  if (!p || !sqrtS) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard guard(p->device);
+  std::memcpy(p->sqrtS_host.data(), sqrtS, sizeof(float) * p->sqrtS_host.size());
+  return upload_sqrtS(p);
+}
+
+extern "C" p2s_status p2s_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int64_t n,
+                                      uint32_t* out, void* stream) {
+  if (n < 0 || (n > 0 && !out)) return set_error(P2S_ERR_INVALID_ARGUMENT, "bad argument");
+  P2S_LAUNCH(launch_philox_fill(c1, c2, c3, k0, k1, n, out, (cudaStream_t)stream), "k_philox_fill");
+  return P2S_OK;
+}

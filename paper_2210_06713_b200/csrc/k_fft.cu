@@ -1,0 +1,404 @@
+// k_fft.cu -- step 1 of DF-P2S on the GPU: Fourier sampling of the Zernike fields.
+//
+// Paper: homogeneous auto-covariance slices are circulant, so y = F^{-1}(S^{1/2} F(e))
+// (P:234-238); N unit-variance fields are drawn this way and mixed point-wise
+// with L, L L^T = A_0 (Eq.10).  Two real fields per complex inverse DFT with
+// Hermitian spectral noise per mode (reading Q8):
+//     Y_p[k] = sqrt(S_a[k]) eta_a[k] + i sqrt(S_b[k]) eta_b[k],  f_a = Re y, f_b = Im y.
+//
+// K1  k_rows : Philox noise + PSD filter (+ AR(1)) fused into the row inverse
+//              DFT (shared-memory Stockham, radix 8/4/2/3/5); the spectrum is never
+//              written.  One CTA per (spectral row, mode pair); the CTA loops over the
+//              frame batch so its sqrt(S) row is read from HBM once per batch.
+// K2  k_cols : column inverse DFT of TC interleaved columns, Re/Im split, crop to H x W;
+//              writes fp32 Zernike planes (API) or bf16 MLP inputs + fp32 tilt planes
+//              (fused simulate path).
+// K3  k_mix  : a = L f per pixel (API p2s_sample_zernike only; simulate folds L into
+//              the MLP's first layer and the warp coefficients).
+#include "p2s_dev.cuh"
+#include "p2s_internal.h"
+
+namespace p2s {
+
+// ------------------------------------------------------------------ small inverse DFTs
+template <int R>
+__device__ __forceinline__ void dft_inv(float2* v);
+
+template <>
+__device__ __forceinline__ void dft_inv<2>(float2* v) {
+  float2 a = v[0], b = v[1];
+  v[0] = make_float2(a.x + b.x, a.y + b.y);
+  v[1] = make_float2(a.x - b.x, a.y - b.y);
+}
+template <>
+__device__ __forceinline__ void dft_inv<4>(float2* v) {
+  float2 a = v[0], b = v[1], c = v[2], d = v[3];
+  float2 s0 = make_float2(a.x + c.x, a.y + c.y), s1 = make_float2(a.x - c.x, a.y - c.y);
+  float2 s2 = make_float2(b.x + d.x, b.y + d.y), s3 = make_float2(b.x - d.x, b.y - d.y);
+  v[0] = make_float2(s0.x + s2.x, s0.y + s2.y);
+  v[2] = make_float2(s0.x - s2.x, s0.y - s2.y);
+  // a + i b - c - i d = s1 + i s3
+  v[1] = make_float2(s1.x - s3.y, s1.y + s3.x);
+  v[3] = make_float2(s1.x + s3.y, s1.y - s3.x);
+}
+template <>
+__device__ __forceinline__ void dft_inv<8>(float2* v) {
+  float2 e[4] = {v[0], v[2], v[4], v[6]};
+  float2 o[4] = {v[1], v[3], v[5], v[7]};
+  dft_inv<4>(e);
+  dft_inv<4>(o);
+  const float r = 0.70710678118654752f;
+  float2 w1 = make_float2(r * (o[1].x - o[1].y), r * (o[1].x + o[1].y));  // (1+i)/sqrt2 * o1
+  float2 w2 = make_float2(-o[2].y, o[2].x);                              // i * o2
+  float2 w3 = make_float2(-r * (o[3].x + o[3].y), r * (o[3].x - o[3].y)); // (-1+i)/sqrt2 * o3
+  v[0] = make_float2(e[0].x + o[0].x, e[0].y + o[0].y);
+  v[4] = make_float2(e[0].x - o[0].x, e[0].y - o[0].y);
+  v[1] = make_float2(e[1].x + w1.x, e[1].y + w1.y);
+  v[5] = make_float2(e[1].x - w1.x, e[1].y - w1.y);
+  v[2] = make_float2(e[2].x + w2.x, e[2].y + w2.y);
+  v[6] = make_float2(e[2].x - w2.x, e[2].y - w2.y);
+  v[3] = make_float2(e[3].x + w3.x, e[3].y + w3.y);
+  v[7] = make_float2(e[3].x - w3.x, e[3].y - w3.y);
+}
+template <>
+__device__ __forceinline__ void dft_inv<3>(float2* v) {
+  const float h = 0.86602540378443865f;
+  float2 t = make_float2(v[1].x + v[2].x, v[1].y + v[2].y);
+  float2 a = make_float2(v[0].x - 0.5f * t.x, v[0].y - 0.5f * t.y);
+  float2 b = make_float2(h * (v[1].x - v[2].x), h * (v[1].y - v[2].y));
+  v[0] = make_float2(v[0].x + t.x, v[0].y + t.y);
+  v[1] = make_float2(a.x - b.y, a.y + b.x);
+  v[2] = make_float2(a.x + b.y, a.y - b.x);
+}
+template <>
+__device__ __forceinline__ void dft_inv<5>(float2* v) {
+  const float c1 = 0.30901699437494742f, c2 = -0.80901699437494742f;
+  const float s1 = 0.95105651629515357f, s2 = 0.58778525229247313f;
+  float2 t1 = make_float2(v[1].x + v[4].x, v[1].y + v[4].y);
+  float2 t2 = make_float2(v[2].x + v[3].x, v[2].y + v[3].y);
+  float2 t3 = make_float2(v[1].x - v[4].x, v[1].y - v[4].y);
+  float2 t4 = make_float2(v[2].x - v[3].x, v[2].y - v[3].y);
+  float2 a1 = make_float2(v[0].x + c1 * t1.x + c2 * t2.x, v[0].y + c1 * t1.y + c2 * t2.y);
+  float2 a2 = make_float2(v[0].x + c2 * t1.x + c1 * t2.x, v[0].y + c2 * t1.y + c1 * t2.y);
+  float2 b1 = make_float2(s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y);
+  float2 b2 = make_float2(s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y);
+  v[0] = make_float2(v[0].x + t1.x + t2.x, v[0].y + t1.y + t2.y);
+  v[1] = make_float2(a1.x - b1.y, a1.y + b1.x);
+  v[4] = make_float2(a1.x + b1.y, a1.y - b1.x);
+  v[2] = make_float2(a2.x - b2.y, a2.y + b2.x);
+  v[3] = make_float2(a2.x + b2.y, a2.y - b2.x);
+}
+
+// One Stockham pass of radix R over TC interleaved sequences of length N:
+// element i of sequence c lives at x[i*TC + c].  Ns = product of earlier radices.
+template <int R>
+__device__ __forceinline__ void stockham_pass(const float2* __restrict__ x, float2* __restrict__ y, int N, int Ns,
+                                              int tc_log2, const float2* __restrict__ tw) {
+  const int NR = N / R;
+  const int TC = 1 << tc_log2;
+  const int total = NR << tc_log2;
+  const int ts = N / (Ns * R);
+  for (int w = threadIdx.x; w < total; w += blockDim.x) {
+    const int c = w & (TC - 1);
+    const int j = w >> tc_log2;
+    const int k = j % Ns;
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = x[((j + r * NR) << tc_log2) + c];
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * k * ts]));
+    }
+    dft_inv<R>(v);
+    const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int q = 0; q < R; ++q) y[((base + q * Ns) << tc_log2) + c] = v[q];
+  }
+}
+
+struct FFTArgs {
+  int N;
+  int nrad;
+  int rad[kMaxRadix];
+  const float2* tw;
+};
+
+// Inverse DFT (e^{+2 pi i}, unnormalised) in shared memory; returns the buffer holding the result.
+__device__ float2* smem_ifft(float2* a, float2* b, const FFTArgs& f, int tc_log2) {
+  int Ns = 1;
+  for (int ip = 0; ip < f.nrad; ++ip) {
+    const int R = f.rad[ip];
+    switch (R) {
+      case 8: stockham_pass<8>(a, b, f.N, Ns, tc_log2, f.tw); break;
+      case 4: stockham_pass<4>(a, b, f.N, Ns, tc_log2, f.tw); break;
+      case 2: stockham_pass<2>(a, b, f.N, Ns, tc_log2, f.tw); break;
+      case 3: stockham_pass<3>(a, b, f.N, Ns, tc_log2, f.tw); break;
+      default: stockham_pass<5>(a, b, f.N, Ns, tc_log2, f.tw); break;
+    }
+    __syncthreads();
+    float2* t = a;
+    a = b;
+    b = t;
+    Ns *= R;
+  }
+  return a;
+}
+
+// ------------------------------------------------------------------ K1: noise + PSD + row IDFT
+struct RowArgs {
+  FFTArgs fq;
+  const float2* sqrtS;  // [npairs][P][Q] scaled amplitudes (sa, sb)
+  float4* ar;           // [npairs][P][Q] AR state (zeta_a, zeta_b), or null
+  float2* Zout;         // [F][npairs][P][Q]
+  int P, Q, npairs;
+  uint32_t k0, k1;
+  int64_t frame0;
+  int F;
+  float alpha, calpha;
+  int64_t t_start;      // first frame evolved (AR replay starts at 0)
+  int load_state;       // AR: state holds eta_{frame0-1}
+};
+
+// Unit-variance Hermitian noise zeta (eta / sqrt(PQ/2)) for both modes of pair p at bin (ky, kx).
+__device__ __forceinline__ float4 spectral_noise(int ky, int kx, int P, int Q, int p, int64_t frame, uint32_t k0,
+                                                 uint32_t k1) {
+  const uint32_t lin = (uint32_t)ky * Q + kx;
+  const int kym = ky ? P - ky : 0, kxm = kx ? Q - kx : 0;
+  const uint32_t linm = (uint32_t)kym * Q + kxm;
+  const uint32_t canon = lin < linm ? lin : linm;
+  uint4 x = philox4x32_10(make_uint4(canon, (uint32_t)p, (uint32_t)frame, (uint32_t)((uint64_t)frame >> 32)), k0, k1);
+  float2 ga = box_muller(x.x, x.y), gb = box_muller(x.z, x.w);
+  if (lin == linm) {  // self-conjugate: sqrt(PQ) g1 = sqrt(2) sqrt(PQ/2) g1
+    const float r2 = 1.41421356237309515f;
+    return make_float4(r2 * ga.x, 0.f, r2 * gb.x, 0.f);
+  }
+  const float sg = (lin == canon) ? 1.f : -1.f;
+  return make_float4(ga.x, sg * ga.y, gb.x, sg * gb.y);
+}
+
+template <bool AR>
+__global__ void __launch_bounds__(256) k_rows(RowArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int Q = a.Q;
+  float2* sS = reinterpret_cast<float2*>(smem);
+  float2* b0 = sS + Q;
+  float2* b1 = b0 + Q;
+  float4* st = reinterpret_cast<float4*>(b1 + Q);  // AR state (AR only)
+  const int ky = blockIdx.x, p = blockIdx.y;
+  const size_t row = ((size_t)p * a.P + ky) * Q;
+  for (int kx = threadIdx.x; kx < Q; kx += blockDim.x) {
+    sS[kx] = a.sqrtS[row + kx];
+    if (AR && a.load_state) st[kx] = a.ar[row + kx];
+  }
+  __syncthreads();
+  const int64_t t_end = a.frame0 + a.F;
+  for (int64_t t = AR ? a.t_start : a.frame0; t < t_end; ++t) {
+    const bool out = t >= a.frame0;
+    for (int kx = threadIdx.x; kx < Q; kx += blockDim.x) {
+      float4 z = spectral_noise(ky, kx, a.P, Q, p, t, a.k0, a.k1);
+      if (AR) {
+        if (t > 0) {
+          float4 o = st[kx];
+          z = make_float4(a.alpha * o.x + a.calpha * z.x, a.alpha * o.y + a.calpha * z.y,
+                          a.alpha * o.z + a.calpha * z.z, a.alpha * o.w + a.calpha * z.w);
+        }
+        st[kx] = z;
+      }
+      if (out) {
+        const float2 s = sS[kx];
+        // Y = sa zeta_a + i sb zeta_b
+        b0[kx] = make_float2(s.x * z.x - s.y * z.w, s.x * z.y + s.y * z.z);
+      }
+    }
+    if (!out) continue;  // AR replay: no transform
+    __syncthreads();
+    float2* res = smem_ifft(b0, b1, a.fq, 0);
+    float2* dst = a.Zout + (size_t)(t - a.frame0) * a.npairs * a.P * Q + row;
+    for (int x = threadIdx.x; x < Q; x += blockDim.x) dst[x] = res[x];
+    __syncthreads();  // b0/b1 are free again; the next spectrum goes to b0
+  }
+  if (AR) {
+    __syncthreads();
+    for (int kx = threadIdx.x; kx < Q; kx += blockDim.x) a.ar[row + kx] = st[kx];
+  }
+}
+
+int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool ar, int ar_mode,
+                int64_t replay_from, cudaStream_t s) {
+  RowArgs a;
+  a.fq.N = pl->fq.N;
+  a.fq.nrad = pl->fq.nrad;
+  for (int i = 0; i < kMaxRadix; ++i) a.fq.rad[i] = pl->fq.rad[i];
+  a.fq.tw = pl->fq.tw;
+  a.sqrtS = pl->d_sqrtS;
+  a.ar = pl->d_ar;
+  a.Zout = pl->d_Z;
+  a.P = pl->P;
+  a.Q = pl->Q;
+  a.npairs = pl->npairs;
+  a.k0 = (uint32_t)seed;
+  a.k1 = (uint32_t)(seed >> 32);
+  a.frame0 = frame0;
+  a.F = F;
+  a.alpha = pl->ar_alpha;
+  a.calpha = sqrtf(1.0f - pl->ar_alpha * pl->ar_alpha);
+  a.t_start = ar ? replay_from : frame0;
+  a.load_state = (ar && ar_mode == 0) ? 1 : 0;
+  dim3 grid(pl->P, pl->npairs);
+  const int nthr = pl->Q >= 1024 ? 256 : 128;
+  if (ar) {
+    size_t sm = (size_t)pl->Q * (3 * sizeof(float2) + sizeof(float4));
+    cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_rows<true><<<grid, nthr, sm, s>>>(a);
+  } else {
+    size_t sm = (size_t)pl->Q * 3 * sizeof(float2);
+    cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_rows<false><<<grid, nthr, sm, s>>>(a);
+  }
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K2: column IDFT
+struct ColArgs {
+  FFTArgs fp;
+  const float2* Zin;  // [F][npairs][P][Q]
+  int P, Q, H, W, npairs, nslots, Z;
+  int tc_log2;
+  float* zern;        // mode 0: [F][Z][H][W]
+  uint16_t* X;        // mode 1: bf16 [F][nslots][H*W]
+  float* tilt;        // mode 1: [F][2][H*W]
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_cols(ColArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int TC = 1 << a.tc_log2;
+  float2* b0 = reinterpret_cast<float2*>(smem);
+  float2* b1 = b0 + (size_t)a.P * TC;
+  const int x0 = blockIdx.x * TC, p = blockIdx.y, f = blockIdx.z;
+  const float2* src = a.Zin + ((size_t)f * a.npairs + p) * a.P * a.Q;
+  const int n = a.P << a.tc_log2;
+  for (int w = threadIdx.x; w < n; w += blockDim.x) {
+    const int c = w & (TC - 1), ky = w >> a.tc_log2;
+    const int x = x0 + c;
+    b0[w] = (x < a.Q) ? src[(size_t)ky * a.Q + x] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  const float2* res = smem_ifft(b0, b1, a.fp, a.tc_log2);
+  const int sa = 2 * p, sb = 2 * p + 1;
+  const size_t HW = (size_t)a.H * a.W;
+  const int m = a.H << a.tc_log2;
+  for (int w = threadIdx.x; w < m; w += blockDim.x) {
+    const int c = w & (TC - 1), yy = w >> a.tc_log2;
+    const int x = x0 + c;
+    if (x >= a.W) continue;
+    const float2 v = res[w];
+    const size_t pix = (size_t)yy * a.W + x;
+    if (MODE == 0) {
+      float* z = a.zern + (size_t)f * a.Z * HW;
+      z[(size_t)(sa + 1) * HW + pix] = v.x;
+      if (sb < a.nslots) z[(size_t)(sb + 1) * HW + pix] = v.y;
+    } else {
+      uint16_t* X = a.X + (size_t)f * a.nslots * HW;
+      X[(size_t)sa * HW + pix] = f_to_bf16(v.x);
+      if (sb < a.nslots) X[(size_t)sb * HW + pix] = f_to_bf16(v.y);
+      if (p == 0) {
+        float* t = a.tilt + (size_t)f * 2 * HW;
+        t[pix] = v.x;
+        t[HW + pix] = v.y;
+      }
+    }
+  }
+}
+
+int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t s) {
+  ColArgs a;
+  a.fp.N = pl->fp.N;
+  a.fp.nrad = pl->fp.nrad;
+  for (int i = 0; i < kMaxRadix; ++i) a.fp.rad[i] = pl->fp.rad[i];
+  a.fp.tw = pl->fp.tw;
+  a.Zin = pl->d_Z;
+  a.P = pl->P;
+  a.Q = pl->Q;
+  a.H = pl->H;
+  a.W = pl->W;
+  a.npairs = pl->npairs;
+  a.nslots = pl->nslots;
+  a.Z = pl->Z;
+  int tcl = 4;
+  while (tcl > 0 && (size_t)16 * pl->P * (1 << tcl) > 160 * 1024) --tcl;
+  a.tc_log2 = tcl;
+  a.zern = zern;
+  a.X = pl->d_X;
+  a.tilt = pl->d_tilt;
+  const int TC = 1 << tcl;
+  dim3 grid((pl->W + TC - 1) / TC, pl->npairs, F);
+  size_t sm = (size_t)2 * pl->P * TC * sizeof(float2);
+  if (mode == 0) {
+    cudaFuncSetAttribute(k_cols<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_cols<0><<<grid, 256, sm, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(k_cols<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_cols<1><<<grid, 256, sm, s>>>(a);
+  }
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K3: Noll mixing a = L f
+__global__ void __launch_bounds__(256) k_mix(float* __restrict__ zern, const float* __restrict__ Lm, int Z,
+                                             size_t HW) {
+  const size_t pix = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= HW) return;
+  float* z = zern + (size_t)blockIdx.y * Z * HW + pix;
+  const int n = Z - 1;
+  float f[65];
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) f[i] = z[(size_t)(i + 1) * HW];
+  z[0] = 0.f;
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    float acc = 0.f;
+    for (int k = 0; k <= i; ++k) acc = fmaf(__ldg(&Lm[i * n + k]), f[k], acc);
+    z[(size_t)(i + 1) * HW] = acc;
+  }
+}
+
+int launch_mix(const p2s_plan_s* pl, int F, float* zern, cudaStream_t s) {
+  size_t HW = (size_t)pl->H * pl->W;
+  dim3 grid((unsigned)((HW + 255) / 256), F);
+  k_mix<<<grid, 256, 0, s>>>(zern, pl->d_L, pl->Z, HW);
+  return (int)cudaGetLastError();
+}
+
+// a_4..a_Z (fp32 Zernike planes) -> bf16 MLP input planes (p2s_blur API path).
+__global__ void k_zern_to_x(const float* __restrict__ zern, uint16_t* __restrict__ X, int Z, size_t HW) {
+  const size_t pix = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= HW) return;
+  const int f = blockIdx.y;
+  const float* z = zern + (size_t)f * Z * HW + pix;
+  uint16_t* x = X + (size_t)f * (Z - 3) * HW + pix;
+  for (int k = 0; k < Z - 3; ++k) x[(size_t)k * HW] = f_to_bf16(z[(size_t)(k + 3) * HW]);
+}
+
+int launch_zern_to_x(const p2s_plan_s* pl, int F, const float* zern, cudaStream_t s) {
+  size_t HW = (size_t)pl->H * pl->W;
+  dim3 grid((unsigned)((HW + 255) / 256), F);
+  k_zern_to_x<<<grid, 256, 0, s>>>(zern, pl->d_X, pl->Z, HW);
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ test support
+__global__ void k_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int64_t n,
+                              uint4* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = philox4x32_10(make_uint4((uint32_t)i, c1, c2, c3), k0, k1);
+}
+
+int launch_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int64_t n, uint32_t* out,
+                       cudaStream_t s) {
+  if (n <= 0) return 0;
+  k_philox_fill<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c1, c2, c3, k0, k1, n, reinterpret_cast<uint4*>(out));
+  return (int)cudaGetLastError();
+}
+
+}  // namespace p2s

@@ -1,0 +1,218 @@
+// k_mlp.cu -- step 3: the Phase-to-Space network on 5th-generation tensor cores.
+//
+// Paper P:172: "train a small neural network to convert the coefficients from the
+// Zernike coefficients a_x ... to the PSF coefficients beta_x".  Shape (reading Q13):
+// n_in -> h1 -> h2 -> K with ReLU hidden layers, linear output.  In the fused
+// simulate path the Noll mixing a = L f is folded into layer 1 (W1' = W1 L),
+// so the inputs are the unmixed unit-variance fields f_2..f_Z.
+//
+// Per 128-pixel tile (M = 128) the three layers are tcgen05.mma kind::f16 GEMMs
+// (bf16 operands in shared memory, fp32 accumulators in TMEM):
+//   layer 1: A1 [128 x k1] MN-major (pixels contiguous per input plane, as stored in
+//            HBM), B = W1 image [n1 x k1] K-major
+//   layer 2: A2 [128 x n1] K-major (written by the layer-1 epilogue), B = W2 image
+//   layer 3: A2 [128 x n2] K-major, B = W3 image
+// Epilogues read TMEM with tcgen05.ld (32 lanes x 16 columns per warp), add bias,
+// ReLU, repack bf16 into the next layer's A operand; the last one writes the basis
+// weights w [F][H*W][n3] bf16 (pixel-major rows for the blur epilogue).
+// Persistent grid: each CTA keeps the weight images resident in shared memory.
+#include "p2s_dev.cuh"
+#include "p2s_internal.h"
+
+namespace p2s {
+
+struct MlpArgs {
+  const uint16_t* X;    // bf16 [F][nin][HW]
+  uint16_t* wout;       // bf16 [F][HW][n3]
+  const uint8_t* blob;  // W1img | W2img | W3img | b1 | b2 | b3
+  int nin, k1, n1, n2, n3;
+  uint32_t off_w2, off_w3, off_b1, off_b2, off_b3, blob_bytes;
+  int HW, F, tiles_per_frame;
+};
+
+// Epilogue: TMEM columns [0, ncols) of this thread's row -> +bias (+ReLU) -> bf16.
+// mode 0: write K-major A operand rows into smem; mode 1: write global row.
+template <bool RELU, bool TO_GLOBAL>
+__device__ __forceinline__ void mlp_epilogue(uint32_t taddr, int ncols, const float* bias, uint8_t* a_smem,
+                                             uint32_t sbo, int m, uint16_t* grow) {
+  for (int cb = 0; cb < ncols / 16; ++cb) {
+    float v[16];
+    tmem_ld16(taddr + cb * 16, v);
+    uint32_t pk[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float x0 = v[2 * i] + bias[cb * 16 + 2 * i];
+      float x1 = v[2 * i + 1] + bias[cb * 16 + 2 * i + 1];
+      if (RELU) {
+        x0 = fmaxf(x0, 0.f);
+        x1 = fmaxf(x1, 0.f);
+      }
+      pk[i] = pack_bf16x2(x0, x1);
+    }
+    if (TO_GLOBAL) {
+      if (grow) {
+        uint4* g = reinterpret_cast<uint4*>(grow + cb * 16);
+        g[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        g[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    } else {
+      uint8_t* base = a_smem + (m & 7) * 16 + (m >> 3) * sbo + (2 * cb) * 128;
+      *reinterpret_cast<uint4*>(base) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      *reinterpret_cast<uint4*>(base + 128) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128, 1) k_mlp(MlpArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* sw = smem;  // weight blob
+  const uint32_t blob_al = (a.blob_bytes + 127) & ~127u;
+  uint8_t* A1 = sw + blob_al;
+  const uint32_t a1_bytes = 128u * a.k1 * 2;
+  uint8_t* A2 = A1 + a1_bytes;
+  const int nmax = a.n1 > a.n2 ? a.n1 : a.n2;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(A2 + 128u * nmax * 2);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // weights -> smem (once per CTA)
+  for (uint32_t i = tid * 16; i < a.blob_bytes; i += 128 * 16)
+    *reinterpret_cast<uint4*>(sw + i) = __ldg(reinterpret_cast<const uint4*>(a.blob + i));
+  // zero the padded input planes of A1 (k in [nin, k1)) once
+  for (int idx = tid; idx < (a.k1 - a.nin) * 16; idx += 128) {
+    const int k = a.nin + idx % (a.k1 - a.nin), g = idx / (a.k1 - a.nin);
+    *reinterpret_cast<uint4*>(A1 + g * (a.k1 * 16) + k * 16) = make_uint4(0, 0, 0, 0);
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  const int nalloc = nmax > a.n3 ? nmax : a.n3;
+  const uint32_t ncols = nalloc <= 32 ? 32 : nalloc <= 64 ? 64 : nalloc <= 128 ? 128 : 256;
+  if (warp == 0) tmem_alloc(tslot, ncols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  const int m = warp * 32 + lane;  // TMEM lane = tile row = pixel offset
+
+  const float* b1 = reinterpret_cast<const float*>(sw + a.off_b1);
+  const float* b2 = reinterpret_cast<const float*>(sw + a.off_b2);
+  const float* b3 = reinterpret_cast<const float*>(sw + a.off_b3);
+  const uint32_t sA1 = smem_u32(A1), sA2 = smem_u32(A2);
+  const uint32_t sW1 = smem_u32(sw), sW2 = smem_u32(sw + a.off_w2), sW3 = smem_u32(sw + a.off_w3);
+  const uint32_t id1 = umma_idesc_bf16(128, a.n1, true, false);
+  const uint32_t id2 = umma_idesc_bf16(128, a.n2, false, false);
+  const uint32_t id3 = umma_idesc_bf16(128, a.n3, false, false);
+  uint32_t phase = 0;
+  const int ntiles = a.F * a.tiles_per_frame;
+  const bool vec_ok = (a.HW % 8) == 0;
+
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int f = tile / a.tiles_per_frame;
+    const int pix0 = (tile - f * a.tiles_per_frame) * 128;
+    // ---- A1: nin input planes x 128 pixels, MN-major (k linear, 16 B per k-row)
+    const uint16_t* Xf = a.X + (size_t)f * a.nin * a.HW;
+    for (int idx = tid; idx < a.nin * 16; idx += 128) {
+      const int k = idx % a.nin, g = idx / a.nin;
+      const int pix = pix0 + 8 * g;
+      const uint16_t* src = Xf + (size_t)k * a.HW + pix;
+      uint4 v;
+      if (vec_ok && pix + 8 <= a.HW) {
+        v = __ldg(reinterpret_cast<const uint4*>(src));
+      } else {
+        uint16_t t[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) t[e] = (pix + e < a.HW) ? src[e] : (uint16_t)0;
+        v = make_uint4(t[0] | (t[1] << 16), t[2] | (t[3] << 16), t[4] | (t[5] << 16), t[6] | (t[7] << 16));
+      }
+      *reinterpret_cast<uint4*>(A1 + g * (a.k1 * 16) + k * 16) = v;
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    // ---- layer 1
+    if (tid == 0) {
+      tc_fence_after();
+      for (int s = 0; s < a.k1 / 16; ++s)
+        umma_bf16(tmem, umma_desc(sA1 + s * 256, 128, a.k1 * 16), umma_desc(sW1 + s * 256, 128, (a.k1 / 8) * 128),
+                  id1, s > 0);
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    mlp_epilogue<true, false>(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m, nullptr);
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    // ---- layer 2
+    if (tid == 0) {
+      tc_fence_after();
+      for (int s = 0; s < a.n1 / 16; ++s)
+        umma_bf16(tmem, umma_desc(sA2 + s * 256, 128, (a.n1 / 8) * 128),
+                  umma_desc(sW2 + s * 256, 128, (a.n1 / 8) * 128), id2, s > 0);
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    mlp_epilogue<true, false>(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m, nullptr);
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    // ---- layer 3
+    if (tid == 0) {
+      tc_fence_after();
+      for (int s = 0; s < a.n2 / 16; ++s)
+        umma_bf16(tmem, umma_desc(sA2 + s * 256, 128, (a.n2 / 8) * 128),
+                  umma_desc(sW3 + s * 256, 128, (a.n2 / 8) * 128), id3, s > 0);
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    const int pix = pix0 + m;
+    uint16_t* grow = (pix < a.HW) ? a.wout + ((size_t)f * a.HW + pix) * a.n3 : nullptr;
+    mlp_epilogue<false, true>(taddr, a.n3, b3, nullptr, 0, m, grow);
+    tc_fence_before();
+    __syncthreads();
+  }
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem, ncols);
+}
+
+int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
+  const MlpGeom& g = folded ? p->mg_fold : p->mg_plain;
+  MlpArgs a;
+  a.X = p->d_X;
+  a.wout = p->d_w;
+  a.blob = folded ? p->d_mlp_fold : p->d_mlp_plain;
+  a.nin = g.nin;
+  a.k1 = g.k1;
+  a.n1 = g.n1;
+  a.n2 = g.n2;
+  a.n3 = g.n3;
+  a.off_w2 = (uint32_t)g.off_w2;
+  a.off_w3 = (uint32_t)g.off_w3;
+  a.off_b1 = (uint32_t)g.off_b1;
+  a.off_b2 = (uint32_t)g.off_b2;
+  a.off_b3 = (uint32_t)g.off_b3;
+  a.blob_bytes = (uint32_t)g.blob_bytes;
+  a.HW = p->H * p->W;
+  a.F = F;
+  a.tiles_per_frame = (a.HW + 127) / 128;
+  const int nmax = g.n1 > g.n2 ? g.n1 : g.n2;
+  size_t sm = ((g.blob_bytes + 127) & ~(size_t)127) + 128 * g.k1 * 2 + 128 * nmax * 2 + 16;
+  cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int ntiles = F * a.tiles_per_frame;
+  // TMEM: at most 256 columns per CTA, so up to 2 CTAs share an SM
+  int blocks_per_sm = (sm <= 100 * 1024) ? 2 : 1;
+  int grid = p->num_sms * blocks_per_sm;
+  if (grid > ntiles) grid = ntiles;
+  k_mlp<<<grid, 128, sm, s>>>(a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace p2s

@@ -1,0 +1,116 @@
+// p2s_internal.h -- private declarations shared by the host plan code and the kernels.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/p2s.h"
+
+#include <cuda_runtime.h>
+
+namespace p2s {
+
+p2s_status set_error(p2s_status st, const std::string& msg);
+
+// ---- plan math (plan_math.cpp, host fp64) ----
+double kolmogorov_cd();
+double kolmogorov_cw();
+double noll_constant();
+void noll_nm(int j, int* n, int* m, int* kind);
+void noll_matrix(int Z, double d_over_r0, std::vector<double>& A);
+bool noll_cholesky(int Z, const std::vector<double>& A, std::vector<double>& L);
+void bessel_j_all(double x, int nmax, double* J);
+void psd_tables(int P, int Q, double s_px, int Z, std::vector<double>& sqrtS, std::vector<double>& clamped);
+int grid_size(int x);
+
+constexpr int kMaxRadix = 24;
+
+// Inverse-DFT plan for one axis: radix list and e^{+2 pi i k/N} table (device).
+struct AxisFFT {
+  int N = 0;
+  int nrad = 0;
+  int rad[kMaxRadix] = {0};
+  float2* tw = nullptr;  // device [N]
+};
+
+// MLP geometry (all padded sizes are multiples of 16).
+struct MlpGeom {
+  int nin = 0;   // real inputs
+  int k1 = 0;    // padded layer-1 K
+  int n1 = 0, n2 = 0, n3 = 0;  // padded widths (n3 = padded K bases)
+  int kout = 0;  // real K
+  size_t blob_bytes = 0;  // W1img | W2img | W3img | b1 | b2 | b3
+  size_t off_w2 = 0, off_w3 = 0, off_b1 = 0, off_b2 = 0, off_b3 = 0;
+};
+
+// Blur geometry: K-step schedule of the tap-row groups (see k_blur.cu).
+struct BlurGeom {
+  int T = 0, c = 0;        // taps, centre
+  int NC = 0;              // source chunks = T + 15
+  int RB = 32;             // output rows per CTA
+  int RS = 0;              // source rows held in smem
+  int nks = 0;             // number of K-steps
+  int np = 0;              // padded N (= MlpGeom.n3)
+  uint32_t* koff = nullptr;  // device [nks]: byte offset of group a relative to (src + yl*16)
+  uint32_t* klbo = nullptr;  // device [nks]: LBO (group b - group a) in bytes
+  uint8_t* bimg = nullptr;   // device [nks][np*32 bytes] B tiles (K-major, no swizzle)
+  float* hsum = nullptr;     // device [np] per-basis tap sum (normalisation)
+};
+
+}  // namespace p2s
+
+struct p2s_plan_s {
+  int H = 0, W = 0, C = 0, Z = 0, K = 0, T = 0, P = 0, Q = 0;
+  int nslots = 0, npairs = 0, h1 = 0, h2 = 0;
+  double d_over_r0 = 0, L_m = 0, s_px = 0, kappa = 0;
+  float ar_alpha = 0, noise_sigma = 0;
+  int normalize = 0, clamp01 = 0, device = 0, max_batch = 0;
+  double clamped_max = 0;
+  std::vector<double> A0, Lc;      // Z x Z
+  std::vector<float> sqrtS_host;   // [nslots][P][Q]
+  std::vector<float> basis_host;   // [K][T][T]
+  std::vector<float> mlp_host;     // packed
+  // device tables
+  float2* d_sqrtS = nullptr;    // [npairs][P][Q] scaled (sa, sb)
+  float4* d_ar = nullptr;       // [npairs][P][Q] AR(1) state (zeta_a, zeta_b)
+  float* d_L = nullptr;         // [(Z-1)*(Z-1)] float L[2..Z][2..Z]
+  uint8_t* d_mlp_fold = nullptr;   // L folded into layer 1 (inputs f_2..f_Z)
+  uint8_t* d_mlp_plain = nullptr;  // plain layer 1 (inputs a_4..a_Z)
+  p2s::MlpGeom mg_fold, mg_plain;
+  p2s::BlurGeom bg;
+  p2s::AxisFFT fq, fp;
+  // workspace (max_batch frames)
+  void* d_ws = nullptr;
+  size_t ws_bytes = 0;
+  float2* d_Z = nullptr;        // [mb][npairs][P][Q]
+  uint16_t* d_X = nullptr;      // bf16 [mb][nslots][H*W] (simulate) / [mb][Z-3][H*W] (blur API)
+  float* d_tilt = nullptr;      // [mb][2][H*W]
+  uint16_t* d_Iw = nullptr;     // bf16 [mb][C][H][W]
+  uint16_t* d_w = nullptr;      // bf16 [mb][H*W][n3]
+  float* d_img = nullptr;       // staging for the host entry point [mb][C][H][W]
+  float* d_out = nullptr;       // staging for the host entry point [mb][C][H][W]
+  // AR bookkeeping
+  bool ar_valid = false;
+  uint64_t ar_seed = 0;
+  int64_t ar_next = 0;
+  int num_sms = 148;
+};
+
+namespace p2s {
+// ---- kernel launchers (k_*.cu); all return cudaGetLastError() as int ----
+int launch_rows(const p2s_plan_s* p, uint64_t seed, int64_t frame0, int F, bool ar, int ar_mode,
+                int64_t replay_from, cudaStream_t s);
+int launch_cols(const p2s_plan_s* p, int F, int mode, float* zern, cudaStream_t s);
+int launch_mix(const p2s_plan_s* p, int F, float* zern, cudaStream_t s);
+int launch_zern_to_x(const p2s_plan_s* p, int F, const float* zern, cudaStream_t s);
+int launch_warp_f32(const p2s_plan_s* p, int F, const float* img, int64_t stride, const float* zern, float* out,
+                    cudaStream_t s);
+int launch_warp_sim(const p2s_plan_s* p, int F, const float* img, int64_t stride, cudaStream_t s);
+int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s);
+int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0,
+                float* out, cudaStream_t s);
+int launch_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int64_t n, uint32_t* out,
+                       cudaStream_t s);
+}  // namespace p2s

@@ -1,0 +1,215 @@
+"""Thin ctypes binding of include/p2s.h (argument marshalling only).
+
+Every step of the simulator runs in libp2s.so (sm_100a CUDA kernels + host plan
+code).  There is no Python or CPU fallback: if the library is missing or cannot be
+loaded the import fails loudly.  torch is used only to hand over device pointers and
+the current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libp2s.so")
+
+P2S_OK = 0
+_STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NUMERIC", 3: "CUDA", 4: "OUT_OF_MEMORY", 5: "UNSUPPORTED"}
+
+# every entry point declared in include/p2s.h
+EXPORTS = ("p2s_plan_create", "p2s_plan_destroy", "p2s_sample_zernike", "p2s_warp", "p2s_blur",
+           "p2s_simulate_frames", "p2s_simulate_frames_host", "p2s_last_error", "p2s_plan_info",
+           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_philox_fill", "p2s_host_tables",
+           "p2s_grid_size")
+
+
+class P2SError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"p2s error {status} ({_STATUS.get(status, '?')}): {msg}")
+        self.status = status
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("taps", ctypes.c_int), ("aperture_m", ctypes.c_double), ("wavelength_m", ctypes.c_double),
+                ("s_per_px", ctypes.c_double), ("tilt_px_per_rad", ctypes.c_double), ("pad", ctypes.c_int),
+                ("mlp_hidden", ctypes.c_int * 2), ("max_batch", ctypes.c_int), ("ar_alpha", ctypes.c_float),
+                ("noise_sigma", ctypes.c_float), ("normalize_psf_sum", ctypes.c_int), ("clamp01", ctypes.c_int),
+                ("device", ctypes.c_int)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() (make -C paper_2210_06713_b200/csrc)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, u32, u64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
+    dp, fp = ctypes.POINTER(ctypes.c_double), ctypes.c_void_p
+    lib.p2s_plan_create.argtypes = [ctypes.POINTER(vp), i32, i32, i32, ctypes.c_double, ctypes.c_double, i32, i32,
+                                    fp, fp, ctypes.POINTER(Options)]
+    lib.p2s_plan_destroy.argtypes = [vp]
+    lib.p2s_sample_zernike.argtypes = [vp, u64, i64, i32, vp, vp]
+    lib.p2s_warp.argtypes = [vp, vp, i64, vp, vp, i32, vp]
+    lib.p2s_blur.argtypes = [vp, vp, vp, u64, i64, vp, i32, vp]
+    lib.p2s_simulate_frames.argtypes = [vp, vp, i64, u64, i64, i32, vp, vp]
+    lib.p2s_simulate_frames_host.argtypes = [vp, vp, i64, u64, i64, i32, vp, vp]
+    lib.p2s_last_error.restype = ctypes.c_char_p
+    lib.p2s_plan_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_size_t), dp,
+                                  ctypes.POINTER(i32)]
+    lib.p2s_plan_export_tables.argtypes = [vp, vp, vp, vp]
+    lib.p2s_plan_import_sqrtS.argtypes = [vp, vp]
+    lib.p2s_philox_fill.argtypes = [u32, u32, u32, u32, u32, i64, vp, vp]
+    lib.p2s_host_tables.argtypes = [i32, i32, ctypes.c_double, ctypes.c_double, i32, vp, vp, vp, vp]
+    lib.p2s_grid_size.argtypes = [i32]
+    lib.p2s_grid_size.restype = i32
+    for name in EXPORTS:
+        if name not in ("p2s_last_error", "p2s_grid_size"):
+            getattr(lib, name).restype = ctypes.c_int
+    return lib
+
+
+lib = _load()
+
+
+def _check(st):
+    if st != P2S_OK:
+        raise P2SError(st, lib.p2s_last_error().decode())
+
+
+def _ptr(x):
+    """Device pointer of a torch tensor (or an int address)."""
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def grid_size(x: int) -> int:
+    return lib.p2s_grid_size(int(x))
+
+
+def host_tables(P, Q, s_per_px, d_over_r0, Z=36, want_sqrtS=True):
+    """Library plan-time tables computed on the host (no GPU): A0, L, sqrt(S), clamped fractions."""
+    A0 = np.zeros((Z, Z))
+    L = np.zeros((Z, Z))
+    sq = np.zeros((Z - 1, P, Q)) if want_sqrtS else None
+    cl = np.zeros(Z - 1) if want_sqrtS else None
+    _check(lib.p2s_host_tables(P, Q, float(s_per_px), float(d_over_r0), Z, A0.ctypes.data, L.ctypes.data,
+                               sq.ctypes.data if want_sqrtS else None, cl.ctypes.data if want_sqrtS else None))
+    return A0, L, sq, cl
+
+
+def philox_fill(c1, c2, c3, k0, k1, n, out, stream=None):
+    _check(lib.p2s_philox_fill(c1, c2, c3, k0, k1, n, _ptr(out), _stream(stream)))
+
+
+@dataclass
+class PlanConfig:
+    H: int
+    W: int
+    C: int
+    d_over_r0: float
+    L_m: float = 1000.0
+    Z: int = 36
+    K: int = 16
+    taps: int = 17
+    aperture_m: float = 0.0
+    wavelength_m: float = 0.0
+    s_per_px: float = 0.0
+    tilt_px_per_rad: float = 0.0
+    pad: int = 0
+    mlp_hidden: tuple = (100, 100)
+    max_batch: int = 0
+    ar_alpha: float = 0.0
+    noise_sigma: float = 0.0
+    normalize_psf_sum: bool = False
+    clamp01: bool = False
+    device: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+class Plan:
+    """Owns a p2s_plan.  Buffers are torch CUDA tensors (float32, contiguous)."""
+
+    def __init__(self, cfg: PlanConfig, basis: np.ndarray, mlp_weights: np.ndarray):
+        self.cfg = cfg
+        basis = np.ascontiguousarray(basis, dtype=np.float32)
+        mlp = np.ascontiguousarray(mlp_weights, dtype=np.float32)
+        o = Options()
+        o.taps = cfg.taps
+        o.aperture_m = cfg.aperture_m
+        o.wavelength_m = cfg.wavelength_m
+        o.s_per_px = cfg.s_per_px
+        o.tilt_px_per_rad = cfg.tilt_px_per_rad
+        o.pad = cfg.pad
+        o.mlp_hidden[0], o.mlp_hidden[1] = cfg.mlp_hidden
+        o.max_batch = cfg.max_batch
+        o.ar_alpha = cfg.ar_alpha
+        o.noise_sigma = cfg.noise_sigma
+        o.normalize_psf_sum = int(cfg.normalize_psf_sum)
+        o.clamp01 = int(cfg.clamp01)
+        o.device = cfg.device
+        self._h = ctypes.c_void_p()
+        _check(lib.p2s_plan_create(ctypes.byref(self._h), cfg.H, cfg.W, cfg.C, float(cfg.d_over_r0),
+                                   float(cfg.L_m), cfg.Z, cfg.K, basis.ctypes.data, mlp.ctypes.data, ctypes.byref(o)))
+        P, Q, ws, cl, mb = ctypes.c_int(), ctypes.c_int(), ctypes.c_size_t(), ctypes.c_double(), ctypes.c_int()
+        _check(lib.p2s_plan_info(self._h, ctypes.byref(P), ctypes.byref(Q), ctypes.byref(ws), ctypes.byref(cl),
+                                 ctypes.byref(mb)))
+        self.P, self.Q, self.workspace_bytes, self.clamped_psd_fraction, self.max_batch = \
+            P.value, Q.value, ws.value, cl.value, mb.value
+
+    def close(self):
+        if self._h:
+            lib.p2s_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- per-frame API
+    def sample_zernike(self, seed, frame0, nframes, zern, stream=None):
+        _check(lib.p2s_sample_zernike(self._h, seed, frame0, nframes, _ptr(zern), _stream(stream)))
+
+    def warp(self, img, img_frame_stride, zern, warped, nframes, stream=None):
+        _check(lib.p2s_warp(self._h, _ptr(img), img_frame_stride, _ptr(zern), _ptr(warped), nframes,
+                            _stream(stream)))
+
+    def blur(self, warped, zern, seed, frame0, out, nframes, stream=None):
+        _check(lib.p2s_blur(self._h, _ptr(warped), _ptr(zern), seed, frame0, _ptr(out), nframes, _stream(stream)))
+
+    def simulate_frames(self, img, img_frame_stride, seed, frame0, nframes, out, stream=None):
+        _check(lib.p2s_simulate_frames(self._h, _ptr(img), img_frame_stride, seed, frame0, nframes, _ptr(out),
+                                       _stream(stream)))
+
+    def simulate_frames_host(self, img_host: np.ndarray, img_frame_stride, seed, frame0, nframes,
+                             out_host: np.ndarray, stream=None):
+        assert img_host.dtype == np.float32 and img_host.flags.c_contiguous
+        assert out_host.dtype == np.float32 and out_host.flags.c_contiguous
+        _check(lib.p2s_simulate_frames_host(self._h, ctypes.c_void_p(img_host.ctypes.data), img_frame_stride, seed,
+                                            frame0, nframes, ctypes.c_void_p(out_host.ctypes.data), _stream(stream)))
+
+    # ---- introspection
+    def export_tables(self):
+        Z, P, Q = self.cfg.Z, self.P, self.Q
+        A0 = np.zeros((Z, Z))
+        L = np.zeros((Z, Z))
+        sq = np.zeros((Z - 1, P, Q), dtype=np.float32)
+        _check(lib.p2s_plan_export_tables(self._h, A0.ctypes.data, L.ctypes.data, sq.ctypes.data))
+        return A0, L, sq
+
+    def import_sqrtS(self, sqrtS: np.ndarray):
+        sq = np.ascontiguousarray(sqrtS, dtype=np.float32)
+        assert sq.shape == (self.cfg.Z - 1, self.P, self.Q)
+        _check(lib.p2s_plan_import_sqrtS(self._h, sq.ctypes.data))

@@ -1,0 +1,256 @@
+"""GPU parity: libp2s (sm_100a) vs the fp64 CPU oracle, element by element.
+
+Every call goes through the C ABI (paper_2210_06713_b200.p2s, ctypes).  Inputs are
+seeded and synthetic (synth/).  Tolerances (BASELINE north_star): rel-L2 <= 1e-4 for
+fp32 stages (step 1 per mode plane, step 2 per channel) and <= 2e-2 for the bf16
+tensor-core stages (steps 3-5, per channel).  Unless a test says otherwise the plan
+imports the oracle's sqrt(S) tables so per-frame parity is isolated from the
+(separately tested) plan-time quadrature.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import correlation, optics, philox, pipeline
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SEED = 2210
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+_TABLES = {}
+
+
+def oracle_tables(P, Q, Z=36, s_px=None):
+    s_px = s_px or optics.geometry()[0]
+    key = (P, Q, Z, s_px)
+    if key not in _TABLES:
+        _TABLES[key] = correlation.sqrt_psd_tables(P, Q, s_px, Z)[0]
+    return _TABLES[key]
+
+
+def make_plan(H, W, C, dr0, K, T, Z=36, basis=None, mlp=None, import_tables=True, **kw):
+    from paper_2210_06713_b200 import Plan, PlanConfig
+    basis = synth.basis(K, T, seed=1) if basis is None else basis
+    mlp = synth.mlp_weights(K, n_in=Z - 3, seed=1) if mlp is None else mlp
+    cfg = PlanConfig(H=H, W=W, C=C, d_over_r0=dr0, Z=Z, K=K, taps=T, **kw)
+    plan = Plan(cfg, basis, mlp)
+    sq = oracle_tables(plan.P, plan.Q, Z)
+    if import_tables:
+        plan.import_sqrtS(sq)
+    A0 = optics.noll_covariance(Z, dr0)
+    L = optics.noll_cholesky(A0)
+    return plan, basis, mlp, sq, L
+
+
+def cuda(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+# ------------------------------------------------------------------ Philox
+def test_device_philox_bit_exact():
+    from paper_2210_06713_b200 import philox_fill
+    n = 4096
+    out = torch.empty((n, 4), dtype=torch.int32, device="cuda")
+    philox_fill(7 | (1 << 16), 123, 4, 0xDEADBEEF, 0x1234, n, out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint32)
+    ref = philox.philox4x32_10(np.arange(n), 7 | (1 << 16), 123, 4, 0xDEADBEEF, 0x1234)
+    for w in range(4):
+        assert np.array_equal(got[:, w], np.asarray(ref[w], dtype=np.uint32))
+
+
+# ------------------------------------------------------------------ step 1
+@pytest.mark.parametrize("H,W,dr0,frame0,F", [(64, 64, 2.0, 0, 2), (60, 90, 3.0, 5, 2), (96, 160, 1.0, 0, 1)])
+def test_sample_zernike_vs_oracle(H, W, dr0, frame0, F):
+    plan, _, _, sq, L = make_plan(H, W, 1, dr0, 16, 17)
+    z = torch.empty((F, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, frame0, F, z)
+    torch.cuda.synchronize()
+    got = z.cpu().numpy()
+    ref = pipeline.sample_zernike(SEED, frame0, F, sq, L, H, W)
+    assert np.all(got[:, 0] == 0)
+    worst = max(rel_l2(got[f, j], ref[f, j]) for f in range(F) for j in range(1, 36))
+    assert worst <= 1e-4, worst
+
+
+def test_sample_zernike_own_tables_vs_oracle():
+    """Library plan tables (C++ quadrature/FFT) instead of the oracle's: the sampled
+    fields still agree to the table tolerance."""
+    H = W = 64
+    plan, _, _, sq, L = make_plan(H, W, 1, 2.0, 16, 17, import_tables=False)
+    z = torch.empty((1, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 0, 1, z)
+    torch.cuda.synchronize()
+    ref = pipeline.sample_zernike(SEED, 0, 1, sq, L, H, W)
+    worst = max(rel_l2(z.cpu().numpy()[0, j], ref[0, j]) for j in range(1, 36))
+    assert worst <= 1e-3, worst
+
+
+def test_sample_zernike_ar_sequence_and_replay():
+    H = W = 64
+    alpha = 0.95
+    plan, _, _, sq, L = make_plan(H, W, 1, 3.0, 16, 17, ar_alpha=alpha)
+    ref = pipeline.sample_zernike(SEED, 0, 6, sq, L, H, W, alpha=alpha)
+    z = torch.empty((6, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 0, 4, z[:4])      # fresh sequence
+    plan.sample_zernike(SEED, 4, 2, z[4:])      # continuation from the stored state
+    torch.cuda.synchronize()
+    got = z.cpu().numpy()
+    worst = max(rel_l2(got[f, j], ref[f, j]) for f in range(6) for j in range(1, 36))
+    assert worst <= 1e-4, worst
+    z2 = torch.empty((2, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 2, 2, z2)         # replay frames 0..1 on the device
+    torch.cuda.synchronize()
+    assert torch.equal(z2, z[2:4])              # bit-identical to the sequential run
+
+
+# ------------------------------------------------------------------ step 2
+@pytest.mark.parametrize("H,W,C", [(64, 64, 1), (60, 90, 3)])
+def test_warp_vs_oracle(H, W, C):
+    plan, _, _, sq, L = make_plan(H, W, C, 5.0, 16, 17)
+    a = pipeline.sample_zernike(SEED, 0, 2, sq, L, H, W)
+    img = synth.image(H, W, C, seed=3)
+    kappa = optics.geometry()[1]
+    out = torch.empty((2, C, H, W), device="cuda")
+    plan.warp(cuda(img), 0, cuda(a), out, 2)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    for f in range(2):
+        ref = pipeline.warp(img, a[f, 1].astype(np.float32).astype(np.float64),
+                            a[f, 2].astype(np.float32).astype(np.float64), kappa)
+        for c in range(C):
+            assert rel_l2(got[f, c], ref[c]) <= 1e-5
+
+
+# ------------------------------------------------------------------ steps 3-5 (p2s_blur)
+def _onehot_mlp(K, k0, Z=36, hidden=(100, 100)):
+    sizes = synth.mlp_sizes(Z - 3, hidden, K)
+    parts = []
+    for li, (o, i) in enumerate(sizes):
+        parts.append(np.zeros(o * i))
+        b = np.zeros(o)
+        if li == len(sizes) - 1:
+            b[k0] = 1.0
+        parts.append(b)
+    return np.concatenate(parts).astype(np.float32)
+
+
+def test_blur_delta_basis_identity():
+    """Delta basis, w = e_0 => out = Iw (BASELINE north_star pin), up to bf16 rounding of Iw."""
+    H, W, C, T = 64, 64, 2, 3
+    basis = np.zeros((1, T, T), dtype=np.float32)
+    basis[0, 1, 1] = 1.0
+    plan, *_ = make_plan(H, W, C, 2.0, 1, T, basis=basis, mlp=_onehot_mlp(1, 0))
+    Iw = synth.image(H, W, C, seed=4)[None]
+    zern = np.zeros((1, 36, H, W), dtype=np.float32)
+    out = torch.empty((1, C, H, W), device="cuda")
+    plan.blur(cuda(Iw), cuda(zern), SEED, 0, out, 1)
+    torch.cuda.synchronize()
+    assert rel_l2(out.cpu().numpy(), Iw) <= 4e-3
+
+
+@pytest.mark.parametrize("H,W,K,T,k0", [(64, 64, 16, 17, 0), (64, 64, 16, 17, 9), (96, 160, 100, 33, 57)])
+def test_blur_single_basis_vs_oracle(H, W, K, T, k0):
+    """w = e_k0 isolates one spatially invariant convolution (Eq.9 term) of the tap GEMM."""
+    plan, basis, *_ = make_plan(H, W, 1, 2.0, K, T, mlp=_onehot_mlp(K, k0))
+    Iw = synth.image(H, W, 1, seed=5)[None]
+    zern = np.zeros((1, 36, H, W), dtype=np.float32)
+    out = torch.empty((1, 1, H, W), device="cuda")
+    plan.blur(cuda(Iw), cuda(zern), SEED, 0, out, 1)
+    torch.cuda.synchronize()
+    w = np.zeros((K, H, W))
+    w[k0] = 1.0
+    ref = pipeline.blur(Iw[0].astype(np.float64), w, basis)
+    assert rel_l2(out.cpu().numpy()[0, 0], ref[0]) <= 1e-2
+
+
+@pytest.mark.parametrize("H,W,C,K,T", [(64, 64, 1, 16, 17), (96, 160, 3, 100, 33)])
+def test_blur_api_vs_oracle(H, W, C, K, T):
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 3.0, K, T)
+    a = pipeline.sample_zernike(SEED, 0, 1, sq, L, H, W).astype(np.float32)
+    Iw = synth.image(H, W, C, seed=6)[None]
+    out = torch.empty((1, C, H, W), device="cuda")
+    plan.blur(cuda(Iw), cuda(a), SEED, 0, out, 1)
+    torch.cuda.synchronize()
+    layers = synth.unpack_mlp(mlp, K)
+    w = pipeline.mlp(a[0, 3:].astype(np.float64), layers)
+    ref = pipeline.blur(Iw[0].astype(np.float64), w, basis)
+    got = out.cpu().numpy()[0]
+    for c in range(C):
+        assert rel_l2(got[c], ref[c]) <= 2e-2
+
+
+# ------------------------------------------------------------------ steps 1-5 fused
+@pytest.mark.parametrize("H,W,C,K,T,dr0,F", [(64, 64, 1, 16, 17, 2.0, 1), (96, 160, 3, 100, 33, 3.0, 2)])
+def test_simulate_vs_oracle(H, W, C, K, T, dr0, F):
+    plan, basis, mlp, sq, L = make_plan(H, W, C, dr0, K, T)
+    img = synth.image(H, W, C, seed=7)
+    out = torch.empty((F, C, H, W), device="cuda")
+    plan.simulate_frames(cuda(img), 0, SEED, 0, F, out)
+    torch.cuda.synchronize()
+    ref = pipeline.simulate(img[None], True, SEED, 0, F, sq, L, basis, synth.unpack_mlp(mlp, K),
+                            optics.geometry()[1])
+    got = out.cpu().numpy()
+    for f in range(F):
+        for c in range(C):
+            assert rel_l2(got[f, c], ref[f, c]) <= 2e-2, (f, c, rel_l2(got[f, c], ref[f, c]))
+
+
+def test_simulate_step5_vs_oracle():
+    H, W, C, K, T = 64, 96, 2, 16, 17
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T, noise_sigma=0.05, clamp01=True)
+    img = synth.image(H, W, C, seed=8)
+    out = torch.empty((1, C, H, W), device="cuda")
+    plan.simulate_frames(cuda(img), 0, SEED, 3, 1, out)
+    torch.cuda.synchronize()
+    ref = pipeline.simulate(img[None], True, SEED, 3, 1, sq, L, basis, synth.unpack_mlp(mlp, K),
+                            optics.geometry()[1], sigma=0.05, clamp01=True)
+    assert rel_l2(out.cpu().numpy(), ref) <= 2e-2
+
+
+def test_simulate_batch_split_bit_identical():
+    H, W, C, K, T = 64, 64, 1, 16, 17
+    plan, *_ = make_plan(H, W, C, 3.0, K, T)
+    img = cuda(synth.image(H, W, C, seed=9))
+    a = torch.empty((4, C, H, W), device="cuda")
+    b = torch.empty((4, C, H, W), device="cuda")
+    plan.simulate_frames(img, 0, SEED, 10, 4, a)
+    for i in range(4):
+        plan.simulate_frames(img, 0, SEED, 10 + i, 1, b[i:i + 1])
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    c = torch.empty_like(a)
+    plan.simulate_frames(img, 0, SEED, 10, 4, c)
+    torch.cuda.synchronize()
+    assert torch.equal(a, c)
+
+
+def test_simulate_host_entry_matches_device_entry():
+    H, W, C, K, T = 64, 64, 2, 16, 17
+    plan, *_ = make_plan(H, W, C, 3.0, K, T)
+    img = synth.image(H, W, C, seed=10)
+    dev = torch.empty((2, C, H, W), device="cuda")
+    plan.simulate_frames(cuda(img), 0, SEED, 0, 2, dev)
+    host = np.empty((2, C, H, W), dtype=np.float32)
+    plan.simulate_frames_host(img, 0, SEED, 0, 2, host)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.cpu().numpy(), host)
+
+
+def test_invalid_arguments_fail_loudly():
+    from paper_2210_06713_b200 import P2SError, Plan, PlanConfig
+    with pytest.raises(P2SError):
+        Plan(PlanConfig(H=64, W=64, C=1, d_over_r0=1.0, K=16, taps=16), synth.basis(16, 17), synth.mlp_weights(16))
+    with pytest.raises(P2SError):
+        Plan(PlanConfig(H=8, W=64, C=1, d_over_r0=1.0, K=16, taps=17), synth.basis(16, 17), synth.mlp_weights(16))
+    with pytest.raises(P2SError):
+        Plan(PlanConfig(H=64, W=64, C=1, d_over_r0=-1.0, K=16, taps=17), synth.basis(16, 17),
+             synth.mlp_weights(16))
