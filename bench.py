@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the DF-P2S dense-field simulator (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg3_512]
+
+One step = one p2s_simulate_frames call over a batch of F frames (all five steps of
+the hot path) on synthetic seeded inputs already resident in HBM.  The
+default workload is BASELINE config 3, the paper's real-time headline: 512x512 RGB,
+F = 64 frames per GPU, D/r0 = 3, Z = 36, K = 100 bases of 33x33 taps, MLP 33-100-100-100.
+Multi-GPU (torchrun, one rank per GPU, NCCL process group for the barrier and the
+max-over-ranks time only): every rank simulates its own disjoint frame range
+(weak scaling, no data-path collective -- frames are independent).
+
+Prints ONE JSON line on rank 0.  `value` is whole-job frames/s from CUDA events
+(max over ranks); `e2e` is the same metric through p2s_simulate_frames_host with
+pinned host buffers (H2D of the image and D2H of every output frame inside the
+timed region); `stages` and `roofline` come from per-launch CUDA event pairs
+recorded by the library on the launching stream (p2s_plan_stage_timing).
+`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample of the
+same workload on the host cores.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "dense-field frames/sec at 512x512 and 3840x2160 RGB, 1/2/4/8 B200; roofline %"
+SEED = 2210
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(FALLBACK_PEAKS)
+    d["source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+WORKLOADS = {
+    # BASELINE.json configs[2]: the metric's 512x512 RGB headline, fits one GPU
+    "cfg3_512": dict(H=512, W=512, C=3, F=64, d_over_r0=3.0, K=100, T=33, ar_alpha=0.0,
+                     desc="512x512 RGB, batch of 64 frames/GPU, D/r0=3, Z=36, K=100 bases 33x33, MLP 33-100-100-100"),
+    "cfg4_1080p": dict(H=1080, W=1920, C=3, F=8, d_over_r0=4.0, K=100, T=33, ar_alpha=0.0,
+                       desc="1920x1080 RGB, 8 frames/GPU per step, D/r0=4, Z=36, K=100 bases 33x33"),
+    "cfg5_4k": dict(H=2160, W=3840, C=3, F=2, d_over_r0=5.0, K=100, T=33, ar_alpha=0.0,
+                    desc="3840x2160 RGB, 2 frames/GPU per step, D/r0=5, Z=36, K=100 bases 33x33"),
+    "cfg2_256": dict(H=256, W=256, C=1, F=100, d_over_r0=3.0, K=100, T=33, ar_alpha=0.95,
+                     desc="256x256 gray, 100-frame AR(0.95) sequence, D/r0=3, K=100 bases 33x33"),
+}
+
+
+def algorithmic_work(w, Z=36, hidden=(100, 100)):
+    """Per-launch algorithmic bytes / flops of each kernel for a batch of F frames."""
+    H, W, C, F, K, T = w["H"], w["W"], w["C"], w["F"], w["K"], w["T"]
+    HW = H * W
+    PQ = HW  # pad = 1 and every config size is 5-smooth
+    npairs = (Z - 1 + 1) // 2
+    nslots = Z - 1
+    n3 = (K + 15) // 16 * 16
+    nin = Z - 3
+    return {
+        # sqrt(S) read once per batch + complex row-transformed spectrum written per frame
+        "k_rows": ("hbm", npairs * PQ * 8 + F * npairs * PQ * 8),
+        # spectrum read, bf16 field planes + fp32 tilt planes written
+        "k_cols": ("hbm", F * (npairs * PQ * 8 + nslots * HW * 2 + 2 * HW * 4)),
+        # tilt planes + broadcast image read, bf16 warped planes written
+        "k_warp": ("hbm", F * (2 * HW * 4 + C * HW * 2) + C * HW * 4),
+        # 2 HW (33*100 + 100*100 + 100*K) flops (SURVEY 8(d) MLP count)
+        "k_mlp": ("tensor", F * 2 * HW * (nin * hidden[0] + hidden[0] * hidden[1] + hidden[1] * K)),
+        # direct Eq.9: 2 HW C K T^2 flops
+        "k_blur": ("tensor", F * 2 * HW * C * K * T * T),
+    }
+
+
+def oracle_sample(w, n_blur_px=2048, seed=SEED, frame=0):
+    """Bounded oracle sample: steps 1-3 and 5 on one full frame, step 4 (Eq.9) on
+    n_blur_px pixels scaled to the frame.  Returns (frame seconds, description)."""
+    import synth
+    from oracle import optics, pipeline
+    H, W, C, K, T, Z = w["H"], w["W"], w["C"], w["K"], w["T"], 36
+    basis = synth.basis(K, T, seed=0)
+    layers = synth.unpack_mlp(synth.mlp_weights(K, seed=0), K)
+    img = synth.image(H, W, C, seed=0).astype(np.float64)
+    A0 = optics.noll_covariance(Z, w["d_over_r0"])
+    L = optics.noll_cholesky(A0)
+    sq = np.ones((Z - 1, H, W))  # timing only: plan tables are off the clock in both arms
+    kappa = optics.geometry()[1]
+    t0 = time.perf_counter()
+    eta = pipeline.white_spectral_noise(seed, frame, H, W, Z)
+    a = pipeline.mix(pipeline.fields_from_noise(eta, sq, H, W), L)
+    Iw = pipeline.warp(img, a[1], a[2], kappa)
+    wts = pipeline.mlp(a[3:], layers)
+    t1 = time.perf_counter()
+    rng = np.random.default_rng(0)
+    ys = rng.integers(0, H, n_blur_px)
+    xs = rng.integers(0, W, n_blur_px)
+    pipeline.blur_at(Iw, wts[:, ys, xs].T, basis, ys, xs)
+    t2 = time.perf_counter()
+    pipeline.step5(np.zeros((C, H, W)), wts, basis, seed, frame, sigma=0.0)
+    t3 = time.perf_counter()
+    frame_s = (t1 - t0) + (t2 - t1) * (H * W / n_blur_px) + (t3 - t2)
+    desc = (f"oracle (fp64 numpy) steps 1-3+5 on one full {H}x{W}x{C} frame, Eq.9 blur on {n_blur_px} "
+            f"random pixels x{H * W // n_blur_px} scaled; sqrt(S) tables not timed")
+    return frame_s, desc
+
+
+def oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [d.get("num_threads", 1) for d in threadpool_info()]
+        return max(n) if n else 1
+    except Exception:
+        return 1
+
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return
+    times = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        s, desc = oracle_sample(w, frame=i)
+        if i >= args.warmup:
+            times.append(s)
+    fps = 1.0 / statistics.mean(times)
+    cores = oracle_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(w, args, world),
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(w, args, world):
+    return {"workload": f"{args.workload}: {w['desc']}", "H": w["H"], "W": w["W"], "C": w["C"],
+            "frames_per_gpu_per_step": w["F"], "global_batch": w["F"] * world, "d_over_r0": w["d_over_r0"],
+            "Z": 36, "K": w["K"], "T": w["T"], "mlp": f"33-100-100-{w['K']}", "ar_alpha": w["ar_alpha"],
+            "parallelism": f"frames dp{world}", "l2": "no flush: per-step working set "
+            "(spectrum + fields + weights, GBs) far exceeds the 126 MB L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3_512", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    w = dict(WORKLOADS[args.workload])
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, w, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import synth
+    from paper_2210_06713_b200 import Plan, PlanConfig
+
+    H, W, C, F, K, T = w["H"], w["W"], w["C"], w["F"], w["K"], w["T"]
+    basis = synth.basis(K, T, seed=0)
+    mlp = synth.mlp_weights(K, seed=0)
+    img_np = synth.image(H, W, C, seed=0)
+    plan = Plan(PlanConfig(H=H, W=W, C=C, d_over_r0=w["d_over_r0"], K=K, taps=T, ar_alpha=w["ar_alpha"],
+                           max_batch=F, device=local), basis, mlp)
+    dev = torch.device("cuda", local)
+    img = torch.from_numpy(img_np).to(dev)
+    out = torch.empty((F, C, H, W), device=dev)
+    stream = torch.cuda.current_stream()
+
+    def frame0(step):
+        return step * world * F + rank * F
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for s in range(args.warmup):
+        plan.simulate_frames(img, 0, SEED, frame0(s), F, out)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    plan.stage_timing(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for s in range(args.steps):
+        plan.simulate_frames(img, 0, SEED, frame0(args.warmup + s), F, out)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    stages = plan.stage_times()
+    plan.stage_timing(False)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * F * args.steps / (ms_max / 1e3)
+
+    # ---- end to end through the host-buffer C-ABI entry point (pinned buffers)
+    e2e = None
+    if not args.no_e2e:
+        img_h = torch.from_numpy(img_np).pin_memory().numpy()
+        out_h = torch.empty((F, C, H, W), dtype=torch.float32).pin_memory().numpy()
+        plan.simulate_frames_host(img_h, 0, SEED, frame0(0), F, out_h)
+        barrier()
+        te0 = time.perf_counter()
+        for s in range(args.steps):
+            plan.simulate_frames_host(img_h, 0, SEED, frame0(args.warmup + s), F, out_h)
+        te = time.perf_counter() - te0
+        tt = torch.tensor([te], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * F * args.steps / float(tt.item()), "unit": "frames/s",
+               "h2d_bytes_per_step": int(img_np.nbytes), "d2h_bytes_per_step": int(out_h.nbytes),
+               "api": "p2s_simulate_frames_host (pinned host buffers, wall clock, max over ranks)"}
+
+    if rank == 0:
+        peaks = load_peaks()
+        work = algorithmic_work(w)
+        st = {}
+        for name, (kind, amount) in work.items():
+            tot_ms, n = stages[name]
+            per = tot_ms / max(n, 1)
+            if kind == "hbm":
+                ach = amount / (per / 1e3) / 1e9
+                peak = peaks["hbm_gbs"]
+                st[name] = {"ms_per_launch": per, "launches": n, "bound": "hbm", "bytes_per_launch": amount,
+                            "achieved": ach, "unit": "GB/s", "peak": peak, "frac": ach / peak}
+            else:
+                ach = amount / (per / 1e3) / 1e12
+                peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+                st[name] = {"ms_per_launch": per, "launches": n, "bound": "tensor", "flops_per_launch": amount,
+                            "achieved": ach, "unit": "TFLOP/s", "peak": peak, "frac": ach / peak}
+            st[name]["share_of_step"] = tot_ms / ms if ms > 0 else None
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(args.workload, {}).get("k_blur")
+        b = st["k_blur"]
+        roofline = {"kernel": "k_blur (Eq.9 implicit GEMM, tcgen05)", "bound": "tensor", "achieved": b["achieved"],
+                    "peak": b["peak"], "unit": "TFLOP/s", "frac": b["frac"], "traffic": traffic,
+                    "work": "2*H*W*C*K*T^2 flop/frame (direct Eq.9)",
+                    "peak_source": peaks["source"] + " bf16 sustained (kernel inside a long step)"}
+        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32 field / bf16 tensor (f32 acc)",
+                "data": "synthetic", "config": config_dict(w, args, world), "clocks": clocks,
+                "e2e": e2e, "gpu_launches": int(sum(n for _, n in stages.values())), "roofline": roofline,
+                "stages": st}
+        if world == 1 and not args.no_cpu_baseline:
+            s, desc = oracle_sample(w)
+            line["cpu_baseline"] = {"value": 1.0 / s, "unit": "frames/s", "cores": oracle_threads(),
+                                    "kind": "oracle", "sample": desc}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

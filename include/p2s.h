@@ -152,6 +152,16 @@ p2s_status p2s_plan_info(p2s_plan p, int* P, int* Q, size_t* workspace_bytes,
  *   sqrtS float  [Z-1][P][Q] sqrt(S_j) for j = 2..Z (sum S_j = P*Q) */
 p2s_status p2s_plan_export_tables(p2s_plan p, double* A0, double* chol, float* sqrtS);
 
+/* Per-stage device timing of the fused path (measurement support).
+ * p2s_plan_stage_timing(p, 1) starts recording a CUDA event pair around every kernel
+ * launch that p2s_simulate_frames enqueues (on the caller's stream) and clears the
+ * accumulators; 0 stops.  p2s_plan_stage_times synchronises on the recorded events and
+ * returns, per stage, the summed kernel time in ms and the number of launches:
+ * index 0 k_rows (noise+PSD+row IDFT), 1 k_cols (column IDFT), 2 k_warp, 3 k_mlp,
+ * 4 k_blur.  ms and launches are arrays of length 5 (nullable). */
+p2s_status p2s_plan_stage_timing(p2s_plan p, int enable);
+p2s_status p2s_plan_stage_times(p2s_plan p, double* ms, int64_t* launches);
+
 /* Replace the plan's sqrt(S_j) (host float [Z-1][P][Q], same layout as export). */
 p2s_status p2s_plan_import_sqrtS(p2s_plan p, const float* sqrtS);
 

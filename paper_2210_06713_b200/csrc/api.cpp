@@ -222,8 +222,11 @@ static p2s_status alloc_workspace(p2s_plan_s* p) {
   return P2S_OK;
 }
 
+static void clear_timing(p2s_plan_s* p);
+
 static void free_plan(p2s_plan_s* p) {
   if (!p) return;
+  clear_timing(p);
   cudaFree(p->d_sqrtS);
   cudaFree(p->d_ar);
   cudaFree(p->d_L);
@@ -257,10 +260,39 @@ static int ar_mode_for(p2s_plan_s* p, uint64_t seed, int64_t frame0) {
   return frame0 == 0 ? 1 : 2;
 }
 
+// Event pair around one launch when stage timing is on.
+struct StageScope {
+  p2s_plan_s* p;
+  cudaStream_t s;
+  cudaEvent_t b = nullptr, e = nullptr;
+  StageScope(p2s_plan_s* p_, int stage, cudaStream_t s_) : p(p_), s(s_) {
+    if (!p->timing) return;
+    cudaEventCreate(&b);
+    cudaEventCreate(&e);
+    cudaEventRecord(b, s);
+    p->t_stage.push_back(stage);
+  }
+  ~StageScope() {
+    if (!p->timing) return;
+    cudaEventRecord(e, s);
+    p->t_ev.push_back(b);
+    p->t_ev.push_back(e);
+  }
+};
+
+static void clear_timing(p2s_plan_s* p) {
+  for (cudaEvent_t ev : p->t_ev) cudaEventDestroy(ev);
+  p->t_ev.clear();
+  p->t_stage.clear();
+}
+
 static p2s_status run_step1(p2s_plan_s* p, uint64_t seed, int64_t f0, int F, cudaStream_t s) {
   const bool ar = p->ar_alpha != 0.f;
   int mode = ar ? ar_mode_for(p, seed, f0) : 1;
-  P2S_LAUNCH(launch_rows(p, seed, f0, F, ar, mode, mode == 2 ? 0 : f0, s), "k_rows");
+  {
+    StageScope sc(p, 0, s);
+    P2S_LAUNCH(launch_rows(p, seed, f0, F, ar, mode, mode == 2 ? 0 : f0, s), "k_rows");
+  }
   if (ar) {
     p->ar_valid = true;
     p->ar_seed = seed;
@@ -503,10 +535,22 @@ extern "C" p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t 
     const int F = std::min(p->max_batch, nframes - i0);
     p2s_status st = run_step1(p, seed, frame0 + i0, F, s);
     if (st != P2S_OK) return st;
-    P2S_LAUNCH(launch_cols(p, F, 1, nullptr, s), "k_cols");
-    P2S_LAUNCH(launch_warp_sim(p, F, img + (size_t)i0 * img_frame_stride, img_frame_stride, s), "k_warp");
-    P2S_LAUNCH(launch_mlp(p, F, true, s), "k_mlp");
-    P2S_LAUNCH(launch_blur(p, F, p->d_Iw, false, seed, frame0 + i0, out + (size_t)i0 * p->C * HW, s), "k_blur");
+    {
+      StageScope sc(p, 1, s);
+      P2S_LAUNCH(launch_cols(p, F, 1, nullptr, s), "k_cols");
+    }
+    {
+      StageScope sc(p, 2, s);
+      P2S_LAUNCH(launch_warp_sim(p, F, img + (size_t)i0 * img_frame_stride, img_frame_stride, s), "k_warp");
+    }
+    {
+      StageScope sc(p, 3, s);
+      P2S_LAUNCH(launch_mlp(p, F, true, s), "k_mlp");
+    }
+    {
+      StageScope sc(p, 4, s);
+      P2S_LAUNCH(launch_blur(p, F, p->d_Iw, false, seed, frame0 + i0, out + (size_t)i0 * p->C * HW, s), "k_blur");
+    }
   }
   return P2S_OK;
 }
@@ -549,6 +593,34 @@ extern "C" p2s_status p2s_plan_info(p2s_plan p, int* P, int* Q, size_t* ws, doub
   if (ws) *ws = p->ws_bytes;
   if (clamped) *clamped = p->clamped_max;
   if (max_batch) *max_batch = p->max_batch;
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_plan_stage_timing(p2s_plan p, int enable) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  DeviceGuard guard(p->device);
+  clear_timing(p);
+  p->timing = enable != 0;
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_plan_stage_times(p2s_plan p, double* ms, int64_t* launches) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  DeviceGuard guard(p->device);
+  double acc[5] = {0, 0, 0, 0, 0};
+  int64_t cnt[5] = {0, 0, 0, 0, 0};
+  for (size_t i = 0; i < p->t_stage.size(); ++i) {
+    cudaEvent_t b = p->t_ev[2 * i], e = p->t_ev[2 * i + 1];
+    P2S_CUDA(cudaEventSynchronize(e), "cudaEventSynchronize");
+    float t = 0.f;
+    P2S_CUDA(cudaEventElapsedTime(&t, b, e), "cudaEventElapsedTime");
+    acc[p->t_stage[i]] += t;
+    cnt[p->t_stage[i]] += 1;
+  }
+  for (int k = 0; k < 5; ++k) {
+    if (ms) ms[k] = acc[k];
+    if (launches) launches[k] = cnt[k];
+  }
   return P2S_OK;
 }
 

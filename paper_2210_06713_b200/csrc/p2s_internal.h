@@ -91,6 +91,10 @@ struct p2s_plan_s {
   uint16_t* d_w = nullptr;      // bf16 [mb][H*W][n3]
   float* d_img = nullptr;       // staging for the host entry point [mb][C][H][W]
   float* d_out = nullptr;       // staging for the host entry point [mb][C][H][W]
+  // per-stage timing (p2s_plan_stage_timing)
+  bool timing = false;
+  std::vector<int> t_stage;
+  std::vector<cudaEvent_t> t_ev;  // pairs
   // AR bookkeeping
   bool ar_valid = false;
   uint64_t ar_seed = 0;

@@ -22,7 +22,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NUMERIC", 3: "CUDA", 4: "OUT_OF_M
 # every entry point declared in include/p2s.h
 EXPORTS = ("p2s_plan_create", "p2s_plan_destroy", "p2s_sample_zernike", "p2s_warp", "p2s_blur",
            "p2s_simulate_frames", "p2s_simulate_frames_host", "p2s_last_error", "p2s_plan_info",
-           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_philox_fill", "p2s_host_tables",
+           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_philox_fill", "p2s_host_tables",
            "p2s_grid_size")
 
 
@@ -59,6 +59,8 @@ def _load():
                                   ctypes.POINTER(i32)]
     lib.p2s_plan_export_tables.argtypes = [vp, vp, vp, vp]
     lib.p2s_plan_import_sqrtS.argtypes = [vp, vp]
+    lib.p2s_plan_stage_timing.argtypes = [vp, i32]
+    lib.p2s_plan_stage_times.argtypes = [vp, vp, vp]
     lib.p2s_philox_fill.argtypes = [u32, u32, u32, u32, u32, i64, vp, vp]
     lib.p2s_host_tables.argtypes = [i32, i32, ctypes.c_double, ctypes.c_double, i32, vp, vp, vp, vp]
     lib.p2s_grid_size.argtypes = [i32]
@@ -208,6 +210,18 @@ class Plan:
         sq = np.zeros((Z - 1, P, Q), dtype=np.float32)
         _check(lib.p2s_plan_export_tables(self._h, A0.ctypes.data, L.ctypes.data, sq.ctypes.data))
         return A0, L, sq
+
+    STAGES = ("k_rows", "k_cols", "k_warp", "k_mlp", "k_blur")
+
+    def stage_timing(self, enable: bool):
+        _check(lib.p2s_plan_stage_timing(self._h, int(enable)))
+
+    def stage_times(self):
+        """{stage: (ms summed over launches, launches)} since stage_timing(True)."""
+        ms = np.zeros(5)
+        n = np.zeros(5, dtype=np.int64)
+        _check(lib.p2s_plan_stage_times(self._h, ms.ctypes.data, n.ctypes.data))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(self.STAGES)}
 
     def import_sqrtS(self, sqrtS: np.ndarray):
         sq = np.ascontiguousarray(sqrtS, dtype=np.float32)
