@@ -25,8 +25,7 @@ namespace p2s {
 
 constexpr int kBlurStages = 6;
 constexpr int kBlurThreads = 192;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue
-constexpr int kRowsInFlight = 4;
-constexpr int kAccStride = 128;    // TMEM columns per accumulator row
+constexpr int kAccStride = 128;    // TMEM columns per accumulator
 
 struct BlurArgs {
   const void* src;          // Iw [F][C][H][W] (bf16 or fp32)
@@ -36,7 +35,7 @@ struct BlurArgs {
   const uint32_t* koff;     // [nks]
   const uint32_t* klbo;     // [nks]
   const float* hsum;        // [np]
-  int C, H, W, T, c, NC, RB, RS, nks, np;
+  int C, H, W, T, c, NC, RB, RS, nks, np, racc;
   uint32_t k0, k1;
   int64_t frame0;
   float sigma;
@@ -55,24 +54,45 @@ __device__ __forceinline__ float load_src(const void* src, size_t idx) {
   return bf16_to_f(__ldg(reinterpret_cast<const uint16_t*>(src) + idx));
 }
 
+struct BlurSmem {
+  uint32_t tile_bytes, w_bytes, b_bytes;
+  uint32_t off_w, off_ring, off_koff, off_klbo, off_hsum, off_bar, total;
+};
+
+__host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int racc, int np, int nks) {
+  BlurSmem L;
+  L.tile_bytes = ((uint32_t)NC * RS * 16 + 127) & ~127u;
+  L.w_bytes = (uint32_t)racc * 128 * np * 2;
+  if (L.w_bytes < 6u * 176 * 4) L.w_bytes = 6u * 176 * 4;  // doubles as the loader's staging rows
+  L.b_bytes = (uint32_t)np * 32;
+  L.off_w = C * L.tile_bytes;
+  L.off_ring = (L.off_w + L.w_bytes + 127) & ~127u;
+  L.off_koff = L.off_ring + kBlurStages * L.b_bytes;
+  L.off_klbo = L.off_koff + 4 * nks;
+  L.off_hsum = L.off_klbo + 4 * nks;
+  L.off_bar = (L.off_hsum + 4 * np + 15) & ~15u;
+  L.total = L.off_bar + (2 * kBlurStages + 3) * 8 + 16;
+  return L;
+}
+
 template <bool SRC_F32>
 __global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const BlurSmem L = blur_smem_layout(a.C, a.NC, a.RS, a.racc, a.np, a.nks);
   const uint32_t sbo_src = (uint32_t)a.RS * 16;
-  uint8_t* tile = smem;
-  const uint32_t tile_bytes = ((uint32_t)a.NC * sbo_src + 127) & ~127u;
-  const uint32_t bbytes = (uint32_t)a.np * 32;
-  uint8_t* ring = tile + tile_bytes;
-  uint32_t* s_koff = reinterpret_cast<uint32_t*>(ring + kBlurStages * bbytes);
-  uint32_t* s_klbo = s_koff + a.nks;
-  float* s_hsum = reinterpret_cast<float*>(s_klbo + a.nks);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(((uintptr_t)(s_hsum + a.np) + 7) & ~(uintptr_t)7);
+  uint8_t* wbuf = smem + L.off_w;
+  uint8_t* ring = smem + L.off_ring;
+  uint32_t* s_koff = reinterpret_cast<uint32_t*>(smem + L.off_koff);
+  uint32_t* s_klbo = reinterpret_cast<uint32_t*>(smem + L.off_klbo);
+  float* s_hsum = reinterpret_cast<float*>(smem + L.off_hsum);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
   uint64_t* full = bars;
   uint64_t* empty = bars + kBlurStages;
   uint64_t* tfull = bars + 2 * kBlurStages;
   uint64_t* tempty = tfull + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* wfull = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(wfull + 1);
 
   const int x0 = blockIdx.x * 128, y0 = blockIdx.y * a.RB, f = blockIdx.z;
   const int HW = a.H * a.W;
@@ -89,133 +109,162 @@ __global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 128);
+    mbar_init(wfull, 1);
     mbar_fence_init();
   }
   if (warp == 0) tmem_alloc(tslot, 512);
+
+  // ---- source tiles of every channel: chunk cc of row rl holds the 8 pixels at window
+  // offsets cc + 16 j of source row y0 - c + rl (mirror boundary).  Each warp stages a
+  // coalesced row segment in smem, then packs the chunks.
+  {
+    float* stg = reinterpret_cast<float*>(wbuf) + warp * 176;
+    const int rows_real = a.RB + a.T - 1;
+    const int seg = 128 + a.T - 1;
+    for (int ch = 0; ch < a.C; ++ch) {
+      uint8_t* tile = smem + ch * L.tile_bytes;
+      const size_t plane = ((size_t)f * a.C + ch) * HW;
+      for (int rl = warp; rl < a.RS; rl += kBlurThreads / 32) {
+        const bool real = rl < rows_real;
+        if (real) {
+          const size_t rowb = plane + (size_t)reflect_idx(y0 - a.c + rl, a.H) * a.W;
+          for (int i = lane; i < seg; i += 32) stg[i] = load_src<SRC_F32>(a.src, rowb + reflect_idx(x0 - a.c + i, a.W));
+        }
+        __syncwarp();
+        for (int cc = lane; cc < a.NC; cc += 32) {
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (real)
+            v = make_uint4(pack_bf16x2(stg[cc], stg[cc + 16]), pack_bf16x2(stg[cc + 32], stg[cc + 48]),
+                           pack_bf16x2(stg[cc + 64], stg[cc + 80]), pack_bf16x2(stg[cc + 96], stg[cc + 112]));
+          *reinterpret_cast<uint4*>(tile + (size_t)cc * sbo_src + rl * 16) = v;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
-  const uint32_t idesc = umma_idesc_bf16(128, a.np, true, false);
-  const uint32_t s_tile = smem_u32(tile);
-  uint32_t p_stage = 0, p_phase = 0;  // producer ring position
-  uint32_t m_stage = 0, m_phase = 0;  // MMA ring position
-  uint32_t rg_count = 0;
-  const int n_rg = a.RB / kRowsInFlight;
+  const int n_rg = (a.RB + a.racc - 1) / a.racc;
+  const int nacc = a.C * a.racc;
+  const int valid_px = min(128, a.W - x0);
 
-  for (int ch = 0; ch < a.C; ++ch) {
-    // ---- source tile: chunk cc, row rl <- pixels (x0 - c + cc + 16 j, y0 - c + rl), mirror boundary
-    const size_t plane = ((size_t)f * a.C + ch) * HW;
-    const int rows_real = a.RB + a.T - 1;
-    for (int idx = tid; idx < a.NC * a.RS; idx += kBlurThreads) {
-      const int cc = idx / a.RS, rl = idx - cc * a.RS;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (rl < rows_real) {
-        const int sy = reflect_idx(y0 - a.c + rl, a.H);
-        const size_t rowb = plane + (size_t)sy * a.W;
-        float e[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) e[j] = load_src<SRC_F32>(a.src, rowb + reflect_idx(x0 - a.c + cc + 16 * j, a.W));
-        v = make_uint4(pack_bf16x2(e[0], e[1]), pack_bf16x2(e[2], e[3]), pack_bf16x2(e[4], e[5]),
-                       pack_bf16x2(e[6], e[7]));
-      }
-      *reinterpret_cast<uint4*>(tile + (size_t)cc * sbo_src + rl * 16) = v;
-    }
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-
-    if (warp == 0) {
-      if (lane == 0) {  // ---- TMA producer: B tiles of every K-step, once per row group
-        for (int rg = 0; rg < n_rg; ++rg)
-          for (int t = 0; t < a.nks; ++t) {
-            mbar_wait(&empty[p_stage], p_phase ^ 1);
-            mbar_arrive_expect_tx(&full[p_stage], bbytes);
-            bulk_g2s(ring + p_stage * bbytes, a.bimg + (size_t)t * bbytes, bbytes, &full[p_stage]);
-            if (++p_stage == kBlurStages) {
-              p_stage = 0;
-              p_phase ^= 1;
-            }
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer: per row group the w rows, then the B tile of every K-step
+      uint32_t stage = 0, phase = 0;
+      const uint32_t bbytes = L.b_bytes;
+      for (int rg = 0; rg < n_rg; ++rg) {
+        mbar_wait(tempty, (rg & 1) ^ 1);  // epilogue finished with wbuf (and TMEM) of rg-1
+        uint32_t wb = 0;
+        for (int r = 0; r < a.racc; ++r) wb += (y0 + rg * a.racc + r < a.H) ? (uint32_t)valid_px * a.np * 2 : 0;
+        mbar_arrive_expect_tx(wfull, wb);
+        for (int r = 0; r < a.racc; ++r) {
+          const int y = y0 + rg * a.racc + r;
+          if (y < a.H)
+            bulk_g2s(wbuf + (size_t)r * 128 * a.np * 2, a.w + ((size_t)f * HW + (size_t)y * a.W + x0) * a.np,
+                     (uint32_t)valid_px * a.np * 2, wfull);
+        }
+        for (int t = 0; t < a.nks; ++t) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], bbytes);
+          bulk_g2s(ring + stage * bbytes, a.bimg + (size_t)t * bbytes, bbytes, &full[stage]);
+          if (++stage == kBlurStages) {
+            stage = 0;
+            phase ^= 1;
           }
-      }
-    } else if (warp == 1) {
-      if (lane == 0) {  // ---- MMA issuer
-        for (int rg = 0; rg < n_rg; ++rg) {
-          mbar_wait(tempty, (rg_count & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t arow = s_tile + (uint32_t)(rg * kRowsInFlight) * 16;
-          for (int t = 0; t < a.nks; ++t) {
-            mbar_wait(&full[m_stage], m_phase);
-            tc_fence_after();
-            const uint64_t bdesc = umma_desc(smem_u32(ring + m_stage * bbytes), 128, 256);
-            const uint32_t ko = s_koff[t], lbo = s_klbo[t];
-#pragma unroll
-            for (int r = 0; r < kRowsInFlight; ++r)
-              umma_bf16(tmem + r * kAccStride, umma_desc(arow + r * 16 + ko, lbo, sbo_src), bdesc, idesc, t > 0);
-            umma_commit(&empty[m_stage]);
-            if (++m_stage == kBlurStages) {
-              m_stage = 0;
-              m_phase ^= 1;
-            }
-          }
-          umma_commit(tfull);
-          ++rg_count;
         }
       }
-    } else {  // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
-      const int qd = warp & 3;
-      const int m = qd * 32 + lane;
-      const int x = x0 + 16 * (m & 7) + (m >> 3);
-      const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer: every K-step feeds C x racc accumulators
+      const uint32_t idesc = umma_idesc_bf16(128, a.np, true, false);
+      const uint32_t s_tile = smem_u32(smem);
+      uint32_t stage = 0, phase = 0;
       for (int rg = 0; rg < n_rg; ++rg) {
-        mbar_wait(tfull, rg_count & 1);
+        mbar_wait(tempty, (rg & 1) ^ 1);
         tc_fence_after();
-        for (int r = 0; r < kRowsInFlight; ++r) {
-          const int y = y0 + rg * kRowsInFlight + r;
-          const bool valid = (y < a.H) && (x < a.W);
-          const uint16_t* wrow = a.w + ((size_t)f * HW + (size_t)(valid ? y : 0) * a.W + (valid ? x : 0)) * a.np;
-          float acc = 0.f, g = 0.f;
-          for (int cb = 0; cb < a.np / 16; ++cb) {
-            float v[16];
-            tmem_ld16(tl + r * kAccStride + cb * 16, v);
-            if (valid) {
-              const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(wrow + cb * 16));
-              const uint4 w1 = __ldg(reinterpret_cast<const uint4*>(wrow + cb * 16 + 8));
-              const uint32_t wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        const uint32_t arow = s_tile + (uint32_t)(rg * a.racc) * 16;
+        for (int t = 0; t < a.nks; ++t) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t bdesc = umma_desc(smem_u32(ring + stage * L.b_bytes), 128, 256);
+          const uint32_t ko = s_koff[t], lbo = s_klbo[t];
+          for (int ch = 0; ch < a.C; ++ch)
+            for (int r = 0; r < a.racc; ++r)
+              umma_bf16(tmem + (ch * a.racc + r) * kAccStride,
+                        umma_desc(arow + ch * L.tile_bytes + r * 16 + ko, lbo, sbo_src), bdesc, idesc, t > 0);
+          umma_commit(&empty[stage]);
+          if (++stage == kBlurStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(tfull);
+      }
+    }
+  } else {  // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
+    const int qd = warp & 3;
+    const int m = qd * 32 + lane;
+    const int q = 16 * (m & 7) + (m >> 3);
+    const int x = x0 + q;
+    const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
+    for (int rg = 0; rg < n_rg; ++rg) {
+      mbar_wait(tfull, rg & 1);
+      mbar_wait(wfull, rg & 1);
+      tc_fence_after();
+      for (int r = 0; r < a.racc; ++r) {
+        const int y = y0 + rg * a.racc + r;
+        const bool valid = (y < a.H) && (x < a.W);
+        const uint8_t* wrow = wbuf + ((size_t)r * 128 + q) * a.np * 2;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        float g = 0.f;
+        for (int cb = 0; cb < a.np / 16; ++cb) {
+          const uint4 w0 = *reinterpret_cast<const uint4*>(wrow + cb * 32);
+          const uint4 w1 = *reinterpret_cast<const uint4*>(wrow + cb * 32 + 16);
+          const uint32_t wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+          float wf[16];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const float wa = bf16_lo(wv[i]), wb = bf16_hi(wv[i]);
-                acc = fmaf(wa, v[2 * i], acc);
-                acc = fmaf(wb, v[2 * i + 1], acc);
-                g = fmaf(wa, s_hsum[cb * 16 + 2 * i], g);
-                g = fmaf(wb, s_hsum[cb * 16 + 2 * i + 1], g);
-              }
+          for (int i = 0; i < 8; ++i) {
+            wf[2 * i] = bf16_lo(wv[i]);
+            wf[2 * i + 1] = bf16_hi(wv[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) g = fmaf(wf[i], s_hsum[cb * 16 + i], g);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (ch < a.C) {
+              float v[16];
+              tmem_ld16(tl + (ch * a.racc + r) * kAccStride + cb * 16, v);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) acc[ch] = fmaf(wf[i], v[i], acc[ch]);
             }
           }
-          if (valid) {
-            float o = acc;
+        }
+        if (valid) {
+          for (int ch = 0; ch < a.C; ++ch) {
+            float o = acc[ch];
             if (a.normalize) o = o / g;
             if (a.sigma != 0.f) {
               const int64_t fr = a.frame0 + f;
-              uint4 rx = philox4x32_10(
-                  make_uint4((uint32_t)(y * a.W + x), (uint32_t)ch | (1u << 16), (uint32_t)fr,
-                             (uint32_t)((uint64_t)fr >> 32)),
-                  a.k0, a.k1);
+              uint4 rx = philox4x32_10(make_uint4((uint32_t)(y * a.W + x), (uint32_t)ch | (1u << 16), (uint32_t)fr,
+                                                  (uint32_t)((uint64_t)fr >> 32)),
+                                       a.k0, a.k1);
               o += a.sigma * box_muller(rx.x, rx.y).x;
             }
             if (a.clamp01) o = fminf(fmaxf(o, 0.f), 1.f);
             a.out[((size_t)f * a.C + ch) * HW + (size_t)y * a.W + x] = o;
           }
         }
-        tc_fence_before();
-        mbar_arrive(tempty);
-        ++rg_count;
       }
+      tc_fence_before();
+      mbar_arrive(tempty);
     }
-    __syncthreads();  // channel done: all MMAs retired (epilogue saw the last tfull)
   }
+  (void)nacc;
+  __syncthreads();
   tc_fence_after();
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
@@ -241,18 +290,17 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.RS = g.RS;
   a.nks = g.nks;
   a.np = g.np;
+  a.racc = g.racc;
   a.k0 = (uint32_t)seed;
   a.k1 = (uint32_t)(seed >> 32);
   a.frame0 = frame0;
   a.sigma = p->noise_sigma;
   a.normalize = p->normalize;
   a.clamp01 = p->clamp01;
-  size_t tile_bytes = ((size_t)g.NC * g.RS * 16 + 127) & ~(size_t)127;
-  size_t sm = tile_bytes + kBlurStages * (size_t)g.np * 32 + (size_t)g.nks * 8 + g.np * 4 + 8 +
-              (2 * kBlurStages + 2) * 8 + 16;
+  const BlurSmem L = blur_smem_layout(a.C, a.NC, a.RS, a.racc, a.np, a.nks);
   // TMEM: this kernel owns all 512 columns of its SM; keep shared memory above half the SM
   // so that two CTAs never co-reside and contend for tcgen05.alloc.
-  if (sm < 116 * 1024) sm = 116 * 1024;
+  size_t sm = L.total < 116 * 1024 ? 116 * 1024 : L.total;
   dim3 grid((p->W + 127) / 128, (p->H + g.RB - 1) / g.RB, F);
   if (src_f32) {
     cudaFuncSetAttribute(k_blur<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -262,6 +310,17 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
     k_blur<false><<<grid, kBlurThreads, sm, s>>>(a);
   }
   return (int)cudaGetLastError();
+}
+
+// Host helper: rows per CTA that fit the shared-memory budget for this geometry.
+int blur_rows_per_cta(int C, int T, int np, int racc, int nks) {
+  const int NC = T + 15, G = (T + 7) / 8;
+  int best = racc;
+  for (int RB = racc; RB <= 64; RB += racc) {
+    const int RS = RB + 8 * G + 8;
+    if (blur_smem_layout(C, NC, RS, racc, np, nks).total <= 227 * 1024) best = RB;
+  }
+  return best;
 }
 
 }  // namespace p2s

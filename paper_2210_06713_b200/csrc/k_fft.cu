@@ -89,19 +89,52 @@ __device__ __forceinline__ void dft_inv<5>(float2* v) {
   v[3] = make_float2(a2.x + b2.y, a2.y - b2.x);
 }
 
-// One Stockham pass of radix R over TC interleaved sequences of length N:
-// element i of sequence c lives at x[i*TC + c].  Ns = product of earlier radices.
-template <int R>
-__device__ __forceinline__ void stockham_pass(const float2* __restrict__ x, float2* __restrict__ y, int N, int Ns,
-                                              int tc_log2, const float2* __restrict__ tw) {
+// ------------------------------------------------------------------ shared-memory Stockham IDFT
+// TC interleaved sequences of length N live in shared memory, element i of sequence c at
+// x[i*TC + c] (TC = 2^tc_log2).  Out-of-place (ping-pong) passes of radix 8/4/2/3/5; the
+// divisions by Ns (product of earlier radices) use a multiply-high magic number.
+constexpr int kColElems = 4608;  // P * TC per column CTA (2 x 36 KB ping-pong)
+
+struct FFTArgs {
+  int N;
+  int nrad;
+  int rad[kMaxRadix];
+  uint32_t magic[kMaxRadix];  // floor(2^32 / Ns) + 1 of each pass (0 when Ns == 1)
+  const float2* tw;           // e^{+2 pi i k / N}
+};
+
+// The radix plan is staged in shared memory so the kernel-parameter struct is never
+// addressed dynamically (which would copy it to local memory).
+struct FFTPlanSmem {
+  int nrad, N;
+  int rad[kMaxRadix];
+  uint32_t magic[kMaxRadix];
+  const float2* tw;
+};
+
+__device__ __forceinline__ void stage_fft_plan(FFTPlanSmem* sp, const FFTArgs& f) {
+  if (threadIdx.x == 0) {
+    sp->nrad = f.nrad;
+    sp->N = f.N;
+    sp->tw = f.tw;
+  }
+  if (threadIdx.x < kMaxRadix) {
+    sp->rad[threadIdx.x] = f.rad[threadIdx.x];
+    sp->magic[threadIdx.x] = f.magic[threadIdx.x];
+  }
+}
+
+template <int R, int NT>
+__device__ __forceinline__ void ifft_pass(const float2* __restrict__ x, float2* __restrict__ y, int N, int Ns,
+                                          uint32_t mag, int tc_log2, const float2* __restrict__ tw) {
   const int NR = N / R;
-  const int TC = 1 << tc_log2;
+  const int TC1 = (1 << tc_log2) - 1;
   const int total = NR << tc_log2;
   const int ts = N / (Ns * R);
-  for (int w = threadIdx.x; w < total; w += blockDim.x) {
-    const int c = w & (TC - 1);
-    const int j = w >> tc_log2;
-    const int k = j % Ns;
+  for (int w = threadIdx.x; w < total; w += NT) {
+    const int c = w & TC1, j = w >> tc_log2;
+    const int q = Ns == 1 ? j : (int)__umulhi((uint32_t)j, mag);
+    const int k = j - q * Ns;
     float2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = x[((j + r * NR) << tc_log2) + c];
@@ -110,30 +143,27 @@ __device__ __forceinline__ void stockham_pass(const float2* __restrict__ x, floa
       for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * k * ts]));
     }
     dft_inv<R>(v);
-    const int base = (j / Ns) * Ns * R + k;
+    const int base = q * Ns * R + k;
 #pragma unroll
-    for (int q = 0; q < R; ++q) y[((base + q * Ns) << tc_log2) + c] = v[q];
+    for (int r = 0; r < R; ++r) y[((base + r * Ns) << tc_log2) + c] = v[r];
   }
 }
 
-struct FFTArgs {
-  int N;
-  int nrad;
-  int rad[kMaxRadix];
-  const float2* tw;
-};
-
-// Inverse DFT (e^{+2 pi i}, unnormalised) in shared memory; returns the buffer holding the result.
-__device__ float2* smem_ifft(float2* a, float2* b, const FFTArgs& f, int tc_log2) {
+// Inverse DFT (e^{+2 pi i}, unnormalised) of TC interleaved sequences, ping-pong between a
+// and b; returns the buffer holding the result.
+template <int NT>
+__device__ __forceinline__ float2* smem_ifft(float2* a, float2* b, const FFTPlanSmem* f, int tc_log2) {
   int Ns = 1;
-  for (int ip = 0; ip < f.nrad; ++ip) {
-    const int R = f.rad[ip];
+  const int nrad = f->nrad;
+  for (int ip = 0; ip < nrad; ++ip) {
+    const int R = f->rad[ip];
+    const uint32_t mg = f->magic[ip];
     switch (R) {
-      case 8: stockham_pass<8>(a, b, f.N, Ns, tc_log2, f.tw); break;
-      case 4: stockham_pass<4>(a, b, f.N, Ns, tc_log2, f.tw); break;
-      case 2: stockham_pass<2>(a, b, f.N, Ns, tc_log2, f.tw); break;
-      case 3: stockham_pass<3>(a, b, f.N, Ns, tc_log2, f.tw); break;
-      default: stockham_pass<5>(a, b, f.N, Ns, tc_log2, f.tw); break;
+      case 8: ifft_pass<8, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 4: ifft_pass<4, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 2: ifft_pass<2, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 3: ifft_pass<3, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
+      default: ifft_pass<5, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
     }
     __syncthreads();
     float2* t = a;
@@ -142,6 +172,21 @@ __device__ float2* smem_ifft(float2* a, float2* b, const FFTArgs& f, int tc_log2
     Ns *= R;
   }
   return a;
+}
+
+static void fill_fft_args(FFTArgs& a, const AxisFFT& ax) {
+  a.N = ax.N;
+  a.nrad = ax.nrad;
+  int Ns = 1;
+  for (int i = 0; i < kMaxRadix; ++i) {
+    a.rad[i] = ax.rad[i];
+    a.magic[i] = 0;
+    if (i < ax.nrad) {
+      a.magic[i] = Ns == 1 ? 0u : (uint32_t)((1ull << 32) / (uint64_t)Ns + 1ull);
+      Ns *= ax.rad[i];
+    }
+  }
+  a.tw = ax.tw;
 }
 
 // ------------------------------------------------------------------ K1: noise + PSD + row IDFT
@@ -176,60 +221,97 @@ __device__ __forceinline__ float4 spectral_noise(int ky, int kx, int P, int Q, i
   return make_float4(ga.x, sg * ga.y, gb.x, sg * gb.y);
 }
 
-template <bool AR>
-__global__ void __launch_bounds__(256) k_rows(RowArgs a) {
+// Y = sa zeta_a + i sb zeta_b
+__device__ __forceinline__ float2 spectrum(float2 s, float4 z) {
+  return make_float2(s.x * z.x - s.y * z.w, s.x * z.y + s.y * z.z);
+}
+
+// White-noise path: one CTA per Hermitian row pair {ky, P-ky}: each Philox draw serves the
+// bin and its mirror (the mirror's noise is the conjugate), the two rows are transformed
+// as two interleaved sequences, and the CTA loops over the frame batch.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int Q = a.Q;
+  float2* sS = reinterpret_cast<float2*>(smem);  // [2][Q]
+  float2* X = sS + 2 * Q;                        // [Q][2] interleaved rows
+  float2* Xb = X + 2 * Q;                        // ping-pong partner
+  __shared__ FFTPlanSmem fpl;
+  stage_fft_plan(&fpl, a.fq);
+  const int ky = blockIdx.x, p = blockIdx.y;
+  const int k1 = ky ? a.P - ky : 0;
+  const size_t plane = (size_t)p * a.P * Q;
+  for (int kx = threadIdx.x; kx < Q; kx += NT) {
+    sS[kx] = a.sqrtS[plane + (size_t)ky * Q + kx];
+    sS[Q + kx] = a.sqrtS[plane + (size_t)k1 * Q + kx];
+  }
+  __syncthreads();
+  for (int t = 0; t < a.F; ++t) {
+    const int64_t fr = a.frame0 + t;
+    for (int kx = threadIdx.x; kx < Q; kx += NT) {
+      const float4 z = spectral_noise(ky, kx, a.P, Q, p, fr, a.k0, a.k1);
+      const int km = kx ? Q - kx : 0;
+      X[2 * kx] = spectrum(sS[kx], z);
+      X[2 * km + 1] = spectrum(sS[Q + km], make_float4(z.x, -z.y, z.z, -z.w));  // mirror bin: conjugate noise
+    }
+    __syncthreads();
+    const float2* R = smem_ifft<NT>(X, Xb, &fpl, 1);
+    float2* dst = a.Zout + (size_t)t * a.npairs * a.P * Q + plane;
+    for (int x = threadIdx.x; x < Q; x += NT) {
+      dst[(size_t)ky * Q + x] = R[2 * x];
+      if (k1 != ky) dst[(size_t)k1 * Q + x] = R[2 * x + 1];
+    }
+    __syncthreads();
+  }
+}
+
+// AR(1) path: one CTA per spectral row with the per-bin state in shared memory;
+// frames are evolved sequentially (including the replay of frames before frame0).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_rows_ar(RowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int Q = a.Q;
   float2* sS = reinterpret_cast<float2*>(smem);
-  float2* b0 = sS + Q;
-  float2* b1 = b0 + Q;
-  float4* st = reinterpret_cast<float4*>(b1 + Q);  // AR state (AR only)
+  float2* X = sS + Q;
+  float2* Xb = X + Q;
+  float4* st = reinterpret_cast<float4*>(Xb + Q);
+  __shared__ FFTPlanSmem fpl;
+  stage_fft_plan(&fpl, a.fq);
   const int ky = blockIdx.x, p = blockIdx.y;
   const size_t row = ((size_t)p * a.P + ky) * Q;
-  for (int kx = threadIdx.x; kx < Q; kx += blockDim.x) {
+  for (int kx = threadIdx.x; kx < Q; kx += NT) {
     sS[kx] = a.sqrtS[row + kx];
-    if (AR && a.load_state) st[kx] = a.ar[row + kx];
+    if (a.load_state) st[kx] = a.ar[row + kx];
   }
   __syncthreads();
   const int64_t t_end = a.frame0 + a.F;
-  for (int64_t t = AR ? a.t_start : a.frame0; t < t_end; ++t) {
+  for (int64_t t = a.t_start; t < t_end; ++t) {
     const bool out = t >= a.frame0;
-    for (int kx = threadIdx.x; kx < Q; kx += blockDim.x) {
+    for (int kx = threadIdx.x; kx < Q; kx += NT) {
       float4 z = spectral_noise(ky, kx, a.P, Q, p, t, a.k0, a.k1);
-      if (AR) {
-        if (t > 0) {
-          float4 o = st[kx];
-          z = make_float4(a.alpha * o.x + a.calpha * z.x, a.alpha * o.y + a.calpha * z.y,
-                          a.alpha * o.z + a.calpha * z.z, a.alpha * o.w + a.calpha * z.w);
-        }
-        st[kx] = z;
+      if (t > 0) {
+        const float4 o = st[kx];
+        z = make_float4(a.alpha * o.x + a.calpha * z.x, a.alpha * o.y + a.calpha * z.y,
+                        a.alpha * o.z + a.calpha * z.z, a.alpha * o.w + a.calpha * z.w);
       }
-      if (out) {
-        const float2 s = sS[kx];
-        // Y = sa zeta_a + i sb zeta_b
-        b0[kx] = make_float2(s.x * z.x - s.y * z.w, s.x * z.y + s.y * z.z);
-      }
+      st[kx] = z;
+      if (out) X[kx] = spectrum(sS[kx], z);
     }
-    if (!out) continue;  // AR replay: no transform
+    if (!out) continue;  // replay: state only
     __syncthreads();
-    float2* res = smem_ifft(b0, b1, a.fq, 0);
+    const float2* R = smem_ifft<NT>(X, Xb, &fpl, 0);
     float2* dst = a.Zout + (size_t)(t - a.frame0) * a.npairs * a.P * Q + row;
-    for (int x = threadIdx.x; x < Q; x += blockDim.x) dst[x] = res[x];
-    __syncthreads();  // b0/b1 are free again; the next spectrum goes to b0
-  }
-  if (AR) {
+    for (int x = threadIdx.x; x < Q; x += NT) dst[x] = R[x];
     __syncthreads();
-    for (int kx = threadIdx.x; kx < Q; kx += blockDim.x) a.ar[row + kx] = st[kx];
   }
+  __syncthreads();
+  for (int kx = threadIdx.x; kx < Q; kx += NT) a.ar[row + kx] = st[kx];
 }
 
 int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool ar, int ar_mode,
                 int64_t replay_from, cudaStream_t s) {
   RowArgs a;
-  a.fq.N = pl->fq.N;
-  a.fq.nrad = pl->fq.nrad;
-  for (int i = 0; i < kMaxRadix; ++i) a.fq.rad[i] = pl->fq.rad[i];
-  a.fq.tw = pl->fq.tw;
+  fill_fft_args(a.fq, pl->fq);
   a.sqrtS = pl->d_sqrtS;
   a.ar = pl->d_ar;
   a.Zout = pl->d_Z;
@@ -244,16 +326,26 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
   a.calpha = sqrtf(1.0f - pl->ar_alpha * pl->ar_alpha);
   a.t_start = ar ? replay_from : frame0;
   a.load_state = (ar && ar_mode == 0) ? 1 : 0;
-  dim3 grid(pl->P, pl->npairs);
-  const int nthr = pl->Q >= 1024 ? 256 : 128;
   if (ar) {
+    dim3 grid(pl->P, pl->npairs);
     size_t sm = (size_t)pl->Q * (3 * sizeof(float2) + sizeof(float4));
-    cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_rows<true><<<grid, nthr, sm, s>>>(a);
+    if (pl->Q > 1024) {
+      cudaFuncSetAttribute(k_rows_ar<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_rows_ar<512><<<grid, 512, sm, s>>>(a);
+    } else {
+      cudaFuncSetAttribute(k_rows_ar<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_rows_ar<128><<<grid, 128, sm, s>>>(a);
+    }
   } else {
-    size_t sm = (size_t)pl->Q * 3 * sizeof(float2);
-    cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_rows<false><<<grid, nthr, sm, s>>>(a);
+    dim3 grid(pl->P / 2 + 1, pl->npairs);
+    size_t sm = (size_t)pl->Q * 6 * sizeof(float2);
+    if (pl->Q > 1024) {
+      cudaFuncSetAttribute(k_rows_pair<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_rows_pair<512><<<grid, 512, sm, s>>>(a);
+    } else {
+      cudaFuncSetAttribute(k_rows_pair<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_rows_pair<256><<<grid, 256, sm, s>>>(a);
+    }
   }
   return (int)cudaGetLastError();
 }
@@ -269,39 +361,41 @@ struct ColArgs {
   float* tilt;        // mode 1: [F][2][H*W]
 };
 
-template <int MODE>
-__global__ void __launch_bounds__(256) k_cols(ColArgs a) {
+template <int MODE, int NT>
+__global__ void __launch_bounds__(NT) k_cols(ColArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int TC = 1 << a.tc_log2;
-  float2* b0 = reinterpret_cast<float2*>(smem);
-  float2* b1 = b0 + (size_t)a.P * TC;
+  float2* X = reinterpret_cast<float2*>(smem);
+  float2* Xb = X + ((size_t)a.P << a.tc_log2);
+  __shared__ FFTPlanSmem fpl;
+  stage_fft_plan(&fpl, a.fp);
   const int x0 = blockIdx.x * TC, p = blockIdx.y, f = blockIdx.z;
   const float2* src = a.Zin + ((size_t)f * a.npairs + p) * a.P * a.Q;
   const int n = a.P << a.tc_log2;
-  for (int w = threadIdx.x; w < n; w += blockDim.x) {
+  for (int w = threadIdx.x; w < n; w += NT) {
     const int c = w & (TC - 1), ky = w >> a.tc_log2;
     const int x = x0 + c;
-    b0[w] = (x < a.Q) ? src[(size_t)ky * a.Q + x] : make_float2(0.f, 0.f);
+    X[w] = (x < a.Q) ? src[(size_t)ky * a.Q + x] : make_float2(0.f, 0.f);
   }
   __syncthreads();
-  const float2* res = smem_ifft(b0, b1, a.fp, a.tc_log2);
+  const float2* R = smem_ifft<NT>(X, Xb, &fpl, a.tc_log2);
   const int sa = 2 * p, sb = 2 * p + 1;
   const size_t HW = (size_t)a.H * a.W;
   const int m = a.H << a.tc_log2;
-  for (int w = threadIdx.x; w < m; w += blockDim.x) {
+  for (int w = threadIdx.x; w < m; w += NT) {
     const int c = w & (TC - 1), yy = w >> a.tc_log2;
     const int x = x0 + c;
     if (x >= a.W) continue;
-    const float2 v = res[w];
+    const float2 v = R[w];
     const size_t pix = (size_t)yy * a.W + x;
     if (MODE == 0) {
       float* z = a.zern + (size_t)f * a.Z * HW;
       z[(size_t)(sa + 1) * HW + pix] = v.x;
       if (sb < a.nslots) z[(size_t)(sb + 1) * HW + pix] = v.y;
     } else {
-      uint16_t* X = a.X + (size_t)f * a.nslots * HW;
-      X[(size_t)sa * HW + pix] = f_to_bf16(v.x);
-      if (sb < a.nslots) X[(size_t)sb * HW + pix] = f_to_bf16(v.y);
+      uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
+      Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
+      if (sb < a.nslots) Xo[(size_t)sb * HW + pix] = f_to_bf16(v.y);
       if (p == 0) {
         float* t = a.tilt + (size_t)f * 2 * HW;
         t[pix] = v.x;
@@ -313,10 +407,7 @@ __global__ void __launch_bounds__(256) k_cols(ColArgs a) {
 
 int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t s) {
   ColArgs a;
-  a.fp.N = pl->fp.N;
-  a.fp.nrad = pl->fp.nrad;
-  for (int i = 0; i < kMaxRadix; ++i) a.fp.rad[i] = pl->fp.rad[i];
-  a.fp.tw = pl->fp.tw;
+  fill_fft_args(a.fp, pl->fp);
   a.Zin = pl->d_Z;
   a.P = pl->P;
   a.Q = pl->Q;
@@ -326,7 +417,7 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   a.nslots = pl->nslots;
   a.Z = pl->Z;
   int tcl = 4;
-  while (tcl > 0 && (size_t)16 * pl->P * (1 << tcl) > 160 * 1024) --tcl;
+  while (tcl > 0 && pl->P * (1 << tcl) > kColElems) --tcl;
   a.tc_log2 = tcl;
   a.zern = zern;
   a.X = pl->d_X;
@@ -335,11 +426,11 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   dim3 grid((pl->W + TC - 1) / TC, pl->npairs, F);
   size_t sm = (size_t)2 * pl->P * TC * sizeof(float2);
   if (mode == 0) {
-    cudaFuncSetAttribute(k_cols<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_cols<0><<<grid, 256, sm, s>>>(a);
+    cudaFuncSetAttribute(k_cols<0, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_cols<0, 256><<<grid, 256, sm, s>>>(a);
   } else {
-    cudaFuncSetAttribute(k_cols<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_cols<1><<<grid, 256, sm, s>>>(a);
+    cudaFuncSetAttribute(k_cols<1, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_cols<1, 256><<<grid, 256, sm, s>>>(a);
   }
   return (int)cudaGetLastError();
 }

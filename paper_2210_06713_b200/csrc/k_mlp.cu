@@ -15,7 +15,9 @@
 // Epilogues read TMEM with tcgen05.ld (32 lanes x 16 columns per warp), add bias,
 // ReLU, repack bf16 into the next layer's A operand; the last one writes the basis
 // weights w [F][H*W][n3] bf16 (pixel-major rows for the blur epilogue).
-// Persistent grid: each CTA keeps the weight images resident in shared memory.
+// Persistent grid, one CTA per SM holding the weight images once in shared memory and
+// running two independent 128-pixel tile pipelines (one per warpgroup, own TMEM columns);
+// the next tile's inputs are prefetched with cp.async while the current one computes.
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
@@ -63,77 +65,118 @@ __device__ __forceinline__ void mlp_epilogue(uint32_t taddr, int ncols, const fl
   }
 }
 
-__global__ void __launch_bounds__(128, 1) k_mlp(MlpArgs a) {
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void wg_sync(int wg) {  // named barrier of one 128-thread warpgroup
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+}
+
+// A1 tile (nin planes x 128 pixels, MN-major, k linear at 16 B) for pixel block pix0 of frame f.
+__device__ __forceinline__ void load_a1(const MlpArgs& a, uint8_t* A1, int f, int pix0, int ltid, bool async) {
+  const uint16_t* Xf = a.X + (size_t)f * a.nin * a.HW;
+  for (int idx = ltid; idx < a.nin * 16; idx += 128) {
+    const int k = idx % a.nin, g = idx / a.nin;
+    const int pix = pix0 + 8 * g;
+    const uint16_t* src = Xf + (size_t)k * a.HW + pix;
+    uint8_t* dst = A1 + g * (a.k1 * 16) + k * 16;
+    if (async) {  // HW % 8 == 0: whole 16-byte chunks, zero-filled past the image
+      cp_async16(dst, pix < a.HW ? src : a.X, pix < a.HW ? 16u : 0u);
+    } else {
+      uint16_t t[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) t[e] = (pix + e < a.HW) ? src[e] : (uint16_t)0;
+      *reinterpret_cast<uint4*>(dst) =
+          make_uint4(t[0] | (t[1] << 16), t[2] | (t[3] << 16), t[4] | (t[5] << 16), t[6] | (t[7] << 16));
+    }
+  }
+}
+
+// Two warpgroups per CTA, each an independent tile pipeline (own A1 double buffer, A2,
+// TMEM columns, mbarrier), sharing one resident copy of the weight images.
+__global__ void __launch_bounds__(256, 1) k_mlp(MlpArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sw = smem;  // weight blob
   const uint32_t blob_al = (a.blob_bytes + 127) & ~127u;
-  uint8_t* A1 = sw + blob_al;
   const uint32_t a1_bytes = 128u * a.k1 * 2;
-  uint8_t* A2 = A1 + a1_bytes;
   const int nmax = a.n1 > a.n2 ? a.n1 : a.n2;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(A2 + 128u * nmax * 2);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
-
+  const uint32_t a2_bytes = 128u * nmax * 2;
+  const uint32_t wg_bytes = 2 * a1_bytes + a2_bytes;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // weights -> smem (once per CTA)
-  for (uint32_t i = tid * 16; i < a.blob_bytes; i += 128 * 16)
+  const int wg = tid >> 7, ltid = tid & 127;
+  uint8_t* A1b[2] = {sw + blob_al + wg * wg_bytes, sw + blob_al + wg * wg_bytes + a1_bytes};
+  uint8_t* A2 = sw + blob_al + wg * wg_bytes + 2 * a1_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sw + blob_al + 2 * wg_bytes);
+  uint64_t* bar = bars + wg;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+
+  for (uint32_t i = tid * 16; i < a.blob_bytes; i += 256 * 16)
     *reinterpret_cast<uint4*>(sw + i) = __ldg(reinterpret_cast<const uint4*>(a.blob + i));
-  // zero the padded input planes of A1 (k in [nin, k1)) once
-  for (int idx = tid; idx < (a.k1 - a.nin) * 16; idx += 128) {
-    const int k = a.nin + idx % (a.k1 - a.nin), g = idx / (a.k1 - a.nin);
-    *reinterpret_cast<uint4*>(A1 + g * (a.k1 * 16) + k * 16) = make_uint4(0, 0, 0, 0);
+  // zero the padded input planes (k in [nin, k1)) of all four A1 buffers once
+  for (int idx = tid; idx < 4 * (a.k1 - a.nin) * 16; idx += 256) {
+    const int per = (a.k1 - a.nin) * 16;
+    const int b = idx / per, r = idx % per;
+    const int k = a.nin + r % (a.k1 - a.nin), g = r / (a.k1 - a.nin);
+    uint8_t* base = sw + blob_al + (b >> 1) * wg_bytes + (b & 1) * a1_bytes;
+    *reinterpret_cast<uint4*>(base + g * (a.k1 * 16) + k * 16) = make_uint4(0, 0, 0, 0);
   }
   if (tid == 0) {
-    mbar_init(bar, 1);
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
     mbar_fence_init();
   }
   const int nalloc = nmax > a.n3 ? nmax : a.n3;
-  const uint32_t ncols = nalloc <= 32 ? 32 : nalloc <= 64 ? 64 : nalloc <= 128 ? 128 : 256;
+  const uint32_t cols_wg = nalloc <= 32 ? 32 : nalloc <= 64 ? 64 : nalloc <= 128 ? 128 : 256;
+  const uint32_t ncols = 2 * cols_wg;
   if (warp == 0) tmem_alloc(tslot, ncols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tslot;
-  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
-  const int m = warp * 32 + lane;  // TMEM lane = tile row = pixel offset
+  const uint32_t tmem = *tslot + wg * cols_wg;
+  const int qd = warp & 3;
+  const uint32_t taddr = tmem + ((uint32_t)(qd * 32) << 16);
+  const int m = qd * 32 + lane;  // TMEM lane = tile row = pixel offset
 
   const float* b1 = reinterpret_cast<const float*>(sw + a.off_b1);
   const float* b2 = reinterpret_cast<const float*>(sw + a.off_b2);
   const float* b3 = reinterpret_cast<const float*>(sw + a.off_b3);
-  const uint32_t sA1 = smem_u32(A1), sA2 = smem_u32(A2);
+  const uint32_t sA2 = smem_u32(A2);
   const uint32_t sW1 = smem_u32(sw), sW2 = smem_u32(sw + a.off_w2), sW3 = smem_u32(sw + a.off_w3);
   const uint32_t id1 = umma_idesc_bf16(128, a.n1, true, false);
   const uint32_t id2 = umma_idesc_bf16(128, a.n2, false, false);
   const uint32_t id3 = umma_idesc_bf16(128, a.n3, false, false);
   uint32_t phase = 0;
   const int ntiles = a.F * a.tiles_per_frame;
-  const bool vec_ok = (a.HW % 8) == 0;
+  const bool async = (a.HW % 8) == 0;
+  const int stride = 2 * gridDim.x;
+  int tile = 2 * blockIdx.x + wg;
+  int buf = 0;
+  if (tile < ntiles) {
+    const int f = tile / a.tiles_per_frame;
+    load_a1(a, A1b[0], f, (tile - f * a.tiles_per_frame) * 128, ltid, async);
+  }
+  cp_async_commit();
 
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (; tile < ntiles; tile += stride, buf ^= 1) {
     const int f = tile / a.tiles_per_frame;
     const int pix0 = (tile - f * a.tiles_per_frame) * 128;
-    // ---- A1: nin input planes x 128 pixels, MN-major (k linear, 16 B per k-row)
-    const uint16_t* Xf = a.X + (size_t)f * a.nin * a.HW;
-    for (int idx = tid; idx < a.nin * 16; idx += 128) {
-      const int k = idx % a.nin, g = idx / a.nin;
-      const int pix = pix0 + 8 * g;
-      const uint16_t* src = Xf + (size_t)k * a.HW + pix;
-      uint4 v;
-      if (vec_ok && pix + 8 <= a.HW) {
-        v = __ldg(reinterpret_cast<const uint4*>(src));
-      } else {
-        uint16_t t[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) t[e] = (pix + e < a.HW) ? src[e] : (uint16_t)0;
-        v = make_uint4(t[0] | (t[1] << 16), t[2] | (t[3] << 16), t[4] | (t[5] << 16), t[6] | (t[7] << 16));
-      }
-      *reinterpret_cast<uint4*>(A1 + g * (a.k1 * 16) + k * 16) = v;
+    const int nxt = tile + stride;
+    if (nxt < ntiles) {  // prefetch the next tile while this one runs
+      const int fn = nxt / a.tiles_per_frame;
+      load_a1(a, A1b[buf ^ 1], fn, (nxt - fn * a.tiles_per_frame) * 128, ltid, async);
     }
+    cp_async_commit();
+    cp_async_wait<1>();
     fence_async_smem();
     tc_fence_before();
-    __syncthreads();
+    wg_sync(wg);
+    const uint32_t sA1 = smem_u32(A1b[buf]);
     // ---- layer 1
-    if (tid == 0) {
+    if (ltid == 0) {
       tc_fence_after();
       for (int s = 0; s < a.k1 / 16; ++s)
         umma_bf16(tmem, umma_desc(sA1 + s * 256, 128, a.k1 * 16), umma_desc(sW1 + s * 256, 128, (a.k1 / 8) * 128),
@@ -146,9 +189,9 @@ __global__ void __launch_bounds__(128, 1) k_mlp(MlpArgs a) {
     mlp_epilogue<true, false>(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m, nullptr);
     fence_async_smem();
     tc_fence_before();
-    __syncthreads();
+    wg_sync(wg);
     // ---- layer 2
-    if (tid == 0) {
+    if (ltid == 0) {
       tc_fence_after();
       for (int s = 0; s < a.n1 / 16; ++s)
         umma_bf16(tmem, umma_desc(sA2 + s * 256, 128, (a.n1 / 8) * 128),
@@ -161,9 +204,9 @@ __global__ void __launch_bounds__(128, 1) k_mlp(MlpArgs a) {
     mlp_epilogue<true, false>(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m, nullptr);
     fence_async_smem();
     tc_fence_before();
-    __syncthreads();
+    wg_sync(wg);
     // ---- layer 3
-    if (tid == 0) {
+    if (ltid == 0) {
       tc_fence_after();
       for (int s = 0; s < a.n2 / 16; ++s)
         umma_bf16(tmem, umma_desc(sA2 + s * 256, 128, (a.n2 / 8) * 128),
@@ -177,10 +220,13 @@ __global__ void __launch_bounds__(128, 1) k_mlp(MlpArgs a) {
     uint16_t* grow = (pix < a.HW) ? a.wout + ((size_t)f * a.HW + pix) * a.n3 : nullptr;
     mlp_epilogue<false, true>(taddr, a.n3, b3, nullptr, 0, m, grow);
     tc_fence_before();
-    __syncthreads();
+    wg_sync(wg);
   }
+  cp_async_wait<0>();
+  tc_fence_before();
+  __syncthreads();
   tc_fence_after();
-  if (warp == 0) tmem_dealloc(tmem, ncols);
+  if (warp == 0) tmem_dealloc(*tslot, ncols);
 }
 
 int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
@@ -204,14 +250,12 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   a.F = F;
   a.tiles_per_frame = (a.HW + 127) / 128;
   const int nmax = g.n1 > g.n2 ? g.n1 : g.n2;
-  size_t sm = ((g.blob_bytes + 127) & ~(size_t)127) + 128 * g.k1 * 2 + 128 * nmax * 2 + 16;
+  size_t sm = ((g.blob_bytes + 127) & ~(size_t)127) + 2 * (2 * 128 * g.k1 * 2 + 128 * nmax * 2) + 32;
   cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int ntiles = F * a.tiles_per_frame;
-  // TMEM: at most 256 columns per CTA, so up to 2 CTAs share an SM
-  int blocks_per_sm = (sm <= 100 * 1024) ? 2 : 1;
-  int grid = p->num_sms * blocks_per_sm;
-  if (grid > ntiles) grid = ntiles;
-  k_mlp<<<grid, 128, sm, s>>>(a);
+  int grid = p->num_sms;  // persistent: one CTA (two tile pipelines) per SM
+  if (2 * grid > ntiles) grid = (ntiles + 1) / 2;
+  k_mlp<<<grid, 256, sm, s>>>(a);
   return (int)cudaGetLastError();
 }
 
