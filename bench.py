@@ -224,7 +224,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import synth
-    from paper_2210_06713_b200 import Plan, PlanConfig
+    from paper_2210_06713_b200 import Plan, PlanConfig, runner
 
     H, W, C, F, K, T = w["H"], w["W"], w["C"], w["F"], w["K"], w["T"]
     basis = synth.basis(K, T, seed=0)
@@ -238,7 +238,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def frame0(step):
-        return step * world * F + rank * F
+        return runner.step_frame0(step, rank, world, F)
 
     def barrier():
         if world > 1:
@@ -265,10 +265,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     stages = plan.stage_times()
     plan.stage_timing(False)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = runner.max_over_ranks(ms)
     value = world * F * args.steps / (ms_max / 1e3)
 
     # ---- end to end through the host-buffer C-ABI entry point (pinned buffers)
@@ -282,10 +279,7 @@ def main():
         for s in range(args.steps):
             plan.simulate_frames_host(img_h, 0, SEED, frame0(args.warmup + s), F, out_h)
         te = time.perf_counter() - te0
-        tt = torch.tensor([te], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * F * args.steps / float(tt.item()), "unit": "frames/s",
+        e2e = {"value": world * F * args.steps / runner.max_over_ranks(te), "unit": "frames/s",
                "h2d_bytes_per_step": int(img_np.nbytes), "d2h_bytes_per_step": int(out_h.nbytes),
                "api": "p2s_simulate_frames_host (pinned host buffers, wall clock, max over ranks)"}
 

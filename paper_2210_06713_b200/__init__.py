@@ -3,5 +3,6 @@
 The product path is libp2s.so (include/p2s.h): hand-written sm_100a kernels for the
 five per-frame steps.  This package only binds it (p2s.py).
 """
+from . import runner  # noqa: F401
 from .p2s import (EXPORTS, LIB_PATH, Options, P2SError, Plan, PlanConfig, grid_size, host_tables,  # noqa: F401
                   lib, philox_fill)

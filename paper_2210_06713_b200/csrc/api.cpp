@@ -127,7 +127,7 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   g.np = round16(K);
   g.racc = std::max(1, 4 / p->C);
   g.nks = (T * G + 1) / 2;
-  g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, g.nks);
+  g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, g.nks, p->H);
   g.RS = g.RB + 8 * G + 8;
   const uint32_t sbo = (uint32_t)g.RS * 16;
   struct Grp { int tx, gi; uint32_t off; };

@@ -23,7 +23,8 @@
 
 namespace p2s {
 
-constexpr int kBlurStages = 6;
+constexpr int kBlurStages = 4;
+constexpr int kStepsPerStage = 2;  // K-steps (B tiles) moved per ring stage
 constexpr int kBlurThreads = 192;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue
 constexpr int kAccStride = 128;    // TMEM columns per accumulator
 
@@ -67,7 +68,7 @@ __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int 
   L.b_bytes = (uint32_t)np * 32;
   L.off_w = C * L.tile_bytes;
   L.off_ring = (L.off_w + L.w_bytes + 127) & ~127u;
-  L.off_koff = L.off_ring + kBlurStages * L.b_bytes;
+  L.off_koff = L.off_ring + kBlurStages * kStepsPerStage * L.b_bytes;
   L.off_klbo = L.off_koff + 4 * nks;
   L.off_hsum = L.off_klbo + 4 * nks;
   L.off_bar = (L.off_hsum + 4 * np + 15) & ~15u;
@@ -153,11 +154,13 @@ __global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
   const int valid_px = min(128, a.W - x0);
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer: per row group the w rows, then the B tile of every K-step
+    if (lane == 0) {  // ---- TMA producer: B tiles stream continuously; the w rows of group rg are
+                      // issued as soon as the epilogue has released group rg-1 (single w buffer)
       uint32_t stage = 0, phase = 0;
       const uint32_t bbytes = L.b_bytes;
-      for (int rg = 0; rg < n_rg; ++rg) {
-        mbar_wait(tempty, (rg & 1) ^ 1);  // epilogue finished with wbuf (and TMEM) of rg-1
+      const int nst = (a.nks + kStepsPerStage - 1) / kStepsPerStage;
+      const uint32_t s_tempty = smem_u32(tempty);
+      auto issue_w = [&](int rg) {
         uint32_t wb = 0;
         for (int r = 0; r < a.racc; ++r) wb += (y0 + rg * a.racc + r < a.H) ? (uint32_t)valid_px * a.np * 2 : 0;
         mbar_arrive_expect_tx(wfull, wb);
@@ -167,14 +170,31 @@ __global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
             bulk_g2s(wbuf + (size_t)r * 128 * a.np * 2, a.w + ((size_t)f * HW + (size_t)y * a.W + x0) * a.np,
                      (uint32_t)valid_px * a.np * 2, wfull);
         }
-        for (int t = 0; t < a.nks; ++t) {
+      };
+      for (int rg = 0; rg < n_rg; ++rg) {
+        bool w_done = false;
+        if (rg == 0) {
+          issue_w(0);
+          w_done = true;
+        }
+        for (int st = 0; st < nst; ++st) {
+          if (!w_done && mbar_try_wait(s_tempty, (rg - 1) & 1)) {
+            issue_w(rg);
+            w_done = true;
+          }
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], bbytes);
-          bulk_g2s(ring + stage * bbytes, a.bimg + (size_t)t * bbytes, bbytes, &full[stage]);
+          const int t0 = st * kStepsPerStage;
+          const int nt = min(kStepsPerStage, a.nks - t0);
+          mbar_arrive_expect_tx(&full[stage], nt * bbytes);
+          bulk_g2s(ring + stage * kStepsPerStage * bbytes, a.bimg + (size_t)t0 * bbytes, nt * bbytes, &full[stage]);
           if (++stage == kBlurStages) {
             stage = 0;
             phase ^= 1;
           }
+        }
+        if (!w_done) {
+          mbar_wait(tempty, (rg - 1) & 1);
+          issue_w(rg);
         }
       }
     }
@@ -182,20 +202,27 @@ __global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
     if (lane == 0) {  // ---- MMA issuer: every K-step feeds C x racc accumulators
       const uint32_t idesc = umma_idesc_bf16(128, a.np, true, false);
       const uint32_t s_tile = smem_u32(smem);
+      const int nst = (a.nks + kStepsPerStage - 1) / kStepsPerStage;
       uint32_t stage = 0, phase = 0;
       for (int rg = 0; rg < n_rg; ++rg) {
         mbar_wait(tempty, (rg & 1) ^ 1);
         tc_fence_after();
         const uint32_t arow = s_tile + (uint32_t)(rg * a.racc) * 16;
-        for (int t = 0; t < a.nks; ++t) {
+        for (int st = 0; st < nst; ++st) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t bdesc = umma_desc(smem_u32(ring + stage * L.b_bytes), 128, 256);
-          const uint32_t ko = s_koff[t], lbo = s_klbo[t];
-          for (int ch = 0; ch < a.C; ++ch)
-            for (int r = 0; r < a.racc; ++r)
-              umma_bf16(tmem + (ch * a.racc + r) * kAccStride,
-                        umma_desc(arow + ch * L.tile_bytes + r * 16 + ko, lbo, sbo_src), bdesc, idesc, t > 0);
+          const uint32_t sring = smem_u32(ring + stage * kStepsPerStage * L.b_bytes);
+          const int t0 = st * kStepsPerStage;
+          const int nt = min(kStepsPerStage, a.nks - t0);
+          for (int u = 0; u < nt; ++u) {
+            const int t = t0 + u;
+            const uint64_t bdesc = umma_desc(sring + u * L.b_bytes, 128, 256);
+            const uint32_t ko = s_koff[t], lbo = s_klbo[t];
+            for (int ch = 0; ch < a.C; ++ch)
+              for (int r = 0; r < a.racc; ++r)
+                umma_bf16(tmem + (ch * a.racc + r) * kAccStride,
+                          umma_desc(arow + ch * L.tile_bytes + r * 16 + ko, lbo, sbo_src), bdesc, idesc, t > 0);
+          }
           umma_commit(&empty[stage]);
           if (++stage == kBlurStages) {
             stage = 0;
@@ -313,14 +340,18 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
 }
 
 // Host helper: rows per CTA that fit the shared-memory budget for this geometry.
-int blur_rows_per_cta(int C, int T, int np, int racc, int nks) {
+int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H) {
   const int NC = T + 15, G = (T + 7) / 8;
   int best = racc;
   for (int RB = racc; RB <= 64; RB += racc) {
     const int RS = RB + 8 * G + 8;
     if (blur_smem_layout(C, NC, RS, racc, np, nks).total <= 227 * 1024) best = RB;
   }
-  return best;
+  // balance the bands: same number of bands, as few padded rows as possible
+  const int bands = (H + best - 1) / best;
+  int rb = (H + bands - 1) / bands;
+  rb = (rb + racc - 1) / racc * racc;
+  return rb < best ? rb : best;
 }
 
 }  // namespace p2s

@@ -1,0 +1,72 @@
+"""Frame-parallel multi-GPU execution.
+
+Frames are independent given (seed, global frame index): the spectral noise is
+counter-based, so every GPU simulates its own disjoint frame range with a plan
+replica and no data-path collective ("scaling": "weak").  An AR(1) sequence split
+across GPUs needs no communication either: a plan asked for frames starting at
+frame0 > 0 rebuilds eta_{frame0-1} on the device by carry replay.  torch.distributed
+(NCCL on GPUs, gloo in the CPU tests) is used only for barriers and max-over-ranks
+timing.
+"""
+from __future__ import annotations
+
+
+def frame_partition(total_frames: int, world: int, rank: int):
+    """Contiguous balanced split of [0, total_frames): (first frame, count) of this rank."""
+    if world < 1 or not (0 <= rank < world) or total_frames < 0:
+        raise ValueError("bad partition arguments")
+    base, extra = divmod(total_frames, world)
+    start = rank * base + min(rank, extra)
+    return start, base + (1 if rank < extra else 0)
+
+
+def step_frame0(step: int, rank: int, world: int, frames_per_rank: int) -> int:
+    """First global frame of `rank` in benchmark step `step` (weak scaling: every step
+    simulates world * frames_per_rank new frames, rank r owns a contiguous block)."""
+    return (step * world + rank) * frames_per_rank
+
+
+def sequence_assignment(n_sequences: int, world: int, rank: int):
+    """Whole sequences per rank when there are at least as many sequences as ranks."""
+    return list(range(rank, n_sequences, world))
+
+
+def max_over_ranks(value: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class FrameShardedRunner:
+    """Runs this rank's share of a frame range through one plan (device buffers)."""
+
+    def __init__(self, plan, rank: int = 0, world: int = 1):
+        self.plan, self.rank, self.world = plan, rank, world
+
+    def local_range(self, total_frames: int, frame_base: int = 0):
+        s, n = frame_partition(total_frames, self.world, self.rank)
+        return frame_base + s, n
+
+    def run(self, img, img_frame_stride, seed, total_frames, out_local, frame_base=0, stream=None):
+        """Simulate this rank's frames of [frame_base, frame_base + total_frames) into out_local."""
+        f0, n = self.local_range(total_frames, frame_base)
+        if n:
+            img_local = img if img_frame_stride == 0 else img[f0 - frame_base:]
+            self.plan.simulate_frames(img_local, img_frame_stride, seed, f0, n, out_local, stream)
+        return f0, n
