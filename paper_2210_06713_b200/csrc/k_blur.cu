@@ -4,20 +4,22 @@
 // invariant convolutions".  Here conv_k(x) = (h_k (*) Iw_c)(x) for all K bases at once is
 // an implicit GEMM  D[pixel][k] = sum_taps A[pixel][tap] B[tap][k]  with
 //   M = 128 pixels of one output row (lane m <-> pixel x0 + 16 (m % 8) + m / 8),
-//   N = np (K padded to 16), fp32 accumulators in TMEM (4 output rows in flight),
+//   N = np (K padded to 16), fp32 accumulators in TMEM, one per (channel, row) in flight,
 //   K = taps, ordered as groups of 8 consecutive tap rows ty at one tap column tx.
-// The A operand is never materialised as im2col: the source tile is stored ONCE in
-// shared memory as 16-byte chunks, chunk cc of source row r holding the 8 pixels at
-// window offsets cc + 16 j (j = 0..7).  With the lane permutation above, the
-// [128 x 8-tap-row] slab of any (output row, tx, tap-row group) is a canonical
-// MN-major SWIZZLE_NONE layout (8 k-rows at 16 B, m-groups at SBO = one chunk
-// column), so every K-step is pure descriptor arithmetic: start = tile + chunk
-// (2c - tx) + rows, and the second 8-row group of the K-step is reached through the
-// descriptor's leading-byte offset.  The B operand (taps x bases, precomputed per
-// K-step on the host) streams through a TMA bulk-copy ring shared by the 4 rows.
-// The epilogue (4 warps) reads the accumulator rows with tcgen05.ld, forms
-// sum_k w_k(x) conv_k(x) with the P2S weights, and applies step 5 (normalise,
-// Philox noise, clamp) before the only HBM write of the frame.
+// The A operand is never materialised as im2col: the source tile of each channel is stored
+// ONCE in shared memory as 16-byte chunks, chunk cc of source row r holding the 8 pixels
+// at window offsets cc + 16 j (j = 0..7).  With the lane permutation above, the
+// [128 x 8-tap-row] slab of any (output row, tx, tap-row group) is a canonical MN-major
+// SWIZZLE_NONE layout (8 k-rows at 16 B, m-groups at SBO = one chunk column), so every
+// K-step is pure descriptor arithmetic: start = tile + chunk (2c - tx) + rows, and the
+// second 8-row group of the K-step is reached through the descriptor's leading-byte
+// offset.  Descriptors of all K-steps are precomputed once per CTA in shared memory; the
+// MMA warp issues C x RACC tcgen05.mma per K-step under elect.sync.
+// The B operand (taps x bases, precomputed per K-step on the host) streams through a TMA
+// bulk-copy ring shared by all accumulators.  Per row group the P2S weights w (k-major
+// planes) arrive by one 2-D TMA tile load per row.  The epilogue warps read the
+// accumulators with tcgen05.ld, form sum_k w_k(x) conv_k(x), apply step 5 (normalise,
+// Philox noise, clamp) and write the output: the only HBM write of the frame.
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
@@ -30,13 +32,12 @@ constexpr int kAccStride = 128;    // TMEM columns per accumulator
 
 struct BlurArgs {
   const void* src;          // Iw [F][C][H][W] (bf16 or fp32)
-  const uint16_t* w;        // bf16 [F][HW][np]
   float* out;               // [F][C][H][W]
   const uint8_t* bimg;      // [nks][np*32]
   const uint32_t* koff;     // [nks]
   const uint32_t* klbo;     // [nks]
   const float* hsum;        // [np]
-  int C, H, W, T, c, NC, RB, RS, nks, np, racc;
+  int H, W, T, c, NC, RB, RS, nks, np;
   uint32_t k0, k1;
   int64_t frame0;
   float sigma;
@@ -57,35 +58,34 @@ __device__ __forceinline__ float load_src(const void* src, size_t idx) {
 
 struct BlurSmem {
   uint32_t tile_bytes, w_bytes, b_bytes;
-  uint32_t off_w, off_ring, off_koff, off_klbo, off_hsum, off_bar, total;
+  uint32_t off_w, off_ring, off_desc, off_hsum, off_bar, total;
 };
 
 __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int racc, int np, int nks) {
   BlurSmem L;
   L.tile_bytes = ((uint32_t)NC * RS * 16 + 127) & ~127u;
-  L.w_bytes = (uint32_t)racc * 128 * np * 2;
+  L.w_bytes = (uint32_t)racc * np * 128 * 2;  // [racc][np][128 px] bf16
   if (L.w_bytes < 6u * 176 * 4) L.w_bytes = 6u * 176 * 4;  // doubles as the loader's staging rows
   L.b_bytes = (uint32_t)np * 32;
   L.off_w = C * L.tile_bytes;
   L.off_ring = (L.off_w + L.w_bytes + 127) & ~127u;
-  L.off_koff = L.off_ring + kBlurStages * kStepsPerStage * L.b_bytes;
-  L.off_klbo = L.off_koff + 4 * nks;
-  L.off_hsum = L.off_klbo + 4 * nks;
+  L.off_desc = L.off_ring + kBlurStages * kStepsPerStage * L.b_bytes;
+  L.off_hsum = L.off_desc + 8 * nks;
   L.off_bar = (L.off_hsum + 4 * np + 15) & ~15u;
   L.total = L.off_bar + (2 * kBlurStages + 3) * 8 + 16;
   return L;
 }
 
-template <bool SRC_F32>
-__global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
+template <bool SRC_F32, int C, int RACC>
+__global__ void __launch_bounds__(kBlurThreads, 1)
+    k_blur(const BlurArgs a, const __grid_constant__ CUtensorMap tmap_w) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const BlurSmem L = blur_smem_layout(a.C, a.NC, a.RS, a.racc, a.np, a.nks);
+  const BlurSmem L = blur_smem_layout(C, a.NC, a.RS, RACC, a.np, a.nks);
   const uint32_t sbo_src = (uint32_t)a.RS * 16;
   uint8_t* wbuf = smem + L.off_w;
   uint8_t* ring = smem + L.off_ring;
-  uint32_t* s_koff = reinterpret_cast<uint32_t*>(smem + L.off_koff);
-  uint32_t* s_klbo = reinterpret_cast<uint32_t*>(smem + L.off_klbo);
+  uint64_t* s_adesc = reinterpret_cast<uint64_t*>(smem + L.off_desc);
   float* s_hsum = reinterpret_cast<float*>(smem + L.off_hsum);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
   uint64_t* full = bars;
@@ -97,11 +97,11 @@ __global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
 
   const int x0 = blockIdx.x * 128, y0 = blockIdx.y * a.RB, f = blockIdx.z;
   const int HW = a.H * a.W;
+  const uint32_t s_tile = smem_u32(smem);
 
-  for (int i = tid; i < a.nks; i += kBlurThreads) {
-    s_koff[i] = a.koff[i];
-    s_klbo[i] = a.klbo[i];
-  }
+  // A descriptor of every K-step for (channel 0, row 0): start = tile + koff, LBO, SBO
+  for (int i = tid; i < a.nks; i += kBlurThreads)
+    s_adesc[i] = umma_desc(s_tile + __ldg(&a.koff[i]), __ldg(&a.klbo[i]), sbo_src);
   for (int i = tid; i < a.np; i += kBlurThreads) s_hsum[i] = a.hsum[i];
   if (tid == 0) {
     for (int s = 0; s < kBlurStages; ++s) {
@@ -122,9 +122,9 @@ __global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
     float* stg = reinterpret_cast<float*>(wbuf) + warp * 176;
     const int rows_real = a.RB + a.T - 1;
     const int seg = 128 + a.T - 1;
-    for (int ch = 0; ch < a.C; ++ch) {
+    for (int ch = 0; ch < C; ++ch) {
       uint8_t* tile = smem + ch * L.tile_bytes;
-      const size_t plane = ((size_t)f * a.C + ch) * HW;
+      const size_t plane = ((size_t)f * C + ch) * HW;
       for (int rl = warp; rl < a.RS; rl += kBlurThreads / 32) {
         const bool real = rl < rows_real;
         if (real) {
@@ -149,129 +149,136 @@ __global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
-  const int n_rg = (a.RB + a.racc - 1) / a.racc;
-  const int nacc = a.C * a.racc;
-  const int valid_px = min(128, a.W - x0);
+  const int n_rg = (a.RB + RACC - 1) / RACC;
+  const int nst = (a.nks + kStepsPerStage - 1) / kStepsPerStage;
+  const uint32_t bbytes = L.b_bytes;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer: B tiles stream continuously; the w rows of group rg are
-                      // issued as soon as the epilogue has released group rg-1 (single w buffer)
-      uint32_t stage = 0, phase = 0;
-      const uint32_t bbytes = L.b_bytes;
-      const int nst = (a.nks + kStepsPerStage - 1) / kStepsPerStage;
-      const uint32_t s_tempty = smem_u32(tempty);
-      auto issue_w = [&](int rg) {
-        uint32_t wb = 0;
-        for (int r = 0; r < a.racc; ++r) wb += (y0 + rg * a.racc + r < a.H) ? (uint32_t)valid_px * a.np * 2 : 0;
-        mbar_arrive_expect_tx(wfull, wb);
-        for (int r = 0; r < a.racc; ++r) {
-          const int y = y0 + rg * a.racc + r;
-          if (y < a.H)
-            bulk_g2s(wbuf + (size_t)r * 128 * a.np * 2, a.w + ((size_t)f * HW + (size_t)y * a.W + x0) * a.np,
-                     (uint32_t)valid_px * a.np * 2, wfull);
-        }
-      };
-      for (int rg = 0; rg < n_rg; ++rg) {
-        bool w_done = false;
-        if (rg == 0) {
-          issue_w(0);
+    // ---- TMA producer: B tiles stream continuously; the w rows of group rg are issued as
+    // soon as the epilogue has released group rg-1 (single w buffer).
+    uint32_t stage = 0, phase = 0;
+    const uint32_t s_tempty = smem_u32(tempty);
+    auto issue_w = [&](int rg) {
+      int nrow = 0;
+      for (int r = 0; r < RACC; ++r) nrow += (y0 + rg * RACC + r < a.H) ? 1 : 0;
+      mbar_arrive_expect_tx(wfull, (uint32_t)nrow * a.np * 128 * 2);
+      for (int r = 0; r < RACC; ++r) {
+        const int y = y0 + rg * RACC + r;
+        if (y < a.H) tma_load_2d(wbuf + (size_t)r * a.np * 256, &tmap_w, y * a.W + x0, f * a.np, wfull);
+      }
+    };
+    for (int rg = 0; rg < n_rg; ++rg) {
+      bool w_done = false;
+      if (rg == 0) {
+        if (elect_one()) issue_w(0);
+        __syncwarp();
+        w_done = true;
+      }
+      for (int st = 0; st < nst; ++st) {
+        if (!w_done && mbar_try_wait(s_tempty, (rg - 1) & 1)) {
+          if (elect_one()) issue_w(rg);
+          __syncwarp();
           w_done = true;
         }
-        for (int st = 0; st < nst; ++st) {
-          if (!w_done && mbar_try_wait(s_tempty, (rg - 1) & 1)) {
-            issue_w(rg);
-            w_done = true;
-          }
-          mbar_wait(&empty[stage], phase ^ 1);
-          const int t0 = st * kStepsPerStage;
-          const int nt = min(kStepsPerStage, a.nks - t0);
+        mbar_wait(&empty[stage], phase ^ 1);
+        const int t0 = st * kStepsPerStage;
+        const int nt = min(kStepsPerStage, a.nks - t0);
+        if (elect_one()) {
           mbar_arrive_expect_tx(&full[stage], nt * bbytes);
           bulk_g2s(ring + stage * kStepsPerStage * bbytes, a.bimg + (size_t)t0 * bbytes, nt * bbytes, &full[stage]);
-          if (++stage == kBlurStages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        if (!w_done) {
-          mbar_wait(tempty, (rg - 1) & 1);
-          issue_w(rg);
+        __syncwarp();
+        if (++stage == kBlurStages) {
+          stage = 0;
+          phase ^= 1;
         }
+      }
+      if (!w_done) {
+        mbar_wait(tempty, (rg - 1) & 1);
+        if (elect_one()) issue_w(rg);
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer: every K-step feeds C x racc accumulators
-      const uint32_t idesc = umma_idesc_bf16(128, a.np, true, false);
-      const uint32_t s_tile = smem_u32(smem);
-      const int nst = (a.nks + kStepsPerStage - 1) / kStepsPerStage;
-      uint32_t stage = 0, phase = 0;
-      for (int rg = 0; rg < n_rg; ++rg) {
-        mbar_wait(tempty, (rg & 1) ^ 1);
+    // ---- MMA issuer (whole warp, one elected lane issues): C x RACC accumulators per K-step
+    const uint32_t idesc = umma_idesc_bf16(128, a.np, true, false);
+    uint32_t stage = 0, phase = 0;
+    const uint64_t ch_step = (uint64_t)(L.tile_bytes >> 4);
+    for (int rg = 0; rg < n_rg; ++rg) {
+      mbar_wait(tempty, (rg & 1) ^ 1);
+      tc_fence_after();
+      const uint64_t row_off = (uint64_t)(rg * RACC);  // start address += rg*RACC*16 bytes
+      for (int st = 0; st < nst; ++st) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t arow = s_tile + (uint32_t)(rg * a.racc) * 16;
-        for (int st = 0; st < nst; ++st) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sring = smem_u32(ring + stage * kStepsPerStage * L.b_bytes);
-          const int t0 = st * kStepsPerStage;
-          const int nt = min(kStepsPerStage, a.nks - t0);
-          for (int u = 0; u < nt; ++u) {
+        const uint64_t bdesc0 = umma_desc(smem_u32(ring + stage * kStepsPerStage * bbytes), 128, 256);
+        const int t0 = st * kStepsPerStage;
+        if (elect_one()) {
+#pragma unroll
+          for (int u = 0; u < kStepsPerStage; ++u) {
             const int t = t0 + u;
-            const uint64_t bdesc = umma_desc(sring + u * L.b_bytes, 128, 256);
-            const uint32_t ko = s_koff[t], lbo = s_klbo[t];
-            for (int ch = 0; ch < a.C; ++ch)
-              for (int r = 0; r < a.racc; ++r)
-                umma_bf16(tmem + (ch * a.racc + r) * kAccStride,
-                          umma_desc(arow + ch * L.tile_bytes + r * 16 + ko, lbo, sbo_src), bdesc, idesc, t > 0);
+            if (t < a.nks) {
+              const uint64_t bd = bdesc0 + (uint64_t)((u * bbytes) >> 4);
+              const uint64_t ad = s_adesc[t] + row_off;
+              const uint32_t acc = t > 0 ? 1u : 0u;
+#pragma unroll
+              for (int ch = 0; ch < C; ++ch)
+#pragma unroll
+                for (int r = 0; r < RACC; ++r)
+                  umma_bf16(tmem + (ch * RACC + r) * kAccStride, ad + ch * ch_step + (uint64_t)r, bd, idesc, acc);
+            }
           }
           umma_commit(&empty[stage]);
-          if (++stage == kBlurStages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        umma_commit(tfull);
+        __syncwarp();
+        if (++stage == kBlurStages) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      if (elect_one()) umma_commit(tfull);
+      __syncwarp();
     }
-  } else {  // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
+  } else {
+    // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
     const int qd = warp & 3;
     const int m = qd * 32 + lane;
     const int q = 16 * (m & 7) + (m >> 3);
     const int x = x0 + q;
     const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
+    const uint16_t* wq = reinterpret_cast<const uint16_t*>(wbuf) + q;
     for (int rg = 0; rg < n_rg; ++rg) {
       mbar_wait(tfull, rg & 1);
       mbar_wait(wfull, rg & 1);
       tc_fence_after();
-      for (int r = 0; r < a.racc; ++r) {
-        const int y = y0 + rg * a.racc + r;
+#pragma unroll
+      for (int r = 0; r < RACC; ++r) {
+        const int y = y0 + rg * RACC + r;
         const bool valid = (y < a.H) && (x < a.W);
-        const uint8_t* wrow = wbuf + ((size_t)r * 128 + q) * a.np * 2;
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint16_t* wr = wq + (size_t)r * a.np * 128;
+        float acc[C];
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) acc[ch] = 0.f;
         float g = 0.f;
         for (int cb = 0; cb < a.np / 16; ++cb) {
-          const uint4 w0 = *reinterpret_cast<const uint4*>(wrow + cb * 32);
-          const uint4 w1 = *reinterpret_cast<const uint4*>(wrow + cb * 32 + 16);
-          const uint32_t wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
           float wf[16];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            wf[2 * i] = bf16_lo(wv[i]);
-            wf[2 * i + 1] = bf16_hi(wv[i]);
+          for (int i = 0; i < 16; ++i) wf[i] = bf16_to_f(wr[(cb * 16 + i) * 128]);
+          if (a.normalize) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) g = fmaf(wf[i], s_hsum[cb * 16 + i], g);
           }
 #pragma unroll
-          for (int i = 0; i < 16; ++i) g = fmaf(wf[i], s_hsum[cb * 16 + i], g);
+          for (int ch = 0; ch < C; ++ch) {
+            float v[16];
+            tmem_ld16(tl + (ch * RACC + r) * kAccStride + cb * 16, v);
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            if (ch < a.C) {
-              float v[16];
-              tmem_ld16(tl + (ch * a.racc + r) * kAccStride + cb * 16, v);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) acc[ch] = fmaf(wf[i], v[i], acc[ch]);
-            }
+            for (int i = 0; i < 16; ++i) acc[ch] = fmaf(wf[i], v[i], acc[ch]);
           }
         }
         if (valid) {
-          for (int ch = 0; ch < a.C; ++ch) {
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) {
             float o = acc[ch];
             if (a.normalize) o = o / g;
             if (a.sigma != 0.f) {
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
               o += a.sigma * box_muller(rx.x, rx.y).x;
             }
             if (a.clamp01) o = fminf(fmaxf(o, 0.f), 1.f);
-            a.out[((size_t)f * a.C + ch) * HW + (size_t)y * a.W + x] = o;
+            a.out[((size_t)f * C + ch) * HW + (size_t)y * a.W + x] = o;
           }
         }
       }
@@ -290,10 +297,26 @@ __global__ void __launch_bounds__(kBlurThreads, 1) k_blur(BlurArgs a) {
       mbar_arrive(tempty);
     }
   }
-  (void)nacc;
   __syncthreads();
   tc_fence_after();
   if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <bool SRC_F32, int C, int RACC>
+static int launch_blur_t(const BlurArgs& a, const CUtensorMap& tm, dim3 grid, size_t sm, cudaStream_t s) {
+  cudaFuncSetAttribute(k_blur<SRC_F32, C, RACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_blur<SRC_F32, C, RACC><<<grid, kBlurThreads, sm, s>>>(a, tm);
+  return (int)cudaGetLastError();
+}
+
+template <bool SRC_F32>
+static int launch_blur_c(int C, const BlurArgs& a, const CUtensorMap& tm, dim3 grid, size_t sm, cudaStream_t s) {
+  switch (C) {
+    case 1: return launch_blur_t<SRC_F32, 1, 4>(a, tm, grid, sm, s);
+    case 2: return launch_blur_t<SRC_F32, 2, 2>(a, tm, grid, sm, s);
+    case 3: return launch_blur_t<SRC_F32, 3, 1>(a, tm, grid, sm, s);
+    default: return launch_blur_t<SRC_F32, 4, 1>(a, tm, grid, sm, s);
+  }
 }
 
 int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0, float* out,
@@ -301,13 +324,11 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   const BlurGeom& g = p->bg;
   BlurArgs a;
   a.src = src;
-  a.w = p->d_w;
   a.out = out;
   a.bimg = g.bimg;
   a.koff = g.koff;
   a.klbo = g.klbo;
   a.hsum = g.hsum;
-  a.C = p->C;
   a.H = p->H;
   a.W = p->W;
   a.T = g.T;
@@ -317,29 +338,22 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.RS = g.RS;
   a.nks = g.nks;
   a.np = g.np;
-  a.racc = g.racc;
   a.k0 = (uint32_t)seed;
   a.k1 = (uint32_t)(seed >> 32);
   a.frame0 = frame0;
   a.sigma = p->noise_sigma;
   a.normalize = p->normalize;
   a.clamp01 = p->clamp01;
-  const BlurSmem L = blur_smem_layout(a.C, a.NC, a.RS, a.racc, a.np, a.nks);
+  const BlurSmem L = blur_smem_layout(p->C, a.NC, a.RS, g.racc, a.np, a.nks);
   // TMEM: this kernel owns all 512 columns of its SM; keep shared memory above half the SM
   // so that two CTAs never co-reside and contend for tcgen05.alloc.
   size_t sm = L.total < 116 * 1024 ? 116 * 1024 : L.total;
   dim3 grid((p->W + 127) / 128, (p->H + g.RB - 1) / g.RB, F);
-  if (src_f32) {
-    cudaFuncSetAttribute(k_blur<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_blur<true><<<grid, kBlurThreads, sm, s>>>(a);
-  } else {
-    cudaFuncSetAttribute(k_blur<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_blur<false><<<grid, kBlurThreads, sm, s>>>(a);
-  }
-  return (int)cudaGetLastError();
+  return src_f32 ? launch_blur_c<true>(p->C, a, p->tmap_w, grid, sm, s)
+                 : launch_blur_c<false>(p->C, a, p->tmap_w, grid, sm, s);
 }
 
-// Host helper: rows per CTA that fit the shared-memory budget for this geometry.
+// Host helper: rows per CTA that fit the shared-memory budget, balanced over the bands.
 int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H) {
   const int NC = T + 15, G = (T + 7) / 8;
   int best = racc;
@@ -347,7 +361,6 @@ int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H) {
     const int RS = RB + 8 * G + 8;
     if (blur_smem_layout(C, NC, RS, racc, np, nks).total <= 227 * 1024) best = RB;
   }
-  // balance the bands: same number of bands, as few padded rows as possible
   const int bands = (H + best - 1) / best;
   int rb = (H + bands - 1) / bands;
   rb = (rb + racc - 1) / racc * racc;

@@ -14,7 +14,7 @@
 //   layer 3: A2 [128 x n2] K-major, B = W3 image
 // Epilogues read TMEM with tcgen05.ld (32 lanes x 16 columns per warp), add bias,
 // ReLU, repack bf16 into the next layer's A operand; the last one writes the basis
-// weights w [F][H*W][n3] bf16 (pixel-major rows for the blur epilogue).
+// weights w [F][n3][HWp] bf16 (k-major planes, fetched per row by the blur's 2-D TMA).
 // Persistent grid, one CTA per SM holding the weight images once in shared memory and
 // running two independent 128-pixel tile pipelines (one per warpgroup, own TMEM columns);
 // the next tile's inputs are prefetched with cp.async while the current one computes.
@@ -25,18 +25,18 @@ namespace p2s {
 
 struct MlpArgs {
   const uint16_t* X;    // bf16 [F][nin][HW]
-  uint16_t* wout;       // bf16 [F][HW][n3]
+  uint16_t* wout;       // bf16 [F][n3][HWp] (k-major planes)
   const uint8_t* blob;  // W1img | W2img | W3img | b1 | b2 | b3
   int nin, k1, n1, n2, n3;
   uint32_t off_w2, off_w3, off_b1, off_b2, off_b3, blob_bytes;
-  int HW, F, tiles_per_frame;
+  int HW, HWp, F, tiles_per_frame;
 };
 
 // Epilogue: TMEM columns [0, ncols) of this thread's row -> +bias (+ReLU) -> bf16.
 // mode 0: write K-major A operand rows into smem; mode 1: write global row.
 template <bool RELU, bool TO_GLOBAL>
 __device__ __forceinline__ void mlp_epilogue(uint32_t taddr, int ncols, const float* bias, uint8_t* a_smem,
-                                             uint32_t sbo, int m, uint16_t* grow) {
+                                             uint32_t sbo, int m, uint16_t* gcol, size_t gstride) {
   for (int cb = 0; cb < ncols / 16; ++cb) {
     float v[16];
     tmem_ld16(taddr + cb * 16, v);
@@ -52,10 +52,12 @@ __device__ __forceinline__ void mlp_epilogue(uint32_t taddr, int ncols, const fl
       pk[i] = pack_bf16x2(x0, x1);
     }
     if (TO_GLOBAL) {
-      if (grow) {
-        uint4* g = reinterpret_cast<uint4*>(grow + cb * 16);
-        g[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        g[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      if (gcol) {  // k-major planes: lanes (consecutive pixels) write contiguous bf16
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          gcol[(size_t)(cb * 16 + 2 * i) * gstride] = (uint16_t)(pk[i] & 0xFFFFu);
+          gcol[(size_t)(cb * 16 + 2 * i + 1) * gstride] = (uint16_t)(pk[i] >> 16);
+        }
       }
     } else {
       uint8_t* base = a_smem + (m & 7) * 16 + (m >> 3) * sbo + (2 * cb) * 128;
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(256, 1) k_mlp(MlpArgs a) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    mlp_epilogue<true, false>(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m, nullptr);
+    mlp_epilogue<true, false>(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m, nullptr, 0);
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(256, 1) k_mlp(MlpArgs a) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    mlp_epilogue<true, false>(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m, nullptr);
+    mlp_epilogue<true, false>(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m, nullptr, 0);
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
@@ -217,8 +219,8 @@ __global__ void __launch_bounds__(256, 1) k_mlp(MlpArgs a) {
     phase ^= 1;
     tc_fence_after();
     const int pix = pix0 + m;
-    uint16_t* grow = (pix < a.HW) ? a.wout + ((size_t)f * a.HW + pix) * a.n3 : nullptr;
-    mlp_epilogue<false, true>(taddr, a.n3, b3, nullptr, 0, m, grow);
+    uint16_t* gcol = (pix < a.HW) ? a.wout + (size_t)f * a.n3 * a.HWp + pix : nullptr;
+    mlp_epilogue<false, true>(taddr, a.n3, b3, nullptr, 0, m, gcol, (size_t)a.HWp);
     tc_fence_before();
     wg_sync(wg);
   }
@@ -247,6 +249,7 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   a.off_b3 = (uint32_t)g.off_b3;
   a.blob_bytes = (uint32_t)g.blob_bytes;
   a.HW = p->H * p->W;
+  a.HWp = p->HWp;
   a.F = F;
   a.tiles_per_frame = (a.HW + 127) / 128;
   const int nmax = g.n1 > g.n2 ? g.n1 : g.n2;

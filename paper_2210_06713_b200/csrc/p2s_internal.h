@@ -8,6 +8,7 @@
 
 #include "../../include/p2s.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace p2s {
@@ -89,7 +90,9 @@ struct p2s_plan_s {
   uint16_t* d_X = nullptr;      // bf16 [mb][nslots][H*W] (simulate) / [mb][Z-3][H*W] (blur API)
   float* d_tilt = nullptr;      // [mb][2][H*W]
   uint16_t* d_Iw = nullptr;     // bf16 [mb][C][H][W]
-  uint16_t* d_w = nullptr;      // bf16 [mb][H*W][n3]
+  uint16_t* d_w = nullptr;      // bf16 [mb][n3][HWp] (k-major planes)
+  int HWp = 0;                  // plane stride of d_w (H*W rounded up to 8)
+  CUtensorMap tmap_w;           // 2-D TMA view of d_w: [mb*n3 rows][HWp], box 128 x n3
   float* d_img = nullptr;       // staging for the host entry point [mb][C][H][W]
   float* d_out = nullptr;       // staging for the host entry point [mb][C][H][W]
   // per-stage timing (p2s_plan_stage_timing)
