@@ -20,9 +20,10 @@ for step in "$@"; do
     ncu_full:*)
       k="${step#ncu_full:}"
       timeout -s KILL 300 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/b_small.log 2>&1 &&
-      timeout -s KILL 1200 ncu --set full --clock-control none --import-source on -k "regex:$k" -s 1 -c 1 \
-        -o "gpurun_out/prof_$k" python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
-        > "gpurun_out/ncu_full_$k.log" 2>&1 ;;
+      n="${NCU_COUNT:-1}"
+      timeout -s KILL 1200 ncu --set full --clock-control none --import-source on -k "regex:$k" -s "${NCU_SKIP:-1}" -c "$n" \
+        -o "gpurun_out/prof_${NCU_TAG:-$k}" python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
+        > "gpurun_out/ncu_full_${NCU_TAG:-x}.log" 2>&1 ;;
   esac
 done
 echo done
