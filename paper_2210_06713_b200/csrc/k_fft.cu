@@ -124,6 +124,11 @@ __device__ __forceinline__ void stage_fft_plan(FFTPlanSmem* sp, const FFTArgs& f
   }
 }
 
+// Shared-memory index with one float2 of padding per 16: spreads the strided Stockham
+// writes over the banks.
+__device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr size_t padded_len(size_t n) { return (n + (n >> 4) + 2) & ~(size_t)1; }
+
 template <int R, int NT>
 __device__ __forceinline__ void ifft_pass(const float2* __restrict__ x, float2* __restrict__ y, int N, int Ns,
                                           uint32_t mag, int tc_log2, const float2* __restrict__ tw) {
@@ -137,7 +142,7 @@ __device__ __forceinline__ void ifft_pass(const float2* __restrict__ x, float2* 
     const int k = j - q * Ns;
     float2 v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = x[((j + r * NR) << tc_log2) + c];
+    for (int r = 0; r < R; ++r) v[r] = x[pidx(((j + r * NR) << tc_log2) + c)];
     if (Ns > 1) {
 #pragma unroll
       for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * k * ts]));
@@ -145,7 +150,7 @@ __device__ __forceinline__ void ifft_pass(const float2* __restrict__ x, float2* 
     dft_inv<R>(v);
     const int base = q * Ns * R + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) y[((base + r * Ns) << tc_log2) + c] = v[r];
+    for (int r = 0; r < R; ++r) y[pidx(((base + r * Ns) << tc_log2) + c)] = v[r];
   }
 }
 
@@ -212,7 +217,7 @@ __device__ __forceinline__ float4 spectral_noise(int ky, int kx, int P, int Q, i
   const uint32_t linm = (uint32_t)kym * Q + kxm;
   const uint32_t canon = lin < linm ? lin : linm;
   uint4 x = philox4x32_10(make_uint4(canon, (uint32_t)p, (uint32_t)frame, (uint32_t)((uint64_t)frame >> 32)), k0, k1);
-  float2 ga = box_muller(x.x, x.y), gb = box_muller(x.z, x.w);
+  float2 ga = box_muller_fast(x.x, x.y), gb = box_muller_fast(x.z, x.w);
   if (lin == linm) {  // self-conjugate: sqrt(PQ) g1 = sqrt(2) sqrt(PQ/2) g1
     const float r2 = 1.41421356237309515f;
     return make_float4(r2 * ga.x, 0.f, r2 * gb.x, 0.f);
@@ -234,8 +239,8 @@ __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int Q = a.Q;
   float2* sS = reinterpret_cast<float2*>(smem);  // [2][Q]
-  float2* X = sS + 2 * Q;                        // [Q][2] interleaved rows
-  float2* Xb = X + 2 * Q;                        // ping-pong partner
+  float2* X = sS + 2 * Q;                        // [Q][2] interleaved rows (padded)
+  float2* Xb = X + padded_len(2 * Q);            // ping-pong partner
   __shared__ FFTPlanSmem fpl;
   stage_fft_plan(&fpl, a.fq);
   const int ky = blockIdx.x, p = blockIdx.y;
@@ -251,15 +256,15 @@ __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
     for (int kx = threadIdx.x; kx < Q; kx += NT) {
       const float4 z = spectral_noise(ky, kx, a.P, Q, p, fr, a.k0, a.k1);
       const int km = kx ? Q - kx : 0;
-      X[2 * kx] = spectrum(sS[kx], z);
-      X[2 * km + 1] = spectrum(sS[Q + km], make_float4(z.x, -z.y, z.z, -z.w));  // mirror bin: conjugate noise
+      X[pidx(2 * kx)] = spectrum(sS[kx], z);
+      X[pidx(2 * km + 1)] = spectrum(sS[Q + km], make_float4(z.x, -z.y, z.z, -z.w));  // mirror: conjugate noise
     }
     __syncthreads();
     const float2* R = smem_ifft<NT>(X, Xb, &fpl, 1);
     float2* dst = a.Zout + (size_t)t * a.npairs * a.P * Q + plane;
     for (int x = threadIdx.x; x < Q; x += NT) {
-      dst[(size_t)ky * Q + x] = R[2 * x];
-      if (k1 != ky) dst[(size_t)k1 * Q + x] = R[2 * x + 1];
+      dst[(size_t)ky * Q + x] = R[pidx(2 * x)];
+      if (k1 != ky) dst[(size_t)k1 * Q + x] = R[pidx(2 * x + 1)];
     }
     __syncthreads();
   }
@@ -271,10 +276,10 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_rows_ar(RowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int Q = a.Q;
-  float2* sS = reinterpret_cast<float2*>(smem);
+  float4* st = reinterpret_cast<float4*>(smem);  // AR state first: 16-byte aligned
+  float2* sS = reinterpret_cast<float2*>(st + Q);
   float2* X = sS + Q;
-  float2* Xb = X + Q;
-  float4* st = reinterpret_cast<float4*>(Xb + Q);
+  float2* Xb = X + padded_len(Q);
   __shared__ FFTPlanSmem fpl;
   stage_fft_plan(&fpl, a.fq);
   const int ky = blockIdx.x, p = blockIdx.y;
@@ -295,13 +300,13 @@ __global__ void __launch_bounds__(NT) k_rows_ar(RowArgs a) {
                         a.alpha * o.z + a.calpha * z.z, a.alpha * o.w + a.calpha * z.w);
       }
       st[kx] = z;
-      if (out) X[kx] = spectrum(sS[kx], z);
+      if (out) X[pidx(kx)] = spectrum(sS[kx], z);
     }
     if (!out) continue;  // replay: state only
     __syncthreads();
     const float2* R = smem_ifft<NT>(X, Xb, &fpl, 0);
     float2* dst = a.Zout + (size_t)(t - a.frame0) * a.npairs * a.P * Q + row;
-    for (int x = threadIdx.x; x < Q; x += NT) dst[x] = R[x];
+    for (int x = threadIdx.x; x < Q; x += NT) dst[x] = R[pidx(x)];
     __syncthreads();
   }
   __syncthreads();
@@ -328,7 +333,7 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
   a.load_state = (ar && ar_mode == 0) ? 1 : 0;
   if (ar) {
     dim3 grid(pl->P, pl->npairs);
-    size_t sm = (size_t)pl->Q * (3 * sizeof(float2) + sizeof(float4));
+    size_t sm = ((size_t)pl->Q + 2 * padded_len(pl->Q)) * sizeof(float2) + (size_t)pl->Q * sizeof(float4) + 16;
     if (pl->Q > 1024) {
       cudaFuncSetAttribute(k_rows_ar<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       k_rows_ar<512><<<grid, 512, sm, s>>>(a);
@@ -338,7 +343,7 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
     }
   } else {
     dim3 grid(pl->P / 2 + 1, pl->npairs);
-    size_t sm = (size_t)pl->Q * 6 * sizeof(float2);
+    size_t sm = ((size_t)2 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
     if (pl->Q > 1024) {
       cudaFuncSetAttribute(k_rows_pair<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       k_rows_pair<512><<<grid, 512, sm, s>>>(a);
@@ -366,16 +371,27 @@ __global__ void __launch_bounds__(NT) k_cols(ColArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int TC = 1 << a.tc_log2;
   float2* X = reinterpret_cast<float2*>(smem);
-  float2* Xb = X + ((size_t)a.P << a.tc_log2);
+  float2* Xb = X + padded_len((size_t)a.P << a.tc_log2);
   __shared__ FFTPlanSmem fpl;
   stage_fft_plan(&fpl, a.fp);
   const int x0 = blockIdx.x * TC, p = blockIdx.y, f = blockIdx.z;
   const float2* src = a.Zin + ((size_t)f * a.npairs + p) * a.P * a.Q;
   const int n = a.P << a.tc_log2;
-  for (int w = threadIdx.x; w < n; w += NT) {
-    const int c = w & (TC - 1), ky = w >> a.tc_log2;
-    const int x = x0 + c;
-    X[w] = (x < a.Q) ? src[(size_t)ky * a.Q + x] : make_float2(0.f, 0.f);
+  constexpr int U = 8;  // batch the global loads so they are in flight together
+  for (int w0 = threadIdx.x; w0 < n; w0 += NT * U) {
+    float2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int w = w0 + u * NT;
+      const int c = w & (TC - 1), ky = w >> a.tc_log2;
+      const int x = x0 + c;
+      v[u] = (w < n && x < a.Q) ? __ldg(&src[(size_t)ky * a.Q + x]) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int w = w0 + u * NT;
+      if (w < n) X[pidx(w)] = v[u];
+    }
   }
   __syncthreads();
   const float2* R = smem_ifft<NT>(X, Xb, &fpl, a.tc_log2);
@@ -386,7 +402,7 @@ __global__ void __launch_bounds__(NT) k_cols(ColArgs a) {
     const int c = w & (TC - 1), yy = w >> a.tc_log2;
     const int x = x0 + c;
     if (x >= a.W) continue;
-    const float2 v = R[w];
+    const float2 v = R[pidx(w)];
     const size_t pix = (size_t)yy * a.W + x;
     if (MODE == 0) {
       float* z = a.zern + (size_t)f * a.Z * HW;
@@ -424,7 +440,7 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   a.tilt = pl->d_tilt;
   const int TC = 1 << tcl;
   dim3 grid((pl->W + TC - 1) / TC, pl->npairs, F);
-  size_t sm = (size_t)2 * pl->P * TC * sizeof(float2);
+  size_t sm = 2 * padded_len((size_t)pl->P * TC) * sizeof(float2);
   if (mode == 0) {
     cudaFuncSetAttribute(k_cols<0, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_cols<0, 256><<<grid, 256, sm, s>>>(a);

@@ -21,6 +21,8 @@
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
+#include <algorithm>
+
 namespace p2s {
 
 struct MlpArgs {
@@ -100,13 +102,14 @@ __device__ __forceinline__ void load_a1(const MlpArgs& a, uint8_t* A1, int f, in
 
 // Two warpgroups per CTA, each an independent tile pipeline (own A1 double buffer, A2,
 // TMEM columns, mbarrier), sharing one resident copy of the weight images.
-__global__ void __launch_bounds__(256, 1) k_mlp(MlpArgs a) {
+__global__ void __launch_bounds__(256, 1) k_mlp(const MlpArgs a, const __grid_constant__ CUtensorMap tmap_w) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sw = smem;  // weight blob
   const uint32_t blob_al = (a.blob_bytes + 127) & ~127u;
   const uint32_t a1_bytes = 128u * a.k1 * 2;
   const int nmax = a.n1 > a.n2 ? a.n1 : a.n2;
-  const uint32_t a2_bytes = 128u * nmax * 2;
+  const int na2 = nmax > a.n3 ? nmax : a.n3;  // A2 also stages the output tile
+  const uint32_t a2_bytes = 128u * na2 * 2;
   const uint32_t wg_bytes = 2 * a1_bytes + a2_bytes;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wg = tid >> 7, ltid = tid & 127;
@@ -179,6 +182,7 @@ __global__ void __launch_bounds__(256, 1) k_mlp(MlpArgs a) {
     const uint32_t sA1 = smem_u32(A1b[buf]);
     // ---- layer 1
     if (ltid == 0) {
+      tma_store_wait_read();  // the previous tile's w store has finished reading A2
       tc_fence_after();
       for (int s = 0; s < a.k1 / 16; ++s)
         umma_bf16(tmem, umma_desc(sA1 + s * 256, 128, a.k1 * 16), umma_desc(sW1 + s * 256, 128, (a.k1 / 8) * 128),
@@ -218,13 +222,23 @@ __global__ void __launch_bounds__(256, 1) k_mlp(MlpArgs a) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    const int pix = pix0 + m;
-    uint16_t* gcol = (pix < a.HW) ? a.wout + (size_t)f * a.n3 * a.HWp + pix : nullptr;
-    mlp_epilogue<false, true>(taddr, a.n3, b3, nullptr, 0, m, gcol, (size_t)a.HWp);
+    // w tile -> A2 as [n3][128 px] bf16, then one 2-D TMA store into the k-major planes
+    {
+      uint16_t* st = reinterpret_cast<uint16_t*>(A2) + m;
+      for (int cb = 0; cb < a.n3 / 16; ++cb) {
+        float v[16];
+        tmem_ld16(taddr + cb * 16, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) st[(cb * 16 + i) * 128] = f_to_bf16(v[i] + b3[cb * 16 + i]);
+      }
+    }
+    fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
+    if (ltid == 0) tma_store_2d(&tmap_w, pix0, f * a.n3, A2);
   }
   cp_async_wait<0>();
+  if (ltid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -252,13 +266,13 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   a.HWp = p->HWp;
   a.F = F;
   a.tiles_per_frame = (a.HW + 127) / 128;
-  const int nmax = g.n1 > g.n2 ? g.n1 : g.n2;
+  const int nmax = std::max(std::max(g.n1, g.n2), g.n3);
   size_t sm = ((g.blob_bytes + 127) & ~(size_t)127) + 2 * (2 * 128 * g.k1 * 2 + 128 * nmax * 2) + 32;
   cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int ntiles = F * a.tiles_per_frame;
   int grid = p->num_sms;  // persistent: one CTA (two tile pipelines) per SM
   if (2 * grid > ntiles) grid = (ntiles + 1) / 2;
-  k_mlp<<<grid, 256, sm, s>>>(a);
+  k_mlp<<<grid, 256, sm, s>>>(a, p->tmap_w);
   return (int)cudaGetLastError();
 }
 

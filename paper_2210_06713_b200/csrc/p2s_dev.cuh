@@ -42,6 +42,18 @@ __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
   return make_float2(r * c, r * s);
 }
 
+// Same transform with the SFU approximations (MUFU lg2/sin/cos): -ln u1 from lg2.approx,
+// the angle folded to [-pi, pi) (cos/sin(2 pi u2) = -cos/sin(2 pi (u2 - 1/2))).  Absolute
+// error ~1e-6; used on the per-bin spectral noise hot path.
+__device__ __forceinline__ float2 box_muller_fast(uint32_t a, uint32_t b) {
+  const float k = 2.3283064365386963e-10f;  // 2^-32
+  const float u1 = fmaf((float)a, k, k);    // (a + 1) 2^-32 in (0, 1]
+  const float r = sqrtf(-2.0f * 0.69314718055994531f * __log2f(u1));
+  float s, c;
+  __sincosf(6.28318530717958648f * fmaf((float)b, k, -0.5f), &s, &c);
+  return make_float2(-r * c, -r * s);
+}
+
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -187,6 +199,17 @@ __device__ __forceinline__ void tma_load_2d(void* sdst, const void* tmap, int c0
           smem_u32(sdst)),
       "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+
+// 2-D TMA tiled store shared -> global (bulk-group completion).
+__device__ __forceinline__ void tma_store_2d(const void* tmap, int c0, int c1, const void* ssrc) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tmap), "r"(c0),
+               "r"(c1), "r"(smem_u32(ssrc))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 }  // namespace p2s

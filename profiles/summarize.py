@@ -59,18 +59,28 @@ def full(path):
     src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source=sass"],
                          capture_output=True, text=True).stdout
     srows = list(csv.reader(io.StringIO(src)))
-    if len(srows) < 3:
-        return
-    h = srows[1]
-    data = srows[2:]
-    i_s = h.index("Warp Stall Sampling (All Samples)")
-    i_src = h.index("Source")
-    stall = [i for i, x in enumerate(h) if x.startswith("stall_") and "Not Issued" not in x]
-    tot = sum(float(r[i_s] or 0) for r in data) or 1.0
-    print("\n# top SASS stall sites (share of warp-stall samples)")
-    for r in sorted(data, key=lambda r: -float(r[i_s] or 0))[:15]:
-        top = sorted(((float(r[i] or 0), h[i]) for i in stall), reverse=True)[:2]
-        print(f"{float(r[i_s]) / tot * 100:5.1f}%  {r[i_src][:58]:58s} {', '.join(f'{n}={int(v)}' for v, n in top)}")
+    # one section per kernel: a "Kernel Name" row, a header row, then instruction rows
+    sections, cur = [], None
+    for r in srows:
+        if r and r[0] == "Kernel Name":
+            cur = [r[1] if len(r) > 1 else "?", None, []]
+            sections.append(cur)
+        elif cur is not None and cur[1] is None:
+            cur[1] = r
+        elif cur is not None:
+            cur[2].append(r)
+    for name, h, data in sections:
+        if not h or "Warp Stall Sampling (All Samples)" not in h:
+            continue
+        i_s = h.index("Warp Stall Sampling (All Samples)")
+        i_src = h.index("Source")
+        stall = [i for i, x in enumerate(h) if x.startswith("stall_") and "Not Issued" not in x]
+        num = lambda v: float(v) if v not in ("", None) else 0.0
+        tot = sum(num(r[i_s]) for r in data) or 1.0
+        print(f"\n# {name}: top SASS stall sites (share of warp-stall samples)")
+        for r in sorted(data, key=lambda r: -num(r[i_s]))[:15]:
+            top = sorted(((num(r[i]), h[i]) for i in stall), reverse=True)[:2]
+            print(f"{num(r[i_s]) / tot * 100:5.1f}%  {r[i_src][:58]:58s} {', '.join(f'{n}={int(v)}' for v, n in top)}")
 
 
 if __name__ == "__main__":
