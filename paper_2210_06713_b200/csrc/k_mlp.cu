@@ -16,8 +16,9 @@
 // ReLU, repack bf16 into the next layer's A operand; the last one writes the basis
 // weights w [F][n3][HWp] bf16 (k-major planes, fetched per row by the blur's 2-D TMA).
 // Persistent grid, one CTA per SM holding the weight images once in shared memory and
-// running two independent 128-pixel tile pipelines (one per warpgroup, own TMEM columns);
-// the next tile's inputs are prefetched with cp.async while the current one computes.
+// running four independent 128-pixel tile pipelines (one per warpgroup, 128 TMEM columns
+// each), so the tensor core always has another warpgroup's GEMM to run while one
+// warpgroup is in an epilogue; the output tile leaves through one 2-D TMA store.
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
@@ -34,35 +35,30 @@ struct MlpArgs {
   int HW, HWp, F, tiles_per_frame;
 };
 
-// Epilogue: TMEM columns [0, ncols) of this thread's row -> +bias (+ReLU) -> bf16.
-// mode 0: write K-major A operand rows into smem; mode 1: write global row.
-template <bool RELU, bool TO_GLOBAL>
-__device__ __forceinline__ void mlp_epilogue(uint32_t taddr, int ncols, const float* bias, uint8_t* a_smem,
-                                             uint32_t sbo, int m, uint16_t* gcol, size_t gstride) {
-  for (int cb = 0; cb < ncols / 16; ++cb) {
-    float v[16];
-    tmem_ld16(taddr + cb * 16, v);
-    uint32_t pk[8];
+// Epilogue of a hidden layer: TMEM columns [0, ncols) of this thread's row -> +bias -> ReLU
+// -> bf16 -> the next layer's K-major A operand (row m of a [128 x ncols] SWIZZLE_NONE
+// image, core matrices of 8 rows x 16 B, k-chunks at 128 B, 8-row groups at sbo).
+// TMEM loads are issued 32 columns at a time before one wait.
+__device__ __forceinline__ void mlp_hidden_epilogue(uint32_t taddr, int ncols, const float* bias, uint8_t* a_smem,
+                                                    uint32_t sbo, int m) {
+  uint8_t* rowbase = a_smem + (m & 7) * 16 + (m >> 3) * sbo;
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld16_issue(taddr + c0, r);
+    const bool two = c0 + 16 < ncols;
+    if (two) tmem_ld16_issue(taddr + c0 + 16, r + 16);
+    tmem_wait_ld();
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float x0 = v[2 * i] + bias[cb * 16 + 2 * i];
-      float x1 = v[2 * i + 1] + bias[cb * 16 + 2 * i + 1];
-      if (RELU) {
-        x0 = fmaxf(x0, 0.f);
-        x1 = fmaxf(x1, 0.f);
-      }
-      pk[i] = pack_bf16x2(x0, x1);
-    }
-    if (TO_GLOBAL) {
-      if (gcol) {  // k-major planes: lanes (consecutive pixels) write contiguous bf16
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !two) break;
+      uint32_t pk[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          gcol[(size_t)(cb * 16 + 2 * i) * gstride] = (uint16_t)(pk[i] & 0xFFFFu);
-          gcol[(size_t)(cb * 16 + 2 * i + 1) * gstride] = (uint16_t)(pk[i] >> 16);
-        }
+      for (int i = 0; i < 8; ++i) {
+        const float x0 = fmaxf(__uint_as_float(r[16 * h + 2 * i]) + bias[c0 + 16 * h + 2 * i], 0.f);
+        const float x1 = fmaxf(__uint_as_float(r[16 * h + 2 * i + 1]) + bias[c0 + 16 * h + 2 * i + 1], 0.f);
+        pk[i] = pack_bf16x2(x0, x1);
       }
-    } else {
-      uint8_t* base = a_smem + (m & 7) * 16 + (m >> 3) * sbo + (2 * cb) * 128;
+      uint8_t* base = rowbase + ((c0 + 16 * h) / 8) * 128;
       *reinterpret_cast<uint4*>(base) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       *reinterpret_cast<uint4*>(base + 128) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
     }
@@ -100,9 +96,13 @@ __device__ __forceinline__ void load_a1(const MlpArgs& a, uint8_t* A1, int f, in
   }
 }
 
-// Two warpgroups per CTA, each an independent tile pipeline (own A1 double buffer, A2,
-// TMEM columns, mbarrier), sharing one resident copy of the weight images.
-__global__ void __launch_bounds__(256, 1) k_mlp(const MlpArgs a, const __grid_constant__ CUtensorMap tmap_w) {
+constexpr int kMlpWG = 4;  // independent 128-pixel tile pipelines per CTA
+
+// kMlpWG warpgroups per CTA, each an independent tile pipeline (own A1, A2, 128 TMEM
+// columns, mbarrier), sharing one resident copy of the weight images; while one warpgroup
+// runs an epilogue the tensor core serves the others.
+__global__ void __launch_bounds__(128 * kMlpWG, 1)
+    k_mlp(const MlpArgs a, const __grid_constant__ CUtensorMap tmap_w) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sw = smem;  // weight blob
   const uint32_t blob_al = (a.blob_bytes + 127) & ~127u;
@@ -110,33 +110,34 @@ __global__ void __launch_bounds__(256, 1) k_mlp(const MlpArgs a, const __grid_co
   const int nmax = a.n1 > a.n2 ? a.n1 : a.n2;
   const int na2 = nmax > a.n3 ? nmax : a.n3;  // A2 also stages the output tile
   const uint32_t a2_bytes = 128u * na2 * 2;
-  const uint32_t wg_bytes = 2 * a1_bytes + a2_bytes;
+  const uint32_t wg_bytes = a1_bytes + a2_bytes;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wg = tid >> 7, ltid = tid & 127;
-  uint8_t* A1b[2] = {sw + blob_al + wg * wg_bytes, sw + blob_al + wg * wg_bytes + a1_bytes};
-  uint8_t* A2 = sw + blob_al + wg * wg_bytes + 2 * a1_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sw + blob_al + 2 * wg_bytes);
+  const int nwg = blockDim.x >> 7;
+  uint8_t* A1 = sw + blob_al + wg * wg_bytes;
+  uint8_t* A2 = A1 + a1_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sw + blob_al + nwg * wg_bytes);
   uint64_t* bar = bars + wg;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + kMlpWG);
 
-  for (uint32_t i = tid * 16; i < a.blob_bytes; i += 256 * 16)
+  for (uint32_t i = tid * 16; i < a.blob_bytes; i += blockDim.x * 16)
     *reinterpret_cast<uint4*>(sw + i) = __ldg(reinterpret_cast<const uint4*>(a.blob + i));
-  // zero the padded input planes (k in [nin, k1)) of all four A1 buffers once
-  for (int idx = tid; idx < 4 * (a.k1 - a.nin) * 16; idx += 256) {
+  // zero the padded input planes (k in [nin, k1)) of every A1 buffer once
+  if (a.k1 > a.nin) {
     const int per = (a.k1 - a.nin) * 16;
-    const int b = idx / per, r = idx % per;
-    const int k = a.nin + r % (a.k1 - a.nin), g = r / (a.k1 - a.nin);
-    uint8_t* base = sw + blob_al + (b >> 1) * wg_bytes + (b & 1) * a1_bytes;
-    *reinterpret_cast<uint4*>(base + g * (a.k1 * 16) + k * 16) = make_uint4(0, 0, 0, 0);
+    for (int idx = tid; idx < nwg * per; idx += blockDim.x) {
+      const int b = idx / per, r = idx % per;
+      const int k = a.nin + r % (a.k1 - a.nin), g = r / (a.k1 - a.nin);
+      *reinterpret_cast<uint4*>(sw + blob_al + b * wg_bytes + g * (a.k1 * 16) + k * 16) = make_uint4(0, 0, 0, 0);
+    }
   }
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < nwg; ++i) mbar_init(&bars[i], 1);
     mbar_fence_init();
   }
-  const int nalloc = nmax > a.n3 ? nmax : a.n3;
-  const uint32_t cols_wg = nalloc <= 32 ? 32 : nalloc <= 64 ? 64 : nalloc <= 128 ? 128 : 256;
-  const uint32_t ncols = 2 * cols_wg;
+  const int wmax = na2;  // widest accumulator (n1, n2 or n3)
+  const uint32_t cols_wg = wmax <= 32 ? 32 : wmax <= 64 ? 64 : wmax <= 128 ? 128 : 256;
+  const uint32_t ncols = nwg * cols_wg;  // <= 512 (the launcher picks nwg)
   if (warp == 0) tmem_alloc(tslot, ncols);
   tc_fence_before();
   __syncthreads();
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(256, 1) k_mlp(const MlpArgs a, const __grid_co
   const float* b1 = reinterpret_cast<const float*>(sw + a.off_b1);
   const float* b2 = reinterpret_cast<const float*>(sw + a.off_b2);
   const float* b3 = reinterpret_cast<const float*>(sw + a.off_b3);
-  const uint32_t sA2 = smem_u32(A2);
+  const uint32_t sA1 = smem_u32(A1), sA2 = smem_u32(A2);
   const uint32_t sW1 = smem_u32(sw), sW2 = smem_u32(sw + a.off_w2), sW3 = smem_u32(sw + a.off_w3);
   const uint32_t id1 = umma_idesc_bf16(128, a.n1, true, false);
   const uint32_t id2 = umma_idesc_bf16(128, a.n2, false, false);
@@ -157,29 +158,17 @@ __global__ void __launch_bounds__(256, 1) k_mlp(const MlpArgs a, const __grid_co
   uint32_t phase = 0;
   const int ntiles = a.F * a.tiles_per_frame;
   const bool async = (a.HW % 8) == 0;
-  const int stride = 2 * gridDim.x;
-  int tile = 2 * blockIdx.x + wg;
-  int buf = 0;
-  if (tile < ntiles) {
-    const int f = tile / a.tiles_per_frame;
-    load_a1(a, A1b[0], f, (tile - f * a.tiles_per_frame) * 128, ltid, async);
-  }
-  cp_async_commit();
+  const int stride = nwg * gridDim.x;
 
-  for (; tile < ntiles; tile += stride, buf ^= 1) {
+  for (int tile = nwg * blockIdx.x + wg; tile < ntiles; tile += stride) {
     const int f = tile / a.tiles_per_frame;
     const int pix0 = (tile - f * a.tiles_per_frame) * 128;
-    const int nxt = tile + stride;
-    if (nxt < ntiles) {  // prefetch the next tile while this one runs
-      const int fn = nxt / a.tiles_per_frame;
-      load_a1(a, A1b[buf ^ 1], fn, (nxt - fn * a.tiles_per_frame) * 128, ltid, async);
-    }
+    load_a1(a, A1, f, pix0, ltid, async);
     cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<0>();
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
-    const uint32_t sA1 = smem_u32(A1b[buf]);
     // ---- layer 1
     if (ltid == 0) {
       tma_store_wait_read();  // the previous tile's w store has finished reading A2
@@ -192,7 +181,7 @@ __global__ void __launch_bounds__(256, 1) k_mlp(const MlpArgs a, const __grid_co
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    mlp_epilogue<true, false>(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m, nullptr, 0);
+    mlp_hidden_epilogue(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m);
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
@@ -207,7 +196,7 @@ __global__ void __launch_bounds__(256, 1) k_mlp(const MlpArgs a, const __grid_co
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    mlp_epilogue<true, false>(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m, nullptr, 0);
+    mlp_hidden_epilogue(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m);
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
@@ -225,11 +214,18 @@ __global__ void __launch_bounds__(256, 1) k_mlp(const MlpArgs a, const __grid_co
     // w tile -> A2 as [n3][128 px] bf16, then one 2-D TMA store into the k-major planes
     {
       uint16_t* st = reinterpret_cast<uint16_t*>(A2) + m;
-      for (int cb = 0; cb < a.n3 / 16; ++cb) {
-        float v[16];
-        tmem_ld16(taddr + cb * 16, v);
+      for (int c0 = 0; c0 < a.n3; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld16_issue(taddr + c0, r);
+        const bool two = c0 + 16 < a.n3;
+        if (two) tmem_ld16_issue(taddr + c0 + 16, r + 16);
+        tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) st[(cb * 16 + i) * 128] = f_to_bf16(v[i] + b3[cb * 16 + i]);
+        for (int i = 0; i < 16; ++i) st[(c0 + i) * 128] = f_to_bf16(__uint_as_float(r[i]) + b3[c0 + i]);
+        if (two) {
+#pragma unroll
+          for (int i = 16; i < 32; ++i) st[(c0 + i) * 128] = f_to_bf16(__uint_as_float(r[i]) + b3[c0 + i]);
+        }
       }
     }
     fence_async_smem();
@@ -237,7 +233,6 @@ __global__ void __launch_bounds__(256, 1) k_mlp(const MlpArgs a, const __grid_co
     wg_sync(wg);
     if (ltid == 0) tma_store_2d(&tmap_w, pix0, f * a.n3, A2);
   }
-  cp_async_wait<0>();
   if (ltid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
@@ -267,12 +262,17 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   a.F = F;
   a.tiles_per_frame = (a.HW + 127) / 128;
   const int nmax = std::max(std::max(g.n1, g.n2), g.n3);
-  size_t sm = ((g.blob_bytes + 127) & ~(size_t)127) + 2 * (2 * 128 * g.k1 * 2 + 128 * nmax * 2) + 32;
+  const int cols_wg = nmax <= 32 ? 32 : nmax <= 64 ? 64 : nmax <= 128 ? 128 : 256;
+  const size_t blob_al = (g.blob_bytes + 127) & ~(size_t)127;
+  const size_t per_wg = 128 * g.k1 * 2 + 128 * nmax * 2;
+  int nwg = std::min(kMlpWG, 512 / cols_wg);
+  while (nwg > 1 && blob_al + nwg * per_wg + 64 > 227 * 1024) --nwg;
+  size_t sm = blob_al + nwg * per_wg + 64;
   cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int ntiles = F * a.tiles_per_frame;
-  int grid = p->num_sms;  // persistent: one CTA (two tile pipelines) per SM
-  if (2 * grid > ntiles) grid = (ntiles + 1) / 2;
-  k_mlp<<<grid, 256, sm, s>>>(a, p->tmap_w);
+  int grid = p->num_sms;  // persistent: one CTA (nwg tile pipelines) per SM
+  if (nwg * grid > ntiles) grid = (ntiles + nwg - 1) / nwg;
+  k_mlp<<<grid, 128 * nwg, sm, s>>>(a, p->tmap_w);
   return (int)cudaGetLastError();
 }
 
