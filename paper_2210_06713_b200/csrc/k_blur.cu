@@ -65,7 +65,7 @@ __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int 
   BlurSmem L;
   L.tile_bytes = ((uint32_t)NC * RS * 16 + 127) & ~127u;
   L.w_bytes = (uint32_t)racc * np * 128 * 2;  // [racc][np][128 px] bf16
-  if (L.w_bytes < 6u * 176 * 4) L.w_bytes = 6u * 176 * 4;  // doubles as the loader's staging rows
+  if (L.w_bytes < 6u * 4 * 192 * 4) L.w_bytes = 6u * 4 * 192 * 4;  // doubles as the loader staging rows
   L.b_bytes = (uint32_t)np * 32;
   L.off_w = C * L.tile_bytes;
   L.off_ring = (L.off_w + L.w_bytes + 127) & ~127u;
@@ -116,28 +116,49 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   if (warp == 0) tmem_alloc(tslot, 512);
 
   // ---- source tiles of every channel: chunk cc of row rl holds the 8 pixels at window
-  // offsets cc + 16 j of source row y0 - c + rl (mirror boundary).  Each warp stages a
-  // coalesced row segment in smem, then packs the chunks.
+  // offsets cc + 16 j of source row y0 - c + rl (mirror boundary).  Each warp stages
+  // kLoadRows coalesced row segments at once (all their loads in flight together), then
+  // packs the chunks.
   {
-    float* stg = reinterpret_cast<float*>(wbuf) + warp * 176;
+    constexpr int kLoadRows = 4;
+    constexpr int kSeg = 192;  // >= 128 + T - 1 for T <= 63
+    float* stg = reinterpret_cast<float*>(wbuf) + warp * kLoadRows * kSeg;
     const int rows_real = a.RB + a.T - 1;
     const int seg = 128 + a.T - 1;
+    const int nwarps = kBlurThreads / 32;
     for (int ch = 0; ch < C; ++ch) {
       uint8_t* tile = smem + ch * L.tile_bytes;
       const size_t plane = ((size_t)f * C + ch) * HW;
-      for (int rl = warp; rl < a.RS; rl += kBlurThreads / 32) {
-        const bool real = rl < rows_real;
-        if (real) {
+      for (int rl0 = warp * kLoadRows; rl0 < a.RS; rl0 += nwarps * kLoadRows) {
+        float v[kLoadRows][(kSeg + 31) / 32];
+#pragma unroll
+        for (int u = 0; u < kLoadRows; ++u) {
+          const int rl = rl0 + u;
           const size_t rowb = plane + (size_t)reflect_idx(y0 - a.c + rl, a.H) * a.W;
-          for (int i = lane; i < seg; i += 32) stg[i] = load_src<SRC_F32>(a.src, rowb + reflect_idx(x0 - a.c + i, a.W));
+#pragma unroll
+          for (int e = 0; e < (kSeg + 31) / 32; ++e) {
+            const int i = lane + 32 * e;
+            v[u][e] = (rl < rows_real && i < seg) ? load_src<SRC_F32>(a.src, rowb + reflect_idx(x0 - a.c + i, a.W))
+                                                  : 0.f;
+          }
         }
+#pragma unroll
+        for (int u = 0; u < kLoadRows; ++u)
+#pragma unroll
+          for (int e = 0; e < (kSeg + 31) / 32; ++e)
+            if (lane + 32 * e < kSeg) stg[u * kSeg + lane + 32 * e] = v[u][e];
         __syncwarp();
-        for (int cc = lane; cc < a.NC; cc += 32) {
-          uint4 v = make_uint4(0, 0, 0, 0);
-          if (real)
-            v = make_uint4(pack_bf16x2(stg[cc], stg[cc + 16]), pack_bf16x2(stg[cc + 32], stg[cc + 48]),
-                           pack_bf16x2(stg[cc + 64], stg[cc + 80]), pack_bf16x2(stg[cc + 96], stg[cc + 112]));
-          *reinterpret_cast<uint4*>(tile + (size_t)cc * sbo_src + rl * 16) = v;
+        for (int u = 0; u < kLoadRows; ++u) {
+          const int rl = rl0 + u;
+          if (rl >= a.RS) break;
+          const float* sr = stg + u * kSeg;
+          for (int cc = lane; cc < a.NC; cc += 32) {
+            uint4 q = make_uint4(0, 0, 0, 0);
+            if (rl < rows_real)
+              q = make_uint4(pack_bf16x2(sr[cc], sr[cc + 16]), pack_bf16x2(sr[cc + 32], sr[cc + 48]),
+                             pack_bf16x2(sr[cc + 64], sr[cc + 80]), pack_bf16x2(sr[cc + 96], sr[cc + 112]));
+            *reinterpret_cast<uint4*>(tile + (size_t)cc * sbo_src + rl * 16) = q;
+          }
         }
         __syncwarp();
       }

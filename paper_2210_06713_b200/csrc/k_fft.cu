@@ -112,11 +112,13 @@ struct FFTPlanSmem {
   const float2* tw;
 };
 
-__device__ __forceinline__ void stage_fft_plan(FFTPlanSmem* sp, const FFTArgs& f) {
+// Stage the radix plan and the twiddle table (N float2) in shared memory.
+__device__ __forceinline__ void stage_fft_plan(FFTPlanSmem* sp, const FFTArgs& f, float2* tw_smem) {
+  for (int k = threadIdx.x; k < f.N; k += blockDim.x) tw_smem[k] = __ldg(&f.tw[k]);
   if (threadIdx.x == 0) {
     sp->nrad = f.nrad;
     sp->N = f.N;
-    sp->tw = f.tw;
+    sp->tw = tw_smem;
   }
   if (threadIdx.x < kMaxRadix) {
     sp->rad[threadIdx.x] = f.rad[threadIdx.x];
@@ -145,7 +147,7 @@ __device__ __forceinline__ void ifft_pass(const float2* __restrict__ x, float2* 
     for (int r = 0; r < R; ++r) v[r] = x[pidx(((j + r * NR) << tc_log2) + c)];
     if (Ns > 1) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * k * ts]));
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[r * k * ts]);
     }
     dft_inv<R>(v);
     const int base = q * Ns * R + k;
@@ -238,11 +240,12 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int Q = a.Q;
-  float2* sS = reinterpret_cast<float2*>(smem);  // [2][Q]
-  float2* X = sS + 2 * Q;                        // [Q][2] interleaved rows (padded)
-  float2* Xb = X + padded_len(2 * Q);            // ping-pong partner
+  float2* twq = reinterpret_cast<float2*>(smem);  // [Q] twiddles
+  float2* sS = twq + Q;                            // [2][Q]
+  float2* X = sS + 2 * Q;                          // [Q][2] interleaved rows (padded)
+  float2* Xb = X + padded_len(2 * Q);              // ping-pong partner
   __shared__ FFTPlanSmem fpl;
-  stage_fft_plan(&fpl, a.fq);
+  stage_fft_plan(&fpl, a.fq, twq);
   const int ky = blockIdx.x, p = blockIdx.y;
   const int k1 = ky ? a.P - ky : 0;
   const size_t plane = (size_t)p * a.P * Q;
@@ -277,11 +280,12 @@ __global__ void __launch_bounds__(NT) k_rows_ar(RowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int Q = a.Q;
   float4* st = reinterpret_cast<float4*>(smem);  // AR state first: 16-byte aligned
-  float2* sS = reinterpret_cast<float2*>(st + Q);
+  float2* twq = reinterpret_cast<float2*>(st + Q);
+  float2* sS = twq + Q;
   float2* X = sS + Q;
   float2* Xb = X + padded_len(Q);
   __shared__ FFTPlanSmem fpl;
-  stage_fft_plan(&fpl, a.fq);
+  stage_fft_plan(&fpl, a.fq, twq);
   const int ky = blockIdx.x, p = blockIdx.y;
   const size_t row = ((size_t)p * a.P + ky) * Q;
   for (int kx = threadIdx.x; kx < Q; kx += NT) {
@@ -333,7 +337,7 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
   a.load_state = (ar && ar_mode == 0) ? 1 : 0;
   if (ar) {
     dim3 grid(pl->P, pl->npairs);
-    size_t sm = ((size_t)pl->Q + 2 * padded_len(pl->Q)) * sizeof(float2) + (size_t)pl->Q * sizeof(float4) + 16;
+    size_t sm = ((size_t)2 * pl->Q + 2 * padded_len(pl->Q)) * sizeof(float2) + (size_t)pl->Q * sizeof(float4) + 16;
     if (pl->Q > 1024) {
       cudaFuncSetAttribute(k_rows_ar<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       k_rows_ar<512><<<grid, 512, sm, s>>>(a);
@@ -343,7 +347,7 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
     }
   } else {
     dim3 grid(pl->P / 2 + 1, pl->npairs);
-    size_t sm = ((size_t)2 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
+    size_t sm = ((size_t)3 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
     if (pl->Q > 1024) {
       cudaFuncSetAttribute(k_rows_pair<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       k_rows_pair<512><<<grid, 512, sm, s>>>(a);
@@ -370,10 +374,11 @@ template <int MODE, int NT>
 __global__ void __launch_bounds__(NT) k_cols(ColArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int TC = 1 << a.tc_log2;
-  float2* X = reinterpret_cast<float2*>(smem);
+  float2* twp = reinterpret_cast<float2*>(smem);
+  float2* X = twp + a.P;
   float2* Xb = X + padded_len((size_t)a.P << a.tc_log2);
   __shared__ FFTPlanSmem fpl;
-  stage_fft_plan(&fpl, a.fp);
+  stage_fft_plan(&fpl, a.fp, twp);
   const int x0 = blockIdx.x * TC, p = blockIdx.y, f = blockIdx.z;
   const float2* src = a.Zin + ((size_t)f * a.npairs + p) * a.P * a.Q;
   const int n = a.P << a.tc_log2;
@@ -440,7 +445,7 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   a.tilt = pl->d_tilt;
   const int TC = 1 << tcl;
   dim3 grid((pl->W + TC - 1) / TC, pl->npairs, F);
-  size_t sm = 2 * padded_len((size_t)pl->P * TC) * sizeof(float2);
+  size_t sm = ((size_t)pl->P + 2 * padded_len((size_t)pl->P * TC)) * sizeof(float2);
   if (mode == 0) {
     cudaFuncSetAttribute(k_cols<0, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_cols<0, 256><<<grid, 256, sm, s>>>(a);

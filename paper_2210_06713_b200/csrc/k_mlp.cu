@@ -160,12 +160,16 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
   const bool async = (a.HW % 8) == 0;
   const int stride = nwg * gridDim.x;
 
-  for (int tile = nwg * blockIdx.x + wg; tile < ntiles; tile += stride) {
+  int tile = nwg * blockIdx.x + wg;
+  if (tile < ntiles) {
+    const int f = tile / a.tiles_per_frame;
+    load_a1(a, A1, f, (tile - f * a.tiles_per_frame) * 128, ltid, async);
+  }
+  cp_async_commit();
+  for (; tile < ntiles; tile += stride) {
     const int f = tile / a.tiles_per_frame;
     const int pix0 = (tile - f * a.tiles_per_frame) * 128;
-    load_a1(a, A1, f, pix0, ltid, async);
-    cp_async_commit();
-    cp_async_wait<0>();
+    cp_async_wait<0>();  // this tile's A1 (issued during the previous tile's layers 2-3)
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
@@ -181,6 +185,14 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
+    {  // A1 is free once layer 1 has completed: prefetch the next tile's inputs
+      const int nxt = tile + stride;
+      if (nxt < ntiles) {
+        const int fn = nxt / a.tiles_per_frame;
+        load_a1(a, A1, fn, (nxt - fn * a.tiles_per_frame) * 128, ltid, async);
+      }
+      cp_async_commit();
+    }
     mlp_hidden_epilogue(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m);
     fence_async_smem();
     tc_fence_before();
