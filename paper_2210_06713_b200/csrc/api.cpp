@@ -128,7 +128,9 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   g.np = round16(K);
   g.racc = std::max(1, 4 / p->C);
   g.nks = (T * G + 1) / 2;
-  g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, g.nks, p->H);
+  const char* pe = getenv("P2S_BLUR_PAIR");
+  g.pair = pe ? (atoi(pe) != 0) : true;
+  g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, g.nks, p->H, g.pair);
   g.RS = g.RB + 8 * G + 8;
   const uint32_t sbo = (uint32_t)g.RS * 16;
   struct Grp { int tx, gi; uint32_t off; };
@@ -167,6 +169,16 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   }
   P2S_CUDA(cudaMalloc(&g.bimg, img.size()), "cudaMalloc blur B");
   P2S_CUDA(cudaMemcpy(g.bimg, img.data(), img.size(), cudaMemcpyHostToDevice), "copy blur B");
+  {  // pair-mode copy: [half][t][np/2 rows x 32 B]
+    const size_t hb = bbytes / 2;
+    std::vector<uint8_t> img2(img.size());
+    for (int h = 0; h < 2; ++h)
+      for (int t = 0; t < g.nks; ++t)
+        std::memcpy(img2.data() + ((size_t)h * g.nks + t) * hb, img.data() + (size_t)t * bbytes + h * hb, hb);
+    P2S_CUDA(cudaMalloc(&g.bimg2, img2.size() + 4096), "cudaMalloc blur B2");
+    P2S_CUDA(cudaMemset(g.bimg2, 0, img2.size() + 4096), "memset blur B2");
+    P2S_CUDA(cudaMemcpy(g.bimg2, img2.data(), img2.size(), cudaMemcpyHostToDevice), "copy blur B2");
+  }
   P2S_CUDA(cudaMalloc(&g.koff, sizeof(uint32_t) * g.nks), "cudaMalloc koff");
   P2S_CUDA(cudaMemcpy(g.koff, koff.data(), sizeof(uint32_t) * g.nks, cudaMemcpyHostToDevice), "copy koff");
   P2S_CUDA(cudaMalloc(&g.klbo, sizeof(uint32_t) * g.nks), "cudaMalloc klbo");
@@ -238,6 +250,16 @@ static p2s_status alloc_workspace(p2s_plan_s* p) {
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(P2S_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  {  // B halves for the CTA-pair blur: rows of 256 B; one box = 2 consecutive K-steps of one half
+    const int rows_per_step = np / 16;  // (np/2 rows x 32 B) / 256 B
+    cuuint64_t bd[2] = {128, (cuuint64_t)(2 * p->bg.nks * rows_per_step + 16)};
+    cuuint64_t bs[1] = {256};
+    cuuint32_t bb[2] = {128, (cuuint32_t)(2 * rows_per_step)};
+    r = encode(&p->tmap_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->bg.bimg2, bd, bs, bb, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(P2S_ERR_CUDA, "cuTensorMapEncodeTiled (B) failed");
+  }
   return P2S_OK;
 }
 
@@ -252,6 +274,7 @@ static void free_plan(p2s_plan_s* p) {
   cudaFree(p->d_mlp_fold);
   cudaFree(p->d_mlp_plain);
   cudaFree(p->bg.bimg);
+  cudaFree(p->bg.bimg2);
   cudaFree(p->bg.koff);
   cudaFree(p->bg.klbo);
   cudaFree(p->bg.hsum);

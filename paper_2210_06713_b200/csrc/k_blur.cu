@@ -20,6 +20,9 @@
 // planes) arrive by one 2-D TMA tile load per row.  The epilogue warps read the
 // accumulators with tcgen05.ld, form sum_k w_k(x) conv_k(x), apply step 5 (normalise,
 // Philox noise, clamp) and write the output: the only HBM write of the frame.
+// PAIR mode (CTA pairs on adjacent x-tiles, cluster of 2): the even CTA issues
+// tcgen05.mma.cta_group::2 with M = 256; each CTA supplies its own 128 pixels of A and half
+// of the bases of B, halving the shared-memory and L2 traffic of the B operand per SM.
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
@@ -61,27 +64,27 @@ struct BlurSmem {
   uint32_t off_w, off_ring, off_desc, off_hsum, off_bar, total;
 };
 
-__host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int racc, int np, int nks) {
+__host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int racc, int np, int nks, bool pair) {
   BlurSmem L;
   L.tile_bytes = ((uint32_t)NC * RS * 16 + 127) & ~127u;
   L.w_bytes = (uint32_t)racc * np * 128 * 2;  // [racc][np][128 px] bf16
   if (L.w_bytes < 6u * 4 * 192 * 4) L.w_bytes = 6u * 4 * 192 * 4;  // doubles as the loader staging rows
-  L.b_bytes = (uint32_t)np * 32;
+  L.b_bytes = (uint32_t)np * 32 / (pair ? 2 : 1);  // per K-step: this CTA's rows of B
   L.off_w = C * L.tile_bytes;
   L.off_ring = (L.off_w + L.w_bytes + 127) & ~127u;
   L.off_desc = L.off_ring + kBlurStages * kStepsPerStage * L.b_bytes;
   L.off_hsum = L.off_desc + 8 * nks;
   L.off_bar = (L.off_hsum + 4 * np + 15) & ~15u;
-  L.total = L.off_bar + (2 * kBlurStages + 3) * 8 + 16;
+  L.total = L.off_bar + (2 * kBlurStages + 4) * 8 + 16;
   return L;
 }
 
-template <bool SRC_F32, int C, int RACC>
+template <bool SRC_F32, int C, int RACC, bool PAIR>
 __global__ void __launch_bounds__(kBlurThreads, 1)
-    k_blur(const BlurArgs a, const __grid_constant__ CUtensorMap tmap_w) {
+    k_blur(const BlurArgs a, const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_b) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const BlurSmem L = blur_smem_layout(C, a.NC, a.RS, RACC, a.np, a.nks);
+  const BlurSmem L = blur_smem_layout(C, a.NC, a.RS, RACC, a.np, a.nks, PAIR);
   const uint32_t sbo_src = (uint32_t)a.RS * 16;
   uint8_t* wbuf = smem + L.off_w;
   uint8_t* ring = smem + L.off_ring;
@@ -91,9 +94,12 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   uint64_t* full = bars;
   uint64_t* empty = bars + kBlurStages;
   uint64_t* tfull = bars + 2 * kBlurStages;
-  uint64_t* tempty = tfull + 1;
+  uint64_t* tempty = tfull + 1;  // TMEM free (on the MMA-issuing CTA; 4 or 8 warp arrivals)
   uint64_t* wfull = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(wfull + 1);
+  uint64_t* wempty = tfull + 3;  // this CTA's w buffer free (4 warp arrivals)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(wempty + 1);
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
 
   const int x0 = blockIdx.x * 128, y0 = blockIdx.y * a.RB, f = blockIdx.z;
   const int HW = a.H * a.W;
@@ -109,11 +115,17 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 128);
+    mbar_init(tempty, PAIR ? 8 : 4);
     mbar_init(wfull, 1);
+    mbar_init(wempty, 4);
     mbar_fence_init();
   }
-  if (warp == 0) tmem_alloc(tslot, 512);
+  if (warp == 0) {
+    if (PAIR)
+      tmem_alloc_pair(tslot, 512);
+    else
+      tmem_alloc(tslot, 512);
+  }
 
   // ---- source tiles of every channel: chunk cc of row rl holds the 8 pixels at window
   // offsets cc + 16 j of source row y0 - c + rl (mirror boundary).  Each warp stages
@@ -167,6 +179,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // both source tiles and all barrier inits visible to the pair
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
@@ -178,14 +191,15 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     // ---- TMA producer: B tiles stream continuously; the w rows of group rg are issued as
     // soon as the epilogue has released group rg-1 (single w buffer).
     uint32_t stage = 0, phase = 0;
-    const uint32_t s_tempty = smem_u32(tempty);
+    const uint32_t s_wempty = smem_u32(wempty);
     auto issue_w = [&](int rg) {
       int nrow = 0;
-      for (int r = 0; r < RACC; ++r) nrow += (y0 + rg * RACC + r < a.H) ? 1 : 0;
+      if (x0 < a.W)
+        for (int r = 0; r < RACC; ++r) nrow += (y0 + rg * RACC + r < a.H) ? 1 : 0;
       mbar_arrive_expect_tx(wfull, (uint32_t)nrow * a.np * 128 * 2);
       for (int r = 0; r < RACC; ++r) {
         const int y = y0 + rg * RACC + r;
-        if (y < a.H) tma_load_2d(wbuf + (size_t)r * a.np * 256, &tmap_w, y * a.W + x0, f * a.np, wfull);
+        if (y < a.H && x0 < a.W) tma_load_2d(wbuf + (size_t)r * a.np * 256, &tmap_w, y * a.W + x0, f * a.np, wfull);
       }
     };
     for (int rg = 0; rg < n_rg; ++rg) {
@@ -196,7 +210,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
         w_done = true;
       }
       for (int st = 0; st < nst; ++st) {
-        if (!w_done && mbar_try_wait(s_tempty, (rg - 1) & 1)) {
+        if (!w_done && mbar_try_wait(s_wempty, (rg - 1) & 1)) {
           if (elect_one()) issue_w(rg);
           __syncwarp();
           w_done = true;
@@ -205,8 +219,14 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
         const int t0 = st * kStepsPerStage;
         const int nt = min(kStepsPerStage, a.nks - t0);
         if (elect_one()) {
-          mbar_arrive_expect_tx(&full[stage], nt * bbytes);
-          bulk_g2s(ring + stage * kStepsPerStage * bbytes, a.bimg + (size_t)t0 * bbytes, nt * bbytes, &full[stage]);
+          if (PAIR) {  // both CTAs load their half; the bytes count on the leader's barrier
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStepsPerStage * bbytes);
+            tma_load_2d_pair(ring + stage * kStepsPerStage * bbytes, &tmap_b, 0,
+                             ((int)rank * a.nks + t0) * (int)(bbytes / 256), &full[stage]);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], nt * bbytes);
+            bulk_g2s(ring + stage * kStepsPerStage * bbytes, a.bimg + (size_t)t0 * bbytes, nt * bbytes, &full[stage]);
+          }
         }
         __syncwarp();
         if (++stage == kBlurStages) {
@@ -215,14 +235,14 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
         }
       }
       if (!w_done) {
-        mbar_wait(tempty, (rg - 1) & 1);
+        mbar_wait(wempty, (rg - 1) & 1);
         if (elect_one()) issue_w(rg);
         __syncwarp();
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && leader) {
     // ---- MMA issuer (whole warp, one elected lane issues): C x RACC accumulators per K-step
-    const uint32_t idesc = umma_idesc_bf16(128, a.np, true, false);
+    const uint32_t idesc = umma_idesc_bf16(PAIR ? 256 : 128, a.np, true, false);
     uint32_t stage = 0, phase = 0;
     const uint64_t ch_step = (uint64_t)(L.tile_bytes >> 4);
     for (int rg = 0; rg < n_rg; ++rg) {
@@ -245,11 +265,18 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
 #pragma unroll
               for (int ch = 0; ch < C; ++ch)
 #pragma unroll
-                for (int r = 0; r < RACC; ++r)
-                  umma_bf16(tmem + (ch * RACC + r) * kAccStride, ad + ch * ch_step + (uint64_t)r, bd, idesc, acc);
+                for (int r = 0; r < RACC; ++r) {
+                  if (PAIR)
+                    umma_bf16_pair(tmem + (ch * RACC + r) * kAccStride, ad + ch * ch_step + (uint64_t)r, bd, idesc, acc);
+                  else
+                    umma_bf16(tmem + (ch * RACC + r) * kAccStride, ad + ch * ch_step + (uint64_t)r, bd, idesc, acc);
+                }
             }
           }
-          umma_commit(&empty[stage]);
+          if (PAIR)
+            umma_commit_pair(&empty[stage]);
+          else
+            umma_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == kBlurStages) {
@@ -257,10 +284,15 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
           phase ^= 1;
         }
       }
-      if (elect_one()) umma_commit(tfull);
+      if (elect_one()) {
+        if (PAIR)
+          umma_commit_pair(tfull);
+        else
+          umma_commit(tfull);
+      }
       __syncwarp();
     }
-  } else {
+  } else if (warp >= 2) {
     // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
     const int qd = warp & 3;
     const int m = qd * 32 + lane;
@@ -268,6 +300,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     const int x = x0 + q;
     const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
     const uint16_t* wq = reinterpret_cast<const uint16_t*>(wbuf) + q;
+    const uint32_t t_tempty_leader = PAIR ? mapa_shared(tempty, 0) : 0u;
     for (int rg = 0; rg < n_rg; ++rg) {
       mbar_wait(tfull, rg & 1);
       mbar_wait(wfull, rg & 1);
@@ -315,28 +348,57 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(tempty);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(wempty);
+        if (PAIR)
+          mbar_arrive_cluster(t_tempty_leader);
+        else
+          mbar_arrive(tempty);
+      }
     }
   }
+  tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // the pair's MMAs and remote arrivals are all done
   tc_fence_after();
-  if (warp == 0) tmem_dealloc(tmem, 512);
+  if (warp == 0) {
+    if (PAIR)
+      tmem_dealloc_pair(tmem, 512);
+    else
+      tmem_dealloc(tmem, 512);
+  }
 }
 
-template <bool SRC_F32, int C, int RACC>
-static int launch_blur_t(const BlurArgs& a, const CUtensorMap& tm, dim3 grid, size_t sm, cudaStream_t s) {
-  cudaFuncSetAttribute(k_blur<SRC_F32, C, RACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_blur<SRC_F32, C, RACC><<<grid, kBlurThreads, sm, s>>>(a, tm);
+template <bool SRC_F32, int C, int RACC, bool PAIR>
+static int launch_blur_t(const BlurArgs& a, const CUtensorMap& tw, const CUtensorMap& tb, dim3 grid, size_t sm,
+                         cudaStream_t s) {
+  auto kern = k_blur<SRC_F32, C, RACC, PAIR>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kBlurThreads);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a, tw, tb);
   return (int)cudaGetLastError();
 }
 
-template <bool SRC_F32>
-static int launch_blur_c(int C, const BlurArgs& a, const CUtensorMap& tm, dim3 grid, size_t sm, cudaStream_t s) {
+template <bool SRC_F32, bool PAIR>
+static int launch_blur_c(int C, const BlurArgs& a, const CUtensorMap& tw, const CUtensorMap& tb, dim3 grid,
+                         size_t sm, cudaStream_t s) {
   switch (C) {
-    case 1: return launch_blur_t<SRC_F32, 1, 4>(a, tm, grid, sm, s);
-    case 2: return launch_blur_t<SRC_F32, 2, 2>(a, tm, grid, sm, s);
-    case 3: return launch_blur_t<SRC_F32, 3, 1>(a, tm, grid, sm, s);
-    default: return launch_blur_t<SRC_F32, 4, 1>(a, tm, grid, sm, s);
+    case 1: return launch_blur_t<SRC_F32, 1, 4, PAIR>(a, tw, tb, grid, sm, s);
+    case 2: return launch_blur_t<SRC_F32, 2, 2, PAIR>(a, tw, tb, grid, sm, s);
+    case 3: return launch_blur_t<SRC_F32, 3, 1, PAIR>(a, tw, tb, grid, sm, s);
+    default: return launch_blur_t<SRC_F32, 4, 1, PAIR>(a, tw, tb, grid, sm, s);
   }
 }
 
@@ -365,22 +427,28 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.sigma = p->noise_sigma;
   a.normalize = p->normalize;
   a.clamp01 = p->clamp01;
-  const BlurSmem L = blur_smem_layout(p->C, a.NC, a.RS, g.racc, a.np, a.nks);
+  const bool pair = g.pair;
+  const BlurSmem L = blur_smem_layout(p->C, a.NC, a.RS, g.racc, a.np, a.nks, pair);
   // TMEM: this kernel owns all 512 columns of its SM; keep shared memory above half the SM
   // so that two CTAs never co-reside and contend for tcgen05.alloc.
   size_t sm = L.total < 116 * 1024 ? 116 * 1024 : L.total;
-  dim3 grid((p->W + 127) / 128, (p->H + g.RB - 1) / g.RB, F);
-  return src_f32 ? launch_blur_c<true>(p->C, a, p->tmap_w, grid, sm, s)
-                 : launch_blur_c<false>(p->C, a, p->tmap_w, grid, sm, s);
+  int gx = (p->W + 127) / 128;
+  if (pair) gx = (gx + 1) / 2 * 2;  // whole CTA pairs; a trailing dummy CTA stores nothing
+  dim3 grid(gx, (p->H + g.RB - 1) / g.RB, F);
+  if (pair)
+    return src_f32 ? launch_blur_c<true, true>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s)
+                   : launch_blur_c<false, true>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s);
+  return src_f32 ? launch_blur_c<true, false>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s)
+                 : launch_blur_c<false, false>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s);
 }
 
 // Host helper: rows per CTA that fit the shared-memory budget, balanced over the bands.
-int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H) {
+int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair) {
   const int NC = T + 15, G = (T + 7) / 8;
   int best = racc;
   for (int RB = racc; RB <= 64; RB += racc) {
     const int RS = RB + 8 * G + 8;
-    if (blur_smem_layout(C, NC, RS, racc, np, nks).total <= 227 * 1024) best = RB;
+    if (blur_smem_layout(C, NC, RS, racc, np, nks, pair).total <= 227 * 1024) best = RB;
   }
   const int bands = (H + best - 1) / best;
   int rb = (H + bands - 1) / bands;

@@ -52,12 +52,14 @@ struct BlurGeom {
   int NC = 0;              // source chunks = T + 15
   int RB = 32;             // output rows per CTA
   int racc = 4;            // output rows per accumulator group (C * racc <= 4 accumulators)
+  bool pair = false;       // CTA pairs with tcgen05 cta_group::2 (M = 256)
   int RS = 0;              // source rows held in smem
   int nks = 0;             // number of K-steps
   int np = 0;              // padded N (= MlpGeom.n3)
   uint32_t* koff = nullptr;  // device [nks]: byte offset of group a relative to (src + yl*16)
   uint32_t* klbo = nullptr;  // device [nks]: LBO (group b - group a) in bytes
   uint8_t* bimg = nullptr;   // device [nks][np*32 bytes] B tiles (K-major, no swizzle)
+  uint8_t* bimg2 = nullptr;  // device [2 halves][nks][np*16 bytes] (pair mode)
   float* hsum = nullptr;     // device [np] per-basis tap sum (normalisation)
 };
 
@@ -93,6 +95,7 @@ struct p2s_plan_s {
   uint16_t* d_w = nullptr;      // bf16 [mb][n3][HWp] (k-major planes)
   int HWp = 0;                  // plane stride of d_w (H*W rounded up to 8)
   CUtensorMap tmap_w;           // 2-D TMA view of d_w: [mb*n3 rows][HWp], box 128 x n3
+  CUtensorMap tmap_b;           // 2-D TMA view of bg.bimg2: rows of 256 B, box 2 K-steps of one half
   float* d_img = nullptr;       // staging for the host entry point [mb][C][H][W]
   float* d_out = nullptr;       // staging for the host entry point [mb][C][H][W]
   // per-stage timing (p2s_plan_stage_timing)
@@ -119,7 +122,7 @@ int launch_warp_sim(const p2s_plan_s* p, int F, const float* img, int64_t stride
 int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s);
 int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0,
                 float* out, cudaStream_t s);
-int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H);
+int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair);
 int launch_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int64_t n, uint32_t* out,
                        cudaStream_t s);
 }  // namespace p2s
