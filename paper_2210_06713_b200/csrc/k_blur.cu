@@ -28,7 +28,7 @@
 
 namespace p2s {
 
-constexpr int kBlurStages = 4;
+constexpr int kMaxStages = 12;
 constexpr int kStepsPerStage = 2;  // K-steps (B tiles) moved per ring stage
 constexpr int kBlurThreads = 192;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue
 constexpr int kAccStride = 128;    // TMEM columns per accumulator
@@ -40,7 +40,7 @@ struct BlurArgs {
   const uint32_t* koff;     // [nks]
   const uint32_t* klbo;     // [nks]
   const float* hsum;        // [np]
-  int H, W, T, c, NC, RB, RS, nks, np;
+  int H, W, T, c, NC, RB, RS, nks, np, stages;
   uint32_t k0, k1;
   int64_t frame0;
   float sigma;
@@ -64,7 +64,8 @@ struct BlurSmem {
   uint32_t off_w, off_ring, off_desc, off_hsum, off_bar, total;
 };
 
-__host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int racc, int np, int nks, bool pair) {
+__host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int racc, int np, int nks, bool pair,
+                                                     int stages) {
   BlurSmem L;
   L.tile_bytes = ((uint32_t)NC * RS * 16 + 127) & ~127u;
   L.w_bytes = (uint32_t)racc * np * 128 * 2;  // [racc][np][128 px] bf16
@@ -72,10 +73,10 @@ __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int 
   L.b_bytes = (uint32_t)np * 32 / (pair ? 2 : 1);  // per K-step: this CTA's rows of B
   L.off_w = C * L.tile_bytes;
   L.off_ring = (L.off_w + L.w_bytes + 127) & ~127u;
-  L.off_desc = L.off_ring + kBlurStages * kStepsPerStage * L.b_bytes;
+  L.off_desc = L.off_ring + stages * kStepsPerStage * L.b_bytes;
   L.off_hsum = L.off_desc + 8 * nks;
   L.off_bar = (L.off_hsum + 4 * np + 15) & ~15u;
-  L.total = L.off_bar + (2 * kBlurStages + 4) * 8 + 16;
+  L.total = L.off_bar + (2 * stages + 4) * 8 + 16;
   return L;
 }
 
@@ -84,7 +85,8 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     k_blur(const BlurArgs a, const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_b) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const BlurSmem L = blur_smem_layout(C, a.NC, a.RS, RACC, a.np, a.nks, PAIR);
+  const BlurSmem L = blur_smem_layout(C, a.NC, a.RS, RACC, a.np, a.nks, PAIR, a.stages);
+  const int kBlurStages = a.stages;
   const uint32_t sbo_src = (uint32_t)a.RS * 16;
   uint8_t* wbuf = smem + L.off_w;
   uint8_t* ring = smem + L.off_ring;
@@ -428,7 +430,8 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.normalize = p->normalize;
   a.clamp01 = p->clamp01;
   const bool pair = g.pair;
-  const BlurSmem L = blur_smem_layout(p->C, a.NC, a.RS, g.racc, a.np, a.nks, pair);
+  a.stages = g.stages;
+  const BlurSmem L = blur_smem_layout(p->C, a.NC, a.RS, g.racc, a.np, a.nks, pair, g.stages);
   // TMEM: this kernel owns all 512 columns of its SM; keep shared memory above half the SM
   // so that two CTAs never co-reside and contend for tcgen05.alloc.
   size_t sm = L.total < 116 * 1024 ? 116 * 1024 : L.total;
@@ -443,12 +446,12 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
 }
 
 // Host helper: rows per CTA that fit the shared-memory budget, balanced over the bands.
-int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair) {
+int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair, int stages) {
   const int NC = T + 15, G = (T + 7) / 8;
   int best = racc;
   for (int RB = racc; RB <= 64; RB += racc) {
     const int RS = RB + 8 * G + 8;
-    if (blur_smem_layout(C, NC, RS, racc, np, nks, pair).total <= 227 * 1024) best = RB;
+    if (blur_smem_layout(C, NC, RS, racc, np, nks, pair, stages).total <= 227 * 1024) best = RB;
   }
   const int bands = (H + best - 1) / best;
   int rb = (H + bands - 1) / bands;

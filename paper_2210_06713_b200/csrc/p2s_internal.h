@@ -53,6 +53,7 @@ struct BlurGeom {
   int RB = 32;             // output rows per CTA
   int racc = 4;            // output rows per accumulator group (C * racc <= 4 accumulators)
   bool pair = false;       // CTA pairs with tcgen05 cta_group::2 (M = 256)
+  int stages = 8;          // B ring depth (stages of 2 K-steps)
   int RS = 0;              // source rows held in smem
   int nks = 0;             // number of K-steps
   int np = 0;              // padded N (= MlpGeom.n3)
@@ -122,7 +123,7 @@ int launch_warp_sim(const p2s_plan_s* p, int F, const float* img, int64_t stride
 int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s);
 int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0,
                 float* out, cudaStream_t s);
-int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair);
+int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair, int stages);
 int launch_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int64_t n, uint32_t* out,
                        cudaStream_t s);
 }  // namespace p2s

@@ -11,6 +11,12 @@ for step in "$@"; do
            echo "smoke exit $?" >> gpurun_out/smoke.log ;;
     bench) timeout -s KILL 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err;
            echo "bench exit $?" >> gpurun_out/bench.err ;;
+    sweep:*)  # sweep:VAR=a,b,c -> short bench per value (blur-focused tuning)
+      kv="${step#sweep:}"; var="${kv%%=*}"; vals="${kv#*=}"
+      for v in ${vals//,/ }; do
+        env "$var=$v" timeout -s KILL 600 python bench.py --steps 5 --warmup 2 --no-cpu-baseline --no-e2e \
+          > "gpurun_out/sweep_${var}_${v}.json" 2>&1
+      done ;;
     bench_ref) timeout -s KILL 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1 ;;
     ncu_launches)
       timeout -s KILL 300 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/b_small.log 2>&1 &&
