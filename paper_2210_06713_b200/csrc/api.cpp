@@ -133,7 +133,7 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   // B ring: enough stages to cover ~2 us of L2 latency at the MMA rate (a stage is
   // 2 K-steps x C*racc MMAs); pair mode halves the bytes per stage.
   const char* se = getenv("P2S_BLUR_STAGES");
-  g.stages = se ? std::max(2, std::min(12, atoi(se))) : (g.pair ? 8 : 6);
+  g.stages = se ? std::max(2, std::min(12, atoi(se))) : 4;
   g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, g.nks, p->H, g.pair, g.stages);
   g.RS = g.RB + 8 * G + 8;
   const uint32_t sbo = (uint32_t)g.RS * 16;
