@@ -26,6 +26,9 @@
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace p2s {
 
 constexpr int kMaxStages = 12;
@@ -45,7 +48,14 @@ struct BlurArgs {
   int64_t frame0;
   float sigma;
   int normalize, clamp01;
+  unsigned long long* probe;  // optional [8] cycle counters (P2S_BLUR_PROBE), else null
 };
+
+__device__ __forceinline__ uint64_t clk() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int reflect_idx(int i, int n) {
   if (i < 0) i = -i;
@@ -106,6 +116,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   const int x0 = blockIdx.x * 128, y0 = blockIdx.y * a.RB, f = blockIdx.z;
   const int HW = a.H * a.W;
   const uint32_t s_tile = smem_u32(smem);
+  const uint64_t t_start = clk();
 
   // A descriptor of every K-step for (channel 0, row 0): start = tile + koff, LBO, SBO
   for (int i = tid; i < a.nks; i += kBlurThreads)
@@ -184,6 +195,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   if (PAIR) cluster_sync_all();  // both source tiles and all barrier inits visible to the pair
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  if (a.probe && tid == 0) atomicAdd(&a.probe[0], (unsigned long long)(clk() - t_start));
 
   const int n_rg = (a.RB + RACC - 1) / RACC;
   const int nst = (a.nks + kStepsPerStage - 1) / kStepsPerStage;
@@ -247,12 +259,18 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     const uint32_t idesc = umma_idesc_bf16(PAIR ? 256 : 128, a.np, true, false);
     uint32_t stage = 0, phase = 0;
     const uint64_t ch_step = (uint64_t)(L.tile_bytes >> 4);
+    uint64_t w_full = 0, w_tempty = 0;
+    const uint64_t t_mma0 = clk();
     for (int rg = 0; rg < n_rg; ++rg) {
+      uint64_t t0c = clk();
       mbar_wait(tempty, (rg & 1) ^ 1);
+      w_tempty += clk() - t0c;
       tc_fence_after();
       const uint64_t row_off = (uint64_t)(rg * RACC);  // start address += rg*RACC*16 bytes
       for (int st = 0; st < nst; ++st) {
+        uint64_t t1c = clk();
         mbar_wait(&full[stage], phase);
+        w_full += clk() - t1c;
         tc_fence_after();
         const uint64_t bdesc0 = umma_desc(smem_u32(ring + stage * kStepsPerStage * bbytes), 128, 256);
         const int t0 = st * kStepsPerStage;
@@ -294,6 +312,11 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       }
       __syncwarp();
     }
+    if (a.probe && lane == 0) {
+      atomicAdd(&a.probe[1], (unsigned long long)w_full);
+      atomicAdd(&a.probe[2], (unsigned long long)w_tempty);
+      atomicAdd(&a.probe[3], (unsigned long long)(clk() - t_mma0));
+    }
   } else if (warp >= 2) {
     // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
     const int qd = warp & 3;
@@ -303,10 +326,14 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
     const uint16_t* wq = reinterpret_cast<const uint16_t*>(wbuf) + q;
     const uint32_t t_tempty_leader = PAIR ? mapa_shared(tempty, 0) : 0u;
+    uint64_t e_wait = 0, e_work = 0;
     for (int rg = 0; rg < n_rg; ++rg) {
+      uint64_t t0c = clk();
       mbar_wait(tfull, rg & 1);
       mbar_wait(wfull, rg & 1);
       tc_fence_after();
+      uint64_t t1c = clk();
+      e_wait += t1c - t0c;
 #pragma unroll
       for (int r = 0; r < RACC; ++r) {
         const int y = y0 + rg * RACC + r;
@@ -351,6 +378,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
+      e_work += clk() - t1c;
       if (lane == 0) {
         mbar_arrive(wempty);
         if (PAIR)
@@ -359,9 +387,17 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
           mbar_arrive(tempty);
       }
     }
+    if (a.probe && warp == 2 && lane == 0) {
+      atomicAdd(&a.probe[4], (unsigned long long)e_wait);
+      atomicAdd(&a.probe[5], (unsigned long long)e_work);
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (a.probe && tid == 0) {
+    atomicAdd(&a.probe[6], (unsigned long long)(clk() - t_start));
+    atomicAdd(&a.probe[7], 1ull);
+  }
   if (PAIR) cluster_sync_all();  // the pair's MMAs and remote arrivals are all done
   tc_fence_after();
   if (warp == 0) {
@@ -429,6 +465,14 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.sigma = p->noise_sigma;
   a.normalize = p->normalize;
   a.clamp01 = p->clamp01;
+  a.probe = nullptr;
+  static unsigned long long* probe = nullptr;
+  const bool want_probe = getenv("P2S_BLUR_PROBE") != nullptr;
+  if (want_probe) {
+    if (!probe) cudaMalloc(&probe, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(probe, 0, 8 * sizeof(unsigned long long), s);
+    a.probe = probe;
+  }
   const bool pair = g.pair;
   a.stages = g.stages;
   const BlurSmem L = blur_smem_layout(p->C, a.NC, a.RS, g.racc, a.np, a.nks, pair, g.stages);
@@ -438,11 +482,24 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   int gx = (p->W + 127) / 128;
   if (pair) gx = (gx + 1) / 2 * 2;  // whole CTA pairs; a trailing dummy CTA stores nothing
   dim3 grid(gx, (p->H + g.RB - 1) / g.RB, F);
+  int rc;
   if (pair)
-    return src_f32 ? launch_blur_c<true, true>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s)
-                   : launch_blur_c<false, true>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s);
-  return src_f32 ? launch_blur_c<true, false>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s)
+    rc = src_f32 ? launch_blur_c<true, true>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s)
+                 : launch_blur_c<false, true>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s);
+  else
+    rc = src_f32 ? launch_blur_c<true, false>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s)
                  : launch_blur_c<false, false>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s);
+  if (want_probe) {  // debug: per-CTA averages of the phase cycle counters
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, probe, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const double n = h[7] ? (double)h[7] : 1.0, nm = pair ? n / 2 : n;
+    fprintf(stderr,
+            "[blur probe] CTAs %llu  per CTA cycles: total %.0f prologue %.0f | MMA warp: loop %.0f wait_full %.0f "
+            "wait_tmem %.0f | epilogue warp: wait %.0f work %.0f\n",
+            h[7], h[6] / n, h[0] / n, h[3] / nm, h[1] / nm, h[2] / nm, h[4] / n, h[5] / n);
+  }
+  return rc;
 }
 
 // Host helper: rows per CTA that fit the shared-memory budget, balanced over the bands.
