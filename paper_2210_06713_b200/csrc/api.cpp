@@ -133,28 +133,39 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   // B ring: enough stages to cover ~2 us of L2 latency at the MMA rate (a stage is
   // 2 K-steps x C*racc MMAs); pair mode halves the bytes per stage.
   const char* se = getenv("P2S_BLUR_STAGES");
-  g.stages = se ? std::max(2, std::min(12, atoi(se))) : 4;
+  g.stages = se ? std::max(2, std::min(12, atoi(se))) : (g.pair ? 8 : 4);
   g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, g.nks, p->H, g.pair, g.stages);
-  g.RS = g.RB + 8 * G + 8;
+  g.RS = g.RB + 8 * G;
   const uint32_t sbo = (uint32_t)g.RS * 16;
   struct Grp { int tx, gi; uint32_t off; };
   std::vector<Grp> groups;
   for (int tx = T - 1; tx >= 0; --tx)
     for (int gi = 0; gi < G; ++gi) groups.push_back({tx, gi, (uint32_t)(2 * g.c - tx) * sbo + 128u * gi});
+  // K-steps: the lowest-address group alone (its partner slot points at the next group with
+  // zero B rows), then consecutive pairs; every A row touched is < yl + 8G, so a tile needs
+  // only RS = RB + 8G source rows.
   g.nks = (int)(groups.size() + 1) / 2;
   const size_t bbytes = (size_t)g.np * 32;
   std::vector<uint8_t> img((size_t)g.nks * bbytes, 0);
   std::vector<uint32_t> koff(g.nks), klbo(g.nks);
+  const bool odd = groups.size() % 2 == 1;
   for (int t = 0; t < g.nks; ++t) {
-    const Grp& ga = groups[2 * t];
-    const bool has_b = (size_t)(2 * t + 1) < groups.size();
+    int ia, ib;
+    if (odd) {
+      ia = t == 0 ? 0 : 2 * t - 1;
+      ib = t == 0 ? -1 : 2 * t;
+    } else {
+      ia = 2 * t;
+      ib = 2 * t + 1;
+    }
+    const Grp& ga = groups[ia];
     koff[t] = ga.off;
-    klbo[t] = has_b ? groups[2 * t + 1].off - ga.off : 128u;
+    klbo[t] = (ib >= 0 ? groups[ib].off : groups[ia + 1].off) - ga.off;
     uint8_t* dst = img.data() + (size_t)t * bbytes;
     for (int k = 0; k < 16; ++k) {
       const bool second = k >= 8;
-      if (second && !has_b) continue;
-      const Grp& gr = second ? groups[2 * t + 1] : ga;
+      if (second && ib < 0) continue;  // dummy half: zero B rows
+      const Grp& gr = second ? groups[ib] : ga;
       const int ty = 2 * g.c - 8 * gr.gi - (k & 7);
       if (ty < 0 || ty >= T) continue;
       for (int n = 0; n < K; ++n) {

@@ -344,6 +344,9 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
         for (int ch = 0; ch < C; ++ch) acc[ch] = 0.f;
         float g = 0.f;
         for (int cb = 0; cb < a.np / 16; ++cb) {
+          uint32_t v[C][16];
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch) tmem_ld16_issue(tl + (ch * RACC + r) * kAccStride + cb * 16, v[ch]);
           float wf[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) wf[i] = bf16_to_f(wr[(cb * 16 + i) * 128]);
@@ -351,13 +354,11 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) g = fmaf(wf[i], s_hsum[cb * 16 + i], g);
           }
+          tmem_wait_ld();
 #pragma unroll
-          for (int ch = 0; ch < C; ++ch) {
-            float v[16];
-            tmem_ld16(tl + (ch * RACC + r) * kAccStride + cb * 16, v);
+          for (int ch = 0; ch < C; ++ch)
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[ch] = fmaf(wf[i], v[i], acc[ch]);
-          }
+            for (int i = 0; i < 16; ++i) acc[ch] = fmaf(wf[i], __uint_as_float(v[ch][i]), acc[ch]);
         }
         if (valid) {
 #pragma unroll
@@ -507,7 +508,7 @@ int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair,
   const int NC = T + 15, G = (T + 7) / 8;
   int best = racc;
   for (int RB = racc; RB <= 64; RB += racc) {
-    const int RS = RB + 8 * G + 8;
+    const int RS = RB + 8 * G;
     if (blur_smem_layout(C, NC, RS, racc, np, nks, pair, stages).total <= 227 * 1024) best = RB;
   }
   const int bands = (H + best - 1) / best;
