@@ -33,7 +33,8 @@ namespace p2s {
 
 constexpr int kMaxStages = 12;
 constexpr int kStepsPerStage = 2;  // K-steps (B tiles) moved per ring stage
-constexpr int kBlurThreads = 192;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue
+constexpr int kBlurThreads = 320;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue
+constexpr int kEpiWarps = 8;       // two warps per TMEM lane quarter, each summing half the bases
 constexpr int kAccStride = 128;    // TMEM columns per accumulator
 
 struct BlurArgs {
@@ -71,7 +72,7 @@ __device__ __forceinline__ float load_src(const void* src, size_t idx) {
 
 struct BlurSmem {
   uint32_t tile_bytes, w_bytes, b_bytes;
-  uint32_t off_w, off_ring, off_desc, off_hsum, off_bar, total;
+  uint32_t off_w, off_ring, off_desc, off_hsum, off_part, off_bar, total;
 };
 
 __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int racc, int np, int nks, bool pair,
@@ -79,13 +80,15 @@ __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int 
   BlurSmem L;
   L.tile_bytes = ((uint32_t)NC * RS * 16 + 127) & ~127u;
   L.w_bytes = (uint32_t)racc * np * 128 * 2;  // [racc][np][128 px] bf16
-  if (L.w_bytes < 6u * 4 * 192 * 4) L.w_bytes = 6u * 4 * 192 * 4;  // doubles as the loader staging rows
+  const uint32_t stg_bytes = (kBlurThreads / 32) * 4u * 192 * 4;   // the loader's staging rows
+  if (L.w_bytes < stg_bytes) L.w_bytes = stg_bytes;
   L.b_bytes = (uint32_t)np * 32 / (pair ? 2 : 1);  // per K-step: this CTA's rows of B
   L.off_w = C * L.tile_bytes;
   L.off_ring = (L.off_w + L.w_bytes + 127) & ~127u;
   L.off_desc = L.off_ring + stages * kStepsPerStage * L.b_bytes;
   L.off_hsum = L.off_desc + 8 * nks;
-  L.off_bar = (L.off_hsum + 4 * np + 15) & ~15u;
+  L.off_part = (L.off_hsum + 4 * np + 15) & ~15u;  // [2][racc][128][C+1] epilogue partial sums
+  L.off_bar = L.off_part + 2u * racc * 128 * (C + 1) * 4;
   L.total = L.off_bar + (2 * stages + 4) * 8 + 16;
   return L;
 }
@@ -106,9 +109,9 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   uint64_t* full = bars;
   uint64_t* empty = bars + kBlurStages;
   uint64_t* tfull = bars + 2 * kBlurStages;
-  uint64_t* tempty = tfull + 1;  // TMEM free (on the MMA-issuing CTA; 4 or 8 warp arrivals)
+  uint64_t* tempty = tfull + 1;  // TMEM free (on the MMA-issuing CTA; one arrival per epilogue warp)
   uint64_t* wfull = tfull + 2;
-  uint64_t* wempty = tfull + 3;  // this CTA's w buffer free (4 warp arrivals)
+  uint64_t* wempty = tfull + 3;  // this CTA's w buffer free (kEpiWarps arrivals)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(wempty + 1);
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
@@ -128,9 +131,9 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, PAIR ? 8 : 4);
+    mbar_init(tempty, PAIR ? 2 * kEpiWarps : kEpiWarps);
     mbar_init(wfull, 1);
-    mbar_init(wempty, 4);
+    mbar_init(wempty, kEpiWarps);
     mbar_fence_init();
   }
   if (warp == 0) {
@@ -318,14 +321,20 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       atomicAdd(&a.probe[3], (unsigned long long)(clk() - t_mma0));
     }
   } else if (warp >= 2) {
-    // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
+    // ---- epilogue warps 2..9: TMEM lane quarter = warp % 4; half h of the basis chunks.
+    // h = 1 leaves its partial sums in smem (double-buffered by group parity); h = 0 adds
+    // them, applies step 5 and stores.
     const int qd = warp & 3;
+    const int h = (warp - 2) >> 2;
     const int m = qd * 32 + lane;
     const int q = 16 * (m & 7) + (m >> 3);
     const int x = x0 + q;
     const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
     const uint16_t* wq = reinterpret_cast<const uint16_t*>(wbuf) + q;
     const uint32_t t_tempty_leader = PAIR ? mapa_shared(tempty, 0) : 0u;
+    float* part = reinterpret_cast<float*>(smem + L.off_part);
+    const int nch = a.np / 16, half = (nch + 1) / 2;
+    const int cb0 = h ? half : 0, cb1 = h ? nch : half;
     uint64_t e_wait = 0, e_work = 0;
     for (int rg = 0; rg < n_rg; ++rg) {
       uint64_t t0c = clk();
@@ -334,16 +343,13 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       tc_fence_after();
       uint64_t t1c = clk();
       e_wait += t1c - t0c;
+      float accs[RACC][C + 1];
 #pragma unroll
       for (int r = 0; r < RACC; ++r) {
-        const int y = y0 + rg * RACC + r;
-        const bool valid = (y < a.H) && (x < a.W);
         const uint16_t* wr = wq + (size_t)r * a.np * 128;
-        float acc[C];
 #pragma unroll
-        for (int ch = 0; ch < C; ++ch) acc[ch] = 0.f;
-        float g = 0.f;
-        for (int cb = 0; cb < a.np / 16; ++cb) {
+        for (int ch = 0; ch <= C; ++ch) accs[r][ch] = 0.f;
+        for (int cb = cb0; cb < cb1; ++cb) {
           uint32_t v[C][16];
 #pragma unroll
           for (int ch = 0; ch < C; ++ch) tmem_ld16_issue(tl + (ch * RACC + r) * kAccStride + cb * 16, v[ch]);
@@ -352,41 +358,62 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
           for (int i = 0; i < 16; ++i) wf[i] = bf16_to_f(wr[(cb * 16 + i) * 128]);
           if (a.normalize) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) g = fmaf(wf[i], s_hsum[cb * 16 + i], g);
+            for (int i = 0; i < 16; ++i) accs[r][C] = fmaf(wf[i], s_hsum[cb * 16 + i], accs[r][C]);
           }
           tmem_wait_ld();
 #pragma unroll
           for (int ch = 0; ch < C; ++ch)
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[ch] = fmaf(wf[i], __uint_as_float(v[ch][i]), acc[ch]);
+            for (int i = 0; i < 16; ++i) accs[r][ch] = fmaf(wf[i], __uint_as_float(v[ch][i]), accs[r][ch]);
         }
-        if (valid) {
+      }
+      // TMEM and w of this group are consumed by this warp.  h = 0 releases them only after
+      // its barrier wait, so h = 1 cannot reach the next group's barrier arrive first.
+      auto release = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(wempty);
+          if (PAIR)
+            mbar_arrive_cluster(t_tempty_leader);
+          else
+            mbar_arrive(tempty);
+        }
+      };
+      float* pb = part + (size_t)(rg & 1) * RACC * 128 * (C + 1);
+      if (h == 1) {
+        release();
 #pragma unroll
-          for (int ch = 0; ch < C; ++ch) {
-            float o = acc[ch];
-            if (a.normalize) o = o / g;
-            if (a.sigma != 0.f) {
-              const int64_t fr = a.frame0 + f;
-              uint4 rx = philox4x32_10(make_uint4((uint32_t)(y * a.W + x), (uint32_t)ch | (1u << 16), (uint32_t)fr,
-                                                  (uint32_t)((uint64_t)fr >> 32)),
-                                       a.k0, a.k1);
-              o += a.sigma * box_muller(rx.x, rx.y).x;
+        for (int r = 0; r < RACC; ++r)
+#pragma unroll
+          for (int ch = 0; ch <= C; ++ch) pb[((size_t)r * (C + 1) + ch) * 128 + m] = accs[r][ch];
+        asm volatile("bar.arrive 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      } else {
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        release();
+#pragma unroll
+        for (int r = 0; r < RACC; ++r) {
+          const int y = y0 + rg * RACC + r;
+          if (y < a.H && x < a.W) {
+            const float g = accs[r][C] + pb[((size_t)r * (C + 1) + C) * 128 + m];
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch) {
+              float o = accs[r][ch] + pb[((size_t)r * (C + 1) + ch) * 128 + m];
+              if (a.normalize) o = o / g;
+              if (a.sigma != 0.f) {
+                const int64_t fr = a.frame0 + f;
+                uint4 rx = philox4x32_10(make_uint4((uint32_t)(y * a.W + x), (uint32_t)ch | (1u << 16), (uint32_t)fr,
+                                                    (uint32_t)((uint64_t)fr >> 32)),
+                                         a.k0, a.k1);
+                o += a.sigma * box_muller(rx.x, rx.y).x;
+              }
+              if (a.clamp01) o = fminf(fmaxf(o, 0.f), 1.f);
+              a.out[((size_t)f * C + ch) * HW + (size_t)y * a.W + x] = o;
             }
-            if (a.clamp01) o = fminf(fmaxf(o, 0.f), 1.f);
-            a.out[((size_t)f * C + ch) * HW + (size_t)y * a.W + x] = o;
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
       e_work += clk() - t1c;
-      if (lane == 0) {
-        mbar_arrive(wempty);
-        if (PAIR)
-          mbar_arrive_cluster(t_tempty_leader);
-        else
-          mbar_arrive(tempty);
-      }
     }
     if (a.probe && warp == 2 && lane == 0) {
       atomicAdd(&a.probe[4], (unsigned long long)e_wait);
