@@ -102,15 +102,40 @@ static p2s_status build_mlp_blob(const std::vector<double>& W1, int nin, int h1,
   g.off_b3 = g.off_b2 + (size_t)g.n2 * 4;
   g.blob_bytes = (g.off_b3 + (size_t)g.n3 * 4 + 15) / 16 * 16;
   std::vector<uint8_t> blob(g.blob_bytes, 0);
-  kmajor_image(W1, h1, nin, g.n1, g.k1, blob.data());
-  kmajor_image(W2, h2, h1, g.n2, g.n1, blob.data() + g.off_w2);
-  kmajor_image(W3, K, h2, g.n3, g.n2, blob.data() + g.off_w3);
-  float* fb1 = reinterpret_cast<float*>(blob.data() + g.off_b1);
-  float* fb2 = reinterpret_cast<float*>(blob.data() + g.off_b2);
-  float* fb3 = reinterpret_cast<float*>(blob.data() + g.off_b3);
-  for (int i = 0; i < h1; ++i) fb1[i] = (float)b1[i];
-  for (int i = 0; i < h2; ++i) fb2[i] = (float)b2[i];
-  for (int i = 0; i < K; ++i) fb3[i] = (float)b3[i];
+  // Bias folding: when every layer has a padding column, a constant-1 input (A1 column nin,
+  // set once in smem) is carried through the network in the first padding unit of each
+  // hidden layer, and the biases become GEMM weights of that unit (bf16).
+  g.bias_folded = (g.k1 > nin) && (g.n1 > h1) && (g.n2 > h2);
+  if (g.bias_folded) {
+    std::vector<double> A1((size_t)g.n1 * g.k1, 0.0), A2((size_t)g.n2 * g.n1, 0.0), A3((size_t)g.n3 * g.n2, 0.0);
+    for (int n = 0; n < h1; ++n) {
+      for (int k = 0; k < nin; ++k) A1[(size_t)n * g.k1 + k] = W1[(size_t)n * nin + k];
+      A1[(size_t)n * g.k1 + nin] = b1[n];
+    }
+    A1[(size_t)h1 * g.k1 + nin] = 1.0;
+    for (int n = 0; n < h2; ++n) {
+      for (int k = 0; k < h1; ++k) A2[(size_t)n * g.n1 + k] = W2[(size_t)n * h1 + k];
+      A2[(size_t)n * g.n1 + h1] = b2[n];
+    }
+    A2[(size_t)h2 * g.n1 + h1] = 1.0;
+    for (int n = 0; n < K; ++n) {
+      for (int k = 0; k < h2; ++k) A3[(size_t)n * g.n2 + k] = W3[(size_t)n * h2 + k];
+      A3[(size_t)n * g.n2 + h2] = b3[n];
+    }
+    kmajor_image(A1, g.n1, g.k1, g.n1, g.k1, blob.data());
+    kmajor_image(A2, g.n2, g.n1, g.n2, g.n1, blob.data() + g.off_w2);
+    kmajor_image(A3, g.n3, g.n2, g.n3, g.n2, blob.data() + g.off_w3);
+  } else {
+    kmajor_image(W1, h1, nin, g.n1, g.k1, blob.data());
+    kmajor_image(W2, h2, h1, g.n2, g.n1, blob.data() + g.off_w2);
+    kmajor_image(W3, K, h2, g.n3, g.n2, blob.data() + g.off_w3);
+    float* fb1 = reinterpret_cast<float*>(blob.data() + g.off_b1);
+    float* fb2 = reinterpret_cast<float*>(blob.data() + g.off_b2);
+    float* fb3 = reinterpret_cast<float*>(blob.data() + g.off_b3);
+    for (int i = 0; i < h1; ++i) fb1[i] = (float)b1[i];
+    for (int i = 0; i < h2; ++i) fb2[i] = (float)b2[i];
+    for (int i = 0; i < K; ++i) fb3[i] = (float)b3[i];
+  }
   P2S_CUDA(cudaMalloc(dblob, g.blob_bytes), "cudaMalloc mlp blob");
   P2S_CUDA(cudaMemcpy(*dblob, blob.data(), g.blob_bytes, cudaMemcpyHostToDevice), "copy mlp blob");
   return P2S_OK;

@@ -33,12 +33,14 @@ struct MlpArgs {
   int nin, k1, n1, n2, n3;
   uint32_t off_w2, off_w3, off_b1, off_b2, off_b3, blob_bytes;
   int HW, HWp, F, tiles_per_frame;
+  int bias_folded;  // A1 column nin is the constant 1; biases live in the weight images
 };
 
 // Epilogue of a hidden layer: TMEM columns [0, ncols) of this thread's row -> +bias -> ReLU
 // -> bf16 -> the next layer's K-major A operand (row m of a [128 x ncols] SWIZZLE_NONE
 // image, core matrices of 8 rows x 16 B, k-chunks at 128 B, 8-row groups at sbo).
 // TMEM loads are issued 32 columns at a time before one wait.
+template <bool BIAS>
 __device__ __forceinline__ void mlp_hidden_epilogue(uint32_t taddr, int ncols, const float* bias, uint8_t* a_smem,
                                                     uint32_t sbo, int m) {
   uint8_t* rowbase = a_smem + (m & 7) * 16 + (m >> 3) * sbo;
@@ -54,8 +56,13 @@ __device__ __forceinline__ void mlp_hidden_epilogue(uint32_t taddr, int ncols, c
       uint32_t pk[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float x0 = fmaxf(__uint_as_float(r[16 * h + 2 * i]) + bias[c0 + 16 * h + 2 * i], 0.f);
-        const float x1 = fmaxf(__uint_as_float(r[16 * h + 2 * i + 1]) + bias[c0 + 16 * h + 2 * i + 1], 0.f);
+        float x0 = __uint_as_float(r[16 * h + 2 * i]), x1 = __uint_as_float(r[16 * h + 2 * i + 1]);
+        if (BIAS) {
+          x0 += bias[c0 + 16 * h + 2 * i];
+          x1 += bias[c0 + 16 * h + 2 * i + 1];
+        }
+        x0 = fmaxf(x0, 0.f);
+        x1 = fmaxf(x1, 0.f);
         pk[i] = pack_bf16x2(x0, x1);
       }
       uint8_t* base = rowbase + ((c0 + 16 * h) / 8) * 128;
@@ -128,7 +135,9 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     for (int idx = tid; idx < nwg * per; idx += blockDim.x) {
       const int b = idx / per, r = idx % per;
       const int k = a.nin + r % (a.k1 - a.nin), g = r / (a.k1 - a.nin);
-      *reinterpret_cast<uint4*>(sw + blob_al + b * wg_bytes + g * (a.k1 * 16) + k * 16) = make_uint4(0, 0, 0, 0);
+      // padding planes are zero; with folded biases plane nin is the constant 1 (bf16 0x3F80)
+      const uint32_t one = (a.bias_folded && k == a.nin) ? 0x3F803F80u : 0u;
+      *reinterpret_cast<uint4*>(sw + blob_al + b * wg_bytes + g * (a.k1 * 16) + k * 16) = make_uint4(one, one, one, one);
     }
   }
   if (tid == 0) {
@@ -193,7 +202,10 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
       }
       cp_async_commit();
     }
-    mlp_hidden_epilogue(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m);
+    if (a.bias_folded)
+      mlp_hidden_epilogue<false>(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m);
+    else
+      mlp_hidden_epilogue<true>(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m);
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
@@ -208,7 +220,10 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    mlp_hidden_epilogue(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m);
+    if (a.bias_folded)
+      mlp_hidden_epilogue<false>(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m);
+    else
+      mlp_hidden_epilogue<true>(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m);
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
@@ -223,20 +238,33 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    // w tile -> A2 as [n3][128 px] bf16, then one 2-D TMA store into the k-major planes
+    // w tile -> A2 as [n3][128 px] bf16, then one 2-D TMA store into the k-major planes.
+    // Lanes 2i and 2i+1 (adjacent pixels) swap halves of their 16-value chunk so each
+    // writes one 32-bit word (2 pixels) per basis row: 8 stores per chunk instead of 16.
     {
-      uint16_t* st = reinterpret_cast<uint16_t*>(A2) + m;
-      for (int c0 = 0; c0 < a.n3; c0 += 32) {
-        uint32_t r[32];
+      uint32_t* st = reinterpret_cast<uint32_t*>(A2) + (m >> 1);
+      const bool odd = lane & 1;
+      for (int c0 = 0; c0 < a.n3; c0 += 16) {
+        uint32_t r[16];
         tmem_ld16_issue(taddr + c0, r);
-        const bool two = c0 + 16 < a.n3;
-        if (two) tmem_ld16_issue(taddr + c0 + 16, r + 16);
         tmem_wait_ld();
+        uint32_t pk[8];  // pack (value i, value i+1) -> bf16x2 of this pixel
 #pragma unroll
-        for (int i = 0; i < 16; ++i) st[(c0 + i) * 128] = f_to_bf16(__uint_as_float(r[i]) + b3[c0 + i]);
-        if (two) {
+        for (int i = 0; i < 8; ++i) {
+          float v0 = __uint_as_float(r[2 * i]), v1 = __uint_as_float(r[2 * i + 1]);
+          if (!a.bias_folded) {
+            v0 += b3[c0 + 2 * i];
+            v1 += b3[c0 + 2 * i + 1];
+          }
+          pk[i] = pack_bf16x2(v0, v1);
+        }
+        // even lane keeps rows c0+2i (its low halves) and receives the neighbour's low halves;
+        // odd lane keeps rows c0+2i+1 (high halves) and receives the neighbour's high halves
 #pragma unroll
-          for (int i = 16; i < 32; ++i) st[(c0 + i) * 128] = f_to_bf16(__uint_as_float(r[i]) + b3[c0 + i]);
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t other = __shfl_xor_sync(0xffffffffu, pk[i], 1);
+          const uint32_t word = odd ? __byte_perm(other, pk[i], 0x7632) : __byte_perm(pk[i], other, 0x5410);
+          st[(c0 + 2 * i + (odd ? 1 : 0)) * 64] = word;
         }
       }
     }
@@ -271,6 +299,7 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   a.blob_bytes = (uint32_t)g.blob_bytes;
   a.HW = p->H * p->W;
   a.HWp = p->HWp;
+  a.bias_folded = g.bias_folded ? 1 : 0;
   a.F = F;
   a.tiles_per_frame = (a.HW + 127) / 128;
   const int nmax = std::max(std::max(g.n1, g.n2), g.n3);

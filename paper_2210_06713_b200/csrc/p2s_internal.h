@@ -42,6 +42,7 @@ struct MlpGeom {
   int k1 = 0;    // padded layer-1 K
   int n1 = 0, n2 = 0, n3 = 0;  // padded widths (n3 = padded K bases)
   int kout = 0;  // real K
+  bool bias_folded = false;  // biases carried by a constant-1 unit inside the GEMMs
   size_t blob_bytes = 0;  // W1img | W2img | W3img | b1 | b2 | b3
   size_t off_w2 = 0, off_w3 = 0, off_b1 = 0, off_b2 = 0, off_b3 = 0;
 };
