@@ -18,6 +18,8 @@
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
+#include <cstdlib>
+
 namespace p2s {
 
 // ------------------------------------------------------------------ small inverse DFTs
@@ -196,6 +198,31 @@ static void fill_fft_args(FFTArgs& a, const AxisFFT& ax) {
   a.tw = ax.tw;
 }
 
+// ------------------------------------------------------------------ register-resident N = 512
+// Fast path for 512-point axes (the bench grid): the same Stockham radix-8 passes as
+// smem_ifft (8 x 8 x 8, identical twiddles and butterflies), but each butterfly's eight
+// points stay in the registers of one thread (butterfly j holds x[j + 64 r]); the two
+// shared-memory exchanges between passes are the only data movement, all index arithmetic
+// is compile-time, and the last pass leaves the result in natural order (thread j holds
+// y[j + 64 r]), so it is stored straight from registers.
+constexpr int kRegN = 512, kRegB = 64;  // points, butterflies per pass
+
+template <int NS>
+__device__ __forceinline__ void reg_pass(float2 (&v)[8], int j, const float2* __restrict__ tw) {
+  if (NS > 1) {
+    const int step = (j & (NS - 1)) * (kRegN / (8 * NS));
+#pragma unroll
+    for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], tw[r * step]);
+  }
+  dft_inv<8>(v);
+}
+// Stockham output position of point r of butterfly j after the pass with span NS.
+template <int NS>
+__device__ __forceinline__ int reg_out(int j, int r) {
+  const int k = j & (NS - 1);
+  return (j - k) * 8 + k + r * NS;
+}
+
 // ------------------------------------------------------------------ K1: noise + PSD + row IDFT
 struct RowArgs {
   FFTArgs fq;
@@ -273,6 +300,87 @@ __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
   }
 }
 
+// White-noise rows at Q = 512: one CTA per (Hermitian row pair, mode pair); NG groups of
+// 64 threads, each group transforms one frame at a time (frames g, g + NG, ...).  Thread t
+// owns butterfly t of row ky and butterfly (64 - t) % 64 of row P - ky, which holds exactly
+// the mirror bins of its own: one Philox draw feeds both (the mirror takes the conjugate).
+template <int NG>
+__global__ void __launch_bounds__(64 * NG) k_rows_pair512(RowArgs a) {
+  constexpr int N = kRegN, B = kRegB, XL = N + N / 8;
+  extern __shared__ __align__(16) unsigned char smem[];
+  float2* tw = reinterpret_cast<float2*>(smem);  // [N]
+  float2* sS = tw + N;                           // [2][N] sqrt(S) of both rows
+  float2* xb = sS + 2 * N;                       // [NG][2][XL] exchange buffers
+  const int ky = blockIdx.x, p = blockIdx.y;
+  const int k1 = ky ? a.P - ky : 0;
+  const size_t plane = (size_t)p * a.P * N;
+  for (int i = threadIdx.x; i < N; i += 64 * NG) {
+    tw[i] = __ldg(&a.fq.tw[i]);
+    sS[i] = __ldg(&a.sqrtS[plane + (size_t)ky * N + i]);
+    sS[N + i] = __ldg(&a.sqrtS[plane + (size_t)k1 * N + i]);
+  }
+  __syncthreads();
+  const int g = threadIdx.x >> 6, t = threadIdx.x & (B - 1);
+  const int tm = (B - t) & (B - 1);
+  float2* x0 = xb + (size_t)g * 2 * XL;
+  float2* x1 = x0 + XL;
+  auto gsync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory"); };
+  auto xi = [](int i) { return i + (i >> 3); };  // exchange padding: conflict-free pass writes
+  for (int fi = g; fi < a.F; fi += NG) {
+    const int64_t fr = a.frame0 + fi;
+    float2 u[8], w[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int kx = t + B * r;
+      const float4 z = spectral_noise(ky, kx, a.P, N, p, fr, a.k0, a.k1);
+      u[r] = spectrum(sS[kx], z);
+      const float4 zc = make_float4(z.x, -z.y, z.z, -z.w);
+      // mirror bin (N - kx) % N = tm + 64 (7 - r) for t > 0, 64 ((8 - r) % 8) for t == 0
+      if (t)
+        w[7 - r] = spectrum(sS[N + tm + B * (7 - r)], zc);
+      else
+        w[(8 - r) & 7] = spectrum(sS[N + B * ((8 - r) & 7)], zc);
+    }
+    reg_pass<1>(u, t, tw);
+    reg_pass<1>(w, tm, tw);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      x0[xi(reg_out<1>(t, r))] = u[r];
+      x1[xi(reg_out<1>(tm, r))] = w[r];
+    }
+    gsync();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      u[r] = x0[xi(t + B * r)];
+      w[r] = x1[xi(tm + B * r)];
+    }
+    gsync();
+    reg_pass<8>(u, t, tw);
+    reg_pass<8>(w, tm, tw);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      x0[xi(reg_out<8>(t, r))] = u[r];
+      x1[xi(reg_out<8>(tm, r))] = w[r];
+    }
+    gsync();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      u[r] = x0[xi(t + B * r)];
+      w[r] = x1[xi(tm + B * r)];
+    }
+    gsync();
+    reg_pass<64>(u, t, tw);
+    reg_pass<64>(w, tm, tw);
+    float2* dst = a.Zout + (size_t)fi * a.npairs * a.P * N + plane;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) dst[(size_t)ky * N + t + B * r] = u[r];
+    if (k1 != ky) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) dst[(size_t)k1 * N + tm + B * r] = w[r];
+    }
+  }
+}
+
 // AR(1) path: one CTA per spectral row with the per-bin state in shared memory;
 // frames are evolved sequentially (including the replay of frames before frame0).
 template <int NT>
@@ -317,6 +425,15 @@ __global__ void __launch_bounds__(NT) k_rows_ar(RowArgs a) {
   for (int kx = threadIdx.x; kx < Q; kx += NT) a.ar[row + kx] = st[kx];
 }
 
+// The register fast path needs a 512-point axis planned as radix 8 x 8 x 8.
+static bool reg512(const AxisFFT& ax) {
+  return ax.N == kRegN && ax.nrad == 3 && ax.rad[0] == 8 && ax.rad[1] == 8 && ax.rad[2] == 8;
+}
+static int getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : 0;
+}
+
 int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool ar, int ar_mode,
                 int64_t replay_from, cudaStream_t s) {
   RowArgs a;
@@ -345,6 +462,12 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
       cudaFuncSetAttribute(k_rows_ar<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       k_rows_ar<128><<<grid, 128, sm, s>>>(a);
     }
+  } else if (reg512(pl->fq) && getenv_flag("P2S_FFT_GENERIC") == 0) {
+    constexpr int NG = 4;
+    dim3 grid(pl->P / 2 + 1, pl->npairs);
+    size_t sm = ((size_t)3 * kRegN + (size_t)NG * 2 * (kRegN + kRegN / 8)) * sizeof(float2);
+    cudaFuncSetAttribute(k_rows_pair512<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_rows_pair512<NG><<<grid, 64 * NG, sm, s>>>(a);
   } else {
     dim3 grid(pl->P / 2 + 1, pl->npairs);
     size_t sm = ((size_t)3 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
@@ -426,6 +549,87 @@ __global__ void __launch_bounds__(NT) k_cols(ColArgs a) {
   }
 }
 
+// Column IDFT at P = 512: 16 interleaved columns per CTA, 512 threads; thread (c, jj) owns
+// butterflies jj and jj + 32 of column c (16 independent 8-byte loads in flight per thread,
+// 128-byte row segments per half-warp).  Exchange buffer column-interleaved (x[i*16 + c]):
+// every half-warp access is 128 contiguous bytes.
+template <int MODE>
+__global__ void __launch_bounds__(512) k_cols512(ColArgs a) {
+  constexpr int N = kRegN, B = kRegB, TC = 16;
+  extern __shared__ __align__(16) unsigned char smem[];
+  float2* tw = reinterpret_cast<float2*>(smem);  // [N]
+  float2* xb = tw + N;                           // [N][TC]
+  for (int i = threadIdx.x; i < N; i += 512) tw[i] = __ldg(&a.fp.tw[i]);
+  const int c = threadIdx.x & (TC - 1), jj = threadIdx.x >> 4;
+  const int x0 = blockIdx.x * TC, p = blockIdx.y, f = blockIdx.z;
+  const int x = x0 + c;
+  const float2* src = a.Zin + ((size_t)f * a.npairs + p) * (size_t)N * a.Q + x;
+  float2 u[8], w[8];
+  const bool xin = x < a.Q;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    u[r] = xin ? __ldg(src + (size_t)(jj + B * r) * a.Q) : make_float2(0.f, 0.f);
+    w[r] = xin ? __ldg(src + (size_t)(jj + 32 + B * r) * a.Q) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();  // twiddles staged
+  const int j0 = jj, j1 = jj + 32;
+  reg_pass<1>(u, j0, tw);
+  reg_pass<1>(w, j1, tw);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    xb[reg_out<1>(j0, r) * TC + c] = u[r];
+    xb[reg_out<1>(j1, r) * TC + c] = w[r];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    u[r] = xb[(j0 + B * r) * TC + c];
+    w[r] = xb[(j1 + B * r) * TC + c];
+  }
+  __syncthreads();
+  reg_pass<8>(u, j0, tw);
+  reg_pass<8>(w, j1, tw);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    xb[reg_out<8>(j0, r) * TC + c] = u[r];
+    xb[reg_out<8>(j1, r) * TC + c] = w[r];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    u[r] = xb[(j0 + B * r) * TC + c];
+    w[r] = xb[(j1 + B * r) * TC + c];
+  }
+  reg_pass<64>(u, j0, tw);
+  reg_pass<64>(w, j1, tw);
+  if (x >= a.W) return;
+  const int sa = 2 * p, sb = 2 * p + 1;
+  const size_t HW = (size_t)a.H * a.W;
+  auto put = [&](int yy, float2 v) {
+    if (yy >= a.H) return;
+    const size_t pix = (size_t)yy * a.W + x;
+    if (MODE == 0) {
+      float* z = a.zern + (size_t)f * a.Z * HW;
+      z[(size_t)(sa + 1) * HW + pix] = v.x;
+      if (sb < a.nslots) z[(size_t)(sb + 1) * HW + pix] = v.y;
+    } else {
+      uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
+      Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
+      if (sb < a.nslots) Xo[(size_t)sb * HW + pix] = f_to_bf16(v.y);
+      if (p == 0) {
+        float* tl = a.tilt + (size_t)f * 2 * HW;
+        tl[pix] = v.x;
+        tl[HW + pix] = v.y;
+      }
+    }
+  };
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    put(j0 + B * r, u[r]);
+    put(j1 + B * r, w[r]);
+  }
+}
+
 int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t s) {
   ColArgs a;
   fill_fft_args(a.fp, pl->fp);
@@ -443,6 +647,18 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   a.zern = zern;
   a.X = pl->d_X;
   a.tilt = pl->d_tilt;
+  if (reg512(pl->fp) && getenv_flag("P2S_FFT_GENERIC") == 0) {
+    dim3 grid((pl->W + 15) / 16, pl->npairs, F);  // only the W cropped columns are needed
+    size_t sm = (size_t)kRegN * 17 * sizeof(float2);
+    if (mode == 0) {
+      cudaFuncSetAttribute(k_cols512<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_cols512<0><<<grid, 512, sm, s>>>(a);
+    } else {
+      cudaFuncSetAttribute(k_cols512<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_cols512<1><<<grid, 512, sm, s>>>(a);
+    }
+    return (int)cudaGetLastError();
+  }
   const int TC = 1 << tcl;
   dim3 grid((pl->W + TC - 1) / TC, pl->npairs, F);
   size_t sm = ((size_t)pl->P + 2 * padded_len((size_t)pl->P * TC)) * sizeof(float2);

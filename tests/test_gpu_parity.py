@@ -81,6 +81,37 @@ def test_sample_zernike_vs_oracle(H, W, dr0, frame0, F):
     assert worst <= 1e-4, worst
 
 
+@pytest.mark.parametrize("H,W,F", [(512, 96, 2), (96, 512, 3), (512, 512, 1)])
+def test_sample_zernike_register_fft_path_vs_oracle(H, W, F):
+    """512-point axes take the register-resident radix-8 kernels (rows: Q = 512, columns:
+    P = 512); each combination with the generic shared-memory path on the other axis."""
+    plan, _, _, sq, L = make_plan(H, W, 1, 3.0, 16, 17)
+    assert (plan.P == 512) or (plan.Q == 512)
+    z = torch.empty((F, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 3, F, z)
+    torch.cuda.synchronize()
+    got = z.cpu().numpy()
+    ref = pipeline.sample_zernike(SEED, 3, F, sq, L, H, W)
+    worst = max(rel_l2(got[f, j], ref[f, j]) for f in range(F) for j in range(1, 36))
+    assert worst <= 1e-4, worst
+
+
+def test_register_fft_matches_generic_fft(monkeypatch):
+    """The 512-point register kernels and the generic shared-memory Stockham kernels run
+    the same radix-8 passes: their fields agree to fp32 rounding."""
+    H = W = 512
+    plan, _, _, _, _ = make_plan(H, W, 1, 3.0, 16, 17)
+    zf = torch.empty((2, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 0, 2, zf)
+    monkeypatch.setenv("P2S_FFT_GENERIC", "1")
+    zg = torch.empty_like(zf)
+    plan.sample_zernike(SEED, 0, 2, zg)
+    torch.cuda.synchronize()
+    a, b = zf.cpu().numpy(), zg.cpu().numpy()
+    worst = max(rel_l2(a[f, j], b[f, j]) for f in range(2) for j in range(1, 36))
+    assert worst <= 1e-6, worst
+
+
 def test_sample_zernike_own_tables_vs_oracle():
     """Library plan tables (C++ quadrature/FFT) instead of the oracle's: the sampled
     fields still agree to the table tolerance."""
