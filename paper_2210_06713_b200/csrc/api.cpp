@@ -155,10 +155,11 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   g.nks = (T * G + 1) / 2;
   const char* pe = getenv("P2S_BLUR_PAIR");
   g.pair = pe ? (atoi(pe) != 0) : true;
-  // B ring: enough stages to cover ~2 us of L2 latency at the MMA rate (a stage is
-  // 2 K-steps x C*racc MMAs); pair mode halves the bytes per stage.
+  // B ring: a stage is kBlurStepsPerStage (4) K-steps x C*racc MMAs.  Large stages keep
+  // the single MMA-issuing thread ahead of the tensor pipe (one barrier wait + commit per
+  // 12 MMAs); 4 stages cover the L2 latency of the B reloads.  Pair mode halves the bytes.
   const char* se = getenv("P2S_BLUR_STAGES");
-  g.stages = se ? std::max(2, std::min(12, atoi(se))) : (g.pair ? 8 : 4);
+  g.stages = se ? std::max(2, std::min(12, atoi(se))) : (g.pair ? 4 : 3);
   g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, g.nks, p->H, g.pair, g.stages);
   g.RS = g.RB + 8 * G;
   const uint32_t sbo = (uint32_t)g.RS * 16;
@@ -207,17 +208,37 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
     for (int i = 0; i < T * T; ++i) s += basis[(size_t)n * T * T + i];
     hs[n] = (float)s;
   }
-  P2S_CUDA(cudaMalloc(&g.bimg, img.size()), "cudaMalloc blur B");
-  P2S_CUDA(cudaMemcpy(g.bimg, img.data(), img.size(), cudaMemcpyHostToDevice), "copy blur B");
-  {  // pair-mode copy: [half][t][np/2 rows x 32 B]
+  // Every CTA streams the same B tiles at about the same time; brep copies (CTA picks one by
+  // its index) spread those reads over more L2 slices.
+  const char* re = getenv("P2S_BLUR_BREP");
+  g.brep = re ? std::max(1, std::min(64, atoi(re))) : 8;
+  g.bstride = (img.size() + 4095) & ~(size_t)4095;
+  P2S_CUDA(cudaMalloc(&g.bimg, g.bstride * g.brep), "cudaMalloc blur B");
+  for (int r = 0; r < g.brep; ++r)
+    P2S_CUDA(cudaMemcpy(g.bimg + r * g.bstride, img.data(), img.size(), cudaMemcpyHostToDevice), "copy blur B");
+  {  // pair-mode copy: [half][t][np/2 rows x 32 B], + 16 zero rows, brep times
     const size_t hb = bbytes / 2;
-    std::vector<uint8_t> img2(img.size());
+    std::vector<uint8_t> img2(img.size() + 4096, 0);
     for (int h = 0; h < 2; ++h)
       for (int t = 0; t < g.nks; ++t)
         std::memcpy(img2.data() + ((size_t)h * g.nks + t) * hb, img.data() + (size_t)t * bbytes + h * hb, hb);
-    P2S_CUDA(cudaMalloc(&g.bimg2, img2.size() + 4096), "cudaMalloc blur B2");
-    P2S_CUDA(cudaMemset(g.bimg2, 0, img2.size() + 4096), "memset blur B2");
-    P2S_CUDA(cudaMemcpy(g.bimg2, img2.data(), img2.size(), cudaMemcpyHostToDevice), "copy blur B2");
+    g.brows = (int)(img2.size() / 256);
+    P2S_CUDA(cudaMalloc(&g.bimg2, img2.size() * g.brep), "cudaMalloc blur B2");
+    for (int r = 0; r < g.brep; ++r)
+      P2S_CUDA(cudaMemcpy(g.bimg2 + r * img2.size(), img2.data(), img2.size(), cudaMemcpyHostToDevice),
+               "copy blur B2");
+  }
+  {
+    std::vector<uint64_t> ad(g.nks);
+    for (int t = 0; t < g.nks; ++t) {
+      uint64_t d = (uint64_t)((koff[t] >> 4) & 0x3FFFu);
+      d |= (uint64_t)((klbo[t] >> 4) & 0x3FFFu) << 16;
+      d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+      d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+      ad[t] = d;
+    }
+    P2S_CUDA(cudaMalloc(&g.adesc, sizeof(uint64_t) * g.nks), "cudaMalloc adesc");
+    P2S_CUDA(cudaMemcpy(g.adesc, ad.data(), sizeof(uint64_t) * g.nks, cudaMemcpyHostToDevice), "copy adesc");
   }
   P2S_CUDA(cudaMalloc(&g.koff, sizeof(uint32_t) * g.nks), "cudaMalloc koff");
   P2S_CUDA(cudaMemcpy(g.koff, koff.data(), sizeof(uint32_t) * g.nks, cudaMemcpyHostToDevice), "copy koff");
@@ -290,11 +311,11 @@ static p2s_status alloc_workspace(p2s_plan_s* p) {
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(P2S_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  {  // B halves for the CTA-pair blur: rows of 256 B; one box = 2 consecutive K-steps of one half
+  {  // B halves for the CTA-pair blur: rows of 256 B; one box = one ring stage of K-steps of one half
     const int rows_per_step = np / 16;  // (np/2 rows x 32 B) / 256 B
-    cuuint64_t bd[2] = {128, (cuuint64_t)(2 * p->bg.nks * rows_per_step + 16)};
+    cuuint64_t bd[2] = {128, (cuuint64_t)p->bg.brows * p->bg.brep};
     cuuint64_t bs[1] = {256};
-    cuuint32_t bb[2] = {128, (cuuint32_t)(2 * rows_per_step)};
+    cuuint32_t bb[2] = {128, (cuuint32_t)(kBlurStepsPerStage * rows_per_step)};
     r = encode(&p->tmap_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->bg.bimg2, bd, bs, bb, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -316,6 +337,7 @@ static void free_plan(p2s_plan_s* p) {
   cudaFree(p->bg.bimg);
   cudaFree(p->bg.bimg2);
   cudaFree(p->bg.koff);
+  cudaFree(p->bg.adesc);
   cudaFree(p->bg.klbo);
   cudaFree(p->bg.hsum);
   cudaFree(p->fq.tw);

@@ -32,7 +32,7 @@
 namespace p2s {
 
 constexpr int kMaxStages = 12;
-constexpr int kStepsPerStage = 2;  // K-steps (B tiles) moved per ring stage
+constexpr int kStepsPerStage = kBlurStepsPerStage;  // K-steps (B tiles) moved per ring stage
 constexpr int kBlurThreads = 320;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue
 constexpr int kEpiWarps = 8;       // two warps per TMEM lane quarter, each summing half the bases
 constexpr int kAccStride = 128;    // TMEM columns per accumulator
@@ -41,15 +41,19 @@ struct BlurArgs {
   const void* src;          // Iw [F][C][H][W] (bf16 or fp32)
   float* out;               // [F][C][H][W]
   const uint8_t* bimg;      // [nks][np*32]
-  const uint32_t* koff;     // [nks]
-  const uint32_t* klbo;     // [nks]
+  const uint64_t* adesc;    // [nks] A descriptor of each K-step relative to tile base 0 (start, LBO, SBO)
+  uint32_t idesc;           // instruction descriptor (M, N = np, A MN-major)
   const float* hsum;        // [np]
   int H, W, T, c, NC, RB, RS, nks, np, stages;
   uint32_t k0, k1;
   int64_t frame0;
   float sigma;
   int normalize, clamp01;
-  unsigned long long* probe;  // optional [8] cycle counters (P2S_BLUR_PROBE), else null
+  unsigned long long* probe;  // optional [12] cycle counters (P2S_BLUR_PROBE), else null
+  int exp;                    // timing experiments only (P2S_BLUR_EXP): 1 skip epilogue, 2 skip B loads
+  unsigned long long* trace;  // optional [n_rg][8] timestamps of CTA (0,0,0) (P2S_BLUR_TRACE), else null
+  int brep, brows;            // B image copies; rows between copies (pair mode tensor map)
+  size_t bstride;             // bytes between copies (bulk path)
 };
 
 __device__ __forceinline__ uint64_t clk() {
@@ -95,7 +99,8 @@ __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int 
 
 template <bool SRC_F32, int C, int RACC, bool PAIR>
 __global__ void __launch_bounds__(kBlurThreads, 1)
-    k_blur(const BlurArgs a, const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_b) {
+    k_blur(const __grid_constant__ BlurArgs a, const __grid_constant__ CUtensorMap tmap_w,
+           const __grid_constant__ CUtensorMap tmap_b) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const BlurSmem L = blur_smem_layout(C, a.NC, a.RS, RACC, a.np, a.nks, PAIR, a.stages);
@@ -103,8 +108,8 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   const uint32_t sbo_src = (uint32_t)a.RS * 16;
   uint8_t* wbuf = smem + L.off_w;
   uint8_t* ring = smem + L.off_ring;
-  uint64_t* s_adesc = reinterpret_cast<uint64_t*>(smem + L.off_desc);
   float* s_hsum = reinterpret_cast<float*>(smem + L.off_hsum);
+  uint64_t* s_adesc = reinterpret_cast<uint64_t*>(smem + L.off_desc);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
   uint64_t* full = bars;
   uint64_t* empty = bars + kBlurStages;
@@ -121,9 +126,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   const uint32_t s_tile = smem_u32(smem);
   const uint64_t t_start = clk();
 
-  // A descriptor of every K-step for (channel 0, row 0): start = tile + koff, LBO, SBO
-  for (int i = tid; i < a.nks; i += kBlurThreads)
-    s_adesc[i] = umma_desc(s_tile + __ldg(&a.koff[i]), __ldg(&a.klbo[i]), sbo_src);
+  for (int i = tid; i < a.nks; i += kBlurThreads) s_adesc[i] = a.adesc[i] + (uint64_t)(s_tile >> 4);
   for (int i = tid; i < a.np; i += kBlurThreads) s_hsum[i] = a.hsum[i];
   if (tid == 0) {
     for (int s = 0; s < kBlurStages; ++s) {
@@ -209,6 +212,9 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     // soon as the epilogue has released group rg-1 (single w buffer).
     uint32_t stage = 0, phase = 0;
     const uint32_t s_wempty = smem_u32(wempty);
+    const int bcopy = (int)((blockIdx.x / 2 + blockIdx.y * 7 + blockIdx.z * 13) % a.brep);
+    const uint8_t* bsrc = a.bimg + (size_t)bcopy * a.bstride;
+    const int brow0 = bcopy * a.brows;
     auto issue_w = [&](int rg) {
       int nrow = 0;
       if (x0 < a.W)
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
         w_done = true;
       }
       for (int st = 0; st < nst; ++st) {
-        if (!w_done && mbar_try_wait(s_wempty, (rg - 1) & 1)) {
+        if (!w_done && mbar_test_wait(s_wempty, (rg - 1) & 1)) {
           if (elect_one()) issue_w(rg);
           __syncwarp();
           w_done = true;
@@ -235,14 +241,14 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         const int t0 = st * kStepsPerStage;
         const int nt = min(kStepsPerStage, a.nks - t0);
-        if (elect_one()) {
+        if (!(a.exp & 2) && elect_one()) {
           if (PAIR) {  // both CTAs load their half; the bytes count on the leader's barrier
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStepsPerStage * bbytes);
             tma_load_2d_pair(ring + stage * kStepsPerStage * bbytes, &tmap_b, 0,
-                             ((int)rank * a.nks + t0) * (int)(bbytes / 256), &full[stage]);
+                             brow0 + ((int)rank * a.nks + t0) * (int)(bbytes / 256), &full[stage]);
           } else {
             mbar_arrive_expect_tx(&full[stage], nt * bbytes);
-            bulk_g2s(ring + stage * kStepsPerStage * bbytes, a.bimg + (size_t)t0 * bbytes, nt * bbytes, &full[stage]);
+            bulk_g2s(ring + stage * kStepsPerStage * bbytes, bsrc + (size_t)t0 * bbytes, nt * bbytes, &full[stage]);
           }
         }
         __syncwarp();
@@ -259,23 +265,37 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     }
   } else if (warp == 1 && leader) {
     // ---- MMA issuer (whole warp, one elected lane issues): C x RACC accumulators per K-step
-    const uint32_t idesc = umma_idesc_bf16(PAIR ? 256 : 128, a.np, true, false);
     uint32_t stage = 0, phase = 0;
     const uint64_t ch_step = (uint64_t)(L.tile_bytes >> 4);
+    const uint64_t b_desc_base = umma_desc(smem_u32(ring), 128, 256);
+    if (tmem != 0) __trap();  // accumulators are addressed from column 0
     uint64_t w_full = 0, w_tempty = 0;
     const uint64_t t_mma0 = clk();
+    unsigned long long* tr = (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? a.trace : nullptr;
     for (int rg = 0; rg < n_rg; ++rg) {
       uint64_t t0c = clk();
       mbar_wait(tempty, (rg & 1) ^ 1);
-      w_tempty += clk() - t0c;
+      const uint64_t t_ok = clk();
+      if (tr && lane == 0) tr[1600 + rg] = global_ns();
+      w_tempty += t_ok - t0c;
+      uint64_t fw = 0, fmax = 0, fmax_st = 0;
       tc_fence_after();
-      const uint64_t row_off = (uint64_t)(rg * RACC);  // start address += rg*RACC*16 bytes
+      const uint64_t a_row_desc = (uint64_t)(rg * RACC);  // start address += rows of this group
       for (int st = 0; st < nst; ++st) {
         uint64_t t1c = clk();
-        mbar_wait(&full[stage], phase);
-        w_full += clk() - t1c;
+        if (!(a.exp & 2)) mbar_wait(&full[stage], phase);
+        const uint64_t dw = clk() - t1c;
+        w_full += dw;
+        fw += dw;
+        if (dw > fmax) {
+          fmax = dw;
+          fmax_st = st;
+        }
         tc_fence_after();
-        const uint64_t bdesc0 = umma_desc(smem_u32(ring + stage * kStepsPerStage * bbytes), 128, 256);
+        // One elected lane issues.  TMEM accumulators sit at fixed columns (the CTA owns the
+        // whole TMEM, base 0); the K-step descriptors and the instruction descriptor come
+        // from the kernel-parameter bank, so the loop is a handful of uniform adds per MMA.
+        const uint64_t bdesc0 = b_desc_base + (uint64_t)((stage * kStepsPerStage * bbytes) >> 4);
         const int t0 = st * kStepsPerStage;
         if (elect_one()) {
 #pragma unroll
@@ -283,16 +303,18 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
             const int t = t0 + u;
             if (t < a.nks) {
               const uint64_t bd = bdesc0 + (uint64_t)((u * bbytes) >> 4);
-              const uint64_t ad = s_adesc[t] + row_off;
+              const uint64_t ad = s_adesc[t] + a_row_desc;
               const uint32_t acc = t > 0 ? 1u : 0u;
 #pragma unroll
               for (int ch = 0; ch < C; ++ch)
 #pragma unroll
                 for (int r = 0; r < RACC; ++r) {
                   if (PAIR)
-                    umma_bf16_pair(tmem + (ch * RACC + r) * kAccStride, ad + ch * ch_step + (uint64_t)r, bd, idesc, acc);
+                    umma_bf16_pair((uint32_t)((ch * RACC + r) * kAccStride), ad + ch * ch_step + (uint64_t)r, bd,
+                                   a.idesc, acc);
                   else
-                    umma_bf16(tmem + (ch * RACC + r) * kAccStride, ad + ch * ch_step + (uint64_t)r, bd, idesc, acc);
+                    umma_bf16((uint32_t)((ch * RACC + r) * kAccStride), ad + ch * ch_step + (uint64_t)r, bd, a.idesc,
+                              acc);
                 }
             }
           }
@@ -314,6 +336,14 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
           umma_commit(tfull);
       }
       __syncwarp();
+      if (tr && lane == 0) {
+        tr[1536 + rg] = global_ns();
+        tr[rg * 8 + 0] = t0c - t_start;
+        tr[rg * 8 + 1] = t_ok - t_start;
+        tr[rg * 8 + 2] = clk() - t_start;
+        tr[rg * 8 + 3] = fw;
+        tr[rg * 8 + 4] = fmax_st * 100000ull + fmax;
+      }
     }
     if (a.probe && lane == 0) {
       atomicAdd(&a.probe[1], (unsigned long long)w_full);
@@ -335,7 +365,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     float* part = reinterpret_cast<float*>(smem + L.off_part);
     const int nch = a.np / 16, half = (nch + 1) / 2;
     const int cb0 = h ? half : 0, cb1 = h ? nch : half;
-    uint64_t e_wait = 0, e_work = 0;
+    uint64_t e_wait = 0, e_work = 0, e_ld = 0, e_rel = 0;
     for (int rg = 0; rg < n_rg; ++rg) {
       uint64_t t0c = clk();
       mbar_wait(tfull, rg & 1);
@@ -343,6 +373,18 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       tc_fence_after();
       uint64_t t1c = clk();
       e_wait += t1c - t0c;
+      if (a.exp & 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(wempty);
+          if (PAIR)
+            mbar_arrive_cluster(t_tempty_leader);
+          else
+            mbar_arrive(tempty);
+        }
+        continue;
+      }
       float accs[RACC][C + 1];
 #pragma unroll
       for (int r = 0; r < RACC; ++r) {
@@ -360,7 +402,9 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) accs[r][C] = fmaf(wf[i], s_hsum[cb * 16 + i], accs[r][C]);
           }
+          const uint64_t tl0 = clk();
           tmem_wait_ld();
+          e_ld += clk() - tl0;
 #pragma unroll
           for (int ch = 0; ch < C; ++ch)
 #pragma unroll
@@ -370,15 +414,33 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       // TMEM and w of this group are consumed by this warp.  h = 0 releases them only after
       // its barrier wait, so h = 1 cannot reach the next group's barrier arrive first.
       auto release = [&]() {
+        e_rel += clk() - t1c;
+        if (a.trace && warp == 2 && lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+          a.trace[rg * 8 + 5] = t1c - t_start;
+          a.trace[rg * 8 + 6] = clk() - t_start;
+        }
+        const uint64_t q0 = clk();
         tc_fence_before();
         __syncwarp();
+        const uint64_t q1 = clk();
+        uint64_t q2 = q1;
         if (lane == 0) {
           mbar_arrive(wempty);
+          q2 = clk();
           if (PAIR)
             mbar_arrive_cluster(t_tempty_leader);
           else
             mbar_arrive(tempty);
         }
+        const uint64_t q3 = clk();
+        if (a.trace && lane == 0 && (warp == 2 || warp == 6) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+          unsigned long long* q = a.trace + 1700 + (warp == 6 ? 3 * 64 : 0) + rg * 3;
+          q[0] = q1 - q0;
+          q[1] = q2 - q1;
+          q[2] = q3 - q2;
+        }
+        if (a.trace && lane == 0 && blockIdx.x < 2 && blockIdx.y == 0 && blockIdx.z == 0)
+          a.trace[512 + (blockIdx.x * 64 + rg) * 8 + (warp - 2)] = global_ns();
       };
       float* pb = part + (size_t)(rg & 1) * RACC * 128 * (C + 1);
       if (h == 1) {
@@ -418,6 +480,12 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     if (a.probe && warp == 2 && lane == 0) {
       atomicAdd(&a.probe[4], (unsigned long long)e_wait);
       atomicAdd(&a.probe[5], (unsigned long long)e_work);
+      atomicAdd(&a.probe[8], (unsigned long long)e_ld);
+      atomicAdd(&a.probe[9], (unsigned long long)e_rel);
+    }
+    if (a.probe && warp == 6 && lane == 0) {
+      atomicAdd(&a.probe[10], (unsigned long long)e_ld);
+      atomicAdd(&a.probe[11], (unsigned long long)e_rel);
     }
   }
   tc_fence_before();
@@ -475,9 +543,12 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.src = src;
   a.out = out;
   a.bimg = g.bimg;
-  a.koff = g.koff;
-  a.klbo = g.klbo;
+  a.adesc = g.adesc;
+  a.idesc = umma_idesc_bf16(g.pair ? 256 : 128, g.np, true, false);
   a.hsum = g.hsum;
+  a.brep = g.brep;
+  a.brows = g.brows;
+  a.bstride = g.bstride;
   a.H = p->H;
   a.W = p->W;
   a.T = g.T;
@@ -494,11 +565,20 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.normalize = p->normalize;
   a.clamp01 = p->clamp01;
   a.probe = nullptr;
+  a.exp = getenv("P2S_BLUR_EXP") ? atoi(getenv("P2S_BLUR_EXP")) : 0;
+  static unsigned long long* trace = nullptr;
+  const bool want_trace = getenv("P2S_BLUR_TRACE") != nullptr;
+  a.trace = nullptr;
+  if (want_trace) {
+    if (!trace) cudaMalloc(&trace, 2400 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace, 0, 2400 * sizeof(unsigned long long), s);
+    a.trace = trace;
+  }
   static unsigned long long* probe = nullptr;
   const bool want_probe = getenv("P2S_BLUR_PROBE") != nullptr;
   if (want_probe) {
-    if (!probe) cudaMalloc(&probe, 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(probe, 0, 8 * sizeof(unsigned long long), s);
+    if (!probe) cudaMalloc(&probe, 12 * sizeof(unsigned long long));
+    cudaMemsetAsync(probe, 0, 12 * sizeof(unsigned long long), s);
     a.probe = probe;
   }
   const bool pair = g.pair;
@@ -517,15 +597,36 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   else
     rc = src_f32 ? launch_blur_c<true, false>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s)
                  : launch_blur_c<false, false>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s);
+  if (want_trace) {  // debug: per-group timeline of CTA (0,0,0)
+    static unsigned long long h[2400];
+    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[blur trace] rg: mma_wait_start tempty_ok issue_end full_wait (max@st) | epi tfull_ok release\n");
+    for (int rg = 0; rg < (a.RB + g.racc - 1) / g.racc && rg < 64; ++rg)
+      fprintf(stderr, "[blur trace] %2d: %8llu %8llu %8llu %6llu (%llu@%llu) | %8llu %8llu\n", rg, h[rg * 8], h[rg * 8 + 1],
+              h[rg * 8 + 2], h[rg * 8 + 3], h[rg * 8 + 4] % 100000ull, h[rg * 8 + 4] / 100000ull, h[rg * 8 + 5],
+              h[rg * 8 + 6]);
+    // release times (ns) of the 8 epilogue warps of both CTAs relative to the MMA warp's
+    // commit-of-tfull time of the same group (globaltimer)
+    for (int rg = 0; rg < 8; ++rg) {
+      fprintf(stderr, "[blur trace] rg %d release-ns after tfull commit: cta0", rg);
+      for (int w = 0; w < 8; ++w) fprintf(stderr, " %lld", (long long)(h[512 + rg * 8 + w] - h[1536 + rg]));
+      fprintf(stderr, " | cta1");
+      for (int w = 0; w < 8; ++w) fprintf(stderr, " %lld", (long long)(h[512 + (64 + rg) * 8 + w] - h[1536 + rg]));
+      fprintf(stderr, " | next tempty_ok %lld | cyc fence/arr_w/arr_t w2 %llu %llu %llu w6 %llu %llu %llu\n",
+              (long long)(h[1600 + rg + 1] - h[1536 + rg]), h[1700 + rg * 3], h[1701 + rg * 3], h[1702 + rg * 3],
+              h[1700 + 192 + rg * 3], h[1701 + 192 + rg * 3], h[1702 + 192 + rg * 3]);
+    }
+  }
   if (want_probe) {  // debug: per-CTA averages of the phase cycle counters
-    unsigned long long h[8];
+    unsigned long long h[12];
     cudaMemcpyAsync(h, probe, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     const double n = h[7] ? (double)h[7] : 1.0, nm = pair ? n / 2 : n;
     fprintf(stderr,
             "[blur probe] CTAs %llu  per CTA cycles: total %.0f prologue %.0f | MMA warp: loop %.0f wait_full %.0f "
-            "wait_tmem %.0f | epilogue warp: wait %.0f work %.0f\n",
-            h[7], h[6] / n, h[0] / n, h[3] / nm, h[1] / nm, h[2] / nm, h[4] / n, h[5] / n);
+            "wait_tmem %.0f | epilogue warp: wait %.0f work %.0f (tmem_wait_ld %.0f, to release %.0f; h1: %.0f, %.0f)\n",
+            h[7], h[6] / n, h[0] / n, h[3] / nm, h[1] / nm, h[2] / nm, h[4] / n, h[5] / n, h[8] / n, h[9] / n, h[10] / n, h[11] / n);
   }
   return rc;
 }

@@ -48,6 +48,12 @@ struct MlpGeom {
 };
 
 // Blur geometry: K-step schedule of the tap-row groups (see k_blur.cu).
+// K-steps (B tiles) moved per blur ring stage (the pair-mode B tensor-map box spans one stage).
+#ifndef P2S_KSPS
+#define P2S_KSPS 4
+#endif
+constexpr int kBlurStepsPerStage = P2S_KSPS;
+
 struct BlurGeom {
   int T = 0, c = 0;        // taps, centre
   int NC = 0;              // source chunks = T + 15
@@ -63,6 +69,10 @@ struct BlurGeom {
   uint8_t* bimg = nullptr;   // device [nks][np*32 bytes] B tiles (K-major, no swizzle)
   uint8_t* bimg2 = nullptr;  // device [2 halves][nks][np*16 bytes] (pair mode)
   float* hsum = nullptr;     // device [np] per-basis tap sum (normalisation)
+  uint64_t* adesc = nullptr;  // device [nks]: A descriptor per K-step relative to tile base 0
+  int brep = 1;              // copies of the B image in HBM (spreads the L2 hot spot)
+  size_t bstride = 0;        // bytes between copies of bimg
+  int brows = 0;             // 256-byte rows between copies of bimg2 (tmap_b coordinate)
 };
 
 }  // namespace p2s

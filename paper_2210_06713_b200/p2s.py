@@ -14,7 +14,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libp2s.so")
+# P2S_LIB_NAME selects an alternative in-tree build (tuning experiments only).
+LIB_PATH = os.path.join(_HERE, os.environ.get("P2S_LIB_NAME", "libp2s.so"))
 
 P2S_OK = 0
 _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NUMERIC", 3: "CUDA", 4: "OUT_OF_MEMORY", 5: "UNSUPPORTED"}
