@@ -273,7 +273,7 @@ static size_t frame_bytes(const p2s_plan_s* p) {
   b += HW * (size_t)std::max(p->nslots, p->Z - 3) * 2;
   b += 2 * HW * 4;
   b += (size_t)p->C * HW * 2;
-  b += (HW + 8) * (size_t)p->mg_fold.n3 * 2;
+  b += (size_t)p->H * ((p->W + 127) / 128) * 128 * (size_t)p->mg_fold.n3 * 2;
   b += 2 * (size_t)p->C * HW * 4;
   return b + 5 * 256;
 }
@@ -292,25 +292,18 @@ static p2s_status alloc_workspace(p2s_plan_s* p) {
   p->d_X = reinterpret_cast<uint16_t*>(take(mb * HW * (size_t)std::max(p->nslots, p->Z - 3) * 2));
   p->d_tilt = reinterpret_cast<float*>(take(mb * 2 * HW * 4));
   p->d_Iw = reinterpret_cast<uint16_t*>(take(mb * (size_t)p->C * HW * 2));
-  p->HWp = (int)((HW + 7) / 8 * 8);
-  p->d_w = reinterpret_cast<uint16_t*>(take(mb * (size_t)p->HWp * p->mg_fold.n3 * 2));
+  p->ntx = (p->W + 127) / 128;
+  p->d_w = reinterpret_cast<uint16_t*>(take(mb * (size_t)p->H * p->ntx * 128 * p->mg_fold.n3 * 2));
   p->d_img = reinterpret_cast<float*>(take(mb * (size_t)p->C * HW * 4));
   p->d_out = reinterpret_cast<float*>(take(mb * (size_t)p->C * HW * 4));
-  // TMA view of the basis-weight planes for the blur epilogue: rows = (frame, k), cols = pixels
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
       q != cudaDriverEntryPointSuccess || !encode)
     return set_error(P2S_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int np = p->mg_fold.n3;
-  cuuint64_t dims[2] = {(cuuint64_t)p->HWp, (cuuint64_t)mb * np};
-  cuuint64_t strides[1] = {(cuuint64_t)p->HWp * 2};
-  cuuint32_t box[2] = {128, (cuuint32_t)np};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(&p->tmap_w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->d_w, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return set_error(P2S_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  CUresult r;
   {  // B halves for the CTA-pair blur: rows of 256 B; one box = one ring stage of K-steps of one half
     const int rows_per_step = np / 16;  // (np/2 rows x 32 B) / 256 B
     cuuint64_t bd[2] = {128, (cuuint64_t)p->bg.brows * p->bg.brep};

@@ -16,10 +16,11 @@
 // offset.  Descriptors of all K-steps are precomputed once per CTA in shared memory; the
 // MMA warp issues C x RACC tcgen05.mma per K-step under elect.sync.
 // The B operand (taps x bases, precomputed per K-step on the host) streams through a TMA
-// bulk-copy ring shared by all accumulators.  Per row group the P2S weights w (k-major
-// planes) arrive by one 2-D TMA tile load per row.  The epilogue warps read the
-// accumulators with tcgen05.ld, form sum_k w_k(x) conv_k(x), apply step 5 (normalise,
-// Philox noise, clamp) and write the output: the only HBM write of the frame.
+// bulk-copy ring shared by all accumulators (4 K-steps per stage).  The 16 epilogue warps
+// read the accumulators with tcgen05.ld, release TMEM as soon as their reads have landed,
+// form sum_k w_k(x) conv_k(x) with the P2S weights w (per-pixel 16-byte loads from HBM,
+// prefetched one row group ahead), apply step 5 (normalise, Philox noise, clamp) and
+// write the output: the only HBM write of the frame.
 // PAIR mode (CTA pairs on adjacent x-tiles, cluster of 2): the even CTA issues
 // tcgen05.mma.cta_group::2 with M = 256; each CTA supplies its own 128 pixels of A and half
 // of the bases of B, halving the shared-memory and L2 traffic of the B operand per SM.
@@ -33,25 +34,26 @@ namespace p2s {
 
 constexpr int kMaxStages = 12;
 constexpr int kStepsPerStage = kBlurStepsPerStage;  // K-steps (B tiles) moved per ring stage
-constexpr int kBlurThreads = 320;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue
-constexpr int kEpiWarps = 8;       // two warps per TMEM lane quarter, each summing half the bases
+constexpr int kEpiWarps = 16;      // four warps per TMEM lane quarter, each owning two 16-basis chunks
+constexpr int kBlurThreads = 64 + 32 * kEpiWarps;  // warp 0 TMA producer, warp 1 MMA issuer, epilogue
 constexpr int kAccStride = 128;    // TMEM columns per accumulator
+constexpr int kLoadRows = 4;       // source rows staged per warp by the tile loader
+constexpr int kSeg = 192;          // staged pixels per source row (>= 128 + T - 1 for T <= 63)
 
 struct BlurArgs {
   const void* src;          // Iw [F][C][H][W] (bf16 or fp32)
   float* out;               // [F][C][H][W]
+  const uint16_t* w;        // P2S weights [F][H][ntx][np/8][128 px][8] bf16 (k_mlp output)
   const uint8_t* bimg;      // [nks][np*32]
   const uint64_t* adesc;    // [nks] A descriptor of each K-step relative to tile base 0 (start, LBO, SBO)
   uint32_t idesc;           // instruction descriptor (M, N = np, A MN-major)
   const float* hsum;        // [np]
-  int H, W, T, c, NC, RB, RS, nks, np, stages;
+  int H, W, T, c, NC, RB, RS, nks, np, stages, ntx;
   uint32_t k0, k1;
   int64_t frame0;
   float sigma;
   int normalize, clamp01;
-  unsigned long long* probe;  // optional [12] cycle counters (P2S_BLUR_PROBE), else null
-  int exp;                    // timing experiments only (P2S_BLUR_EXP): 1 skip epilogue, 2 skip B loads
-  unsigned long long* trace;  // optional [n_rg][8] timestamps of CTA (0,0,0) (P2S_BLUR_TRACE), else null
+  unsigned long long* probe;  // optional [8] cycle counters (P2S_BLUR_PROBE), else null
   int brep, brows;            // B image copies; rows between copies (pair mode tensor map)
   size_t bstride;             // bytes between copies (bulk path)
 };
@@ -69,44 +71,40 @@ __device__ __forceinline__ int reflect_idx(int i, int n) {
 }
 
 template <bool SRC_F32>
-__device__ __forceinline__ float load_src(const void* src, size_t idx) {
-  if (SRC_F32) return __ldg(reinterpret_cast<const float*>(src) + idx);
-  return bf16_to_f(__ldg(reinterpret_cast<const uint16_t*>(src) + idx));
+__device__ __forceinline__ uint16_t load_src_bf16(const void* src, size_t idx) {
+  if (SRC_F32) return f_to_bf16(__ldg(reinterpret_cast<const float*>(src) + idx));
+  return __ldg(reinterpret_cast<const uint16_t*>(src) + idx);
 }
 
 struct BlurSmem {
-  uint32_t tile_bytes, w_bytes, b_bytes;
-  uint32_t off_w, off_ring, off_desc, off_hsum, off_part, off_bar, total;
+  uint32_t tile_bytes, b_bytes, ring_bytes;
+  uint32_t off_ring, off_desc, off_hsum, off_part, off_bar, total;
 };
 
 __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int racc, int np, int nks, bool pair,
                                                      int stages) {
   BlurSmem L;
   L.tile_bytes = ((uint32_t)NC * RS * 16 + 127) & ~127u;
-  L.w_bytes = (uint32_t)racc * np * 128 * 2;  // [racc][np][128 px] bf16
-  const uint32_t stg_bytes = (kBlurThreads / 32) * 4u * 192 * 4;   // the loader's staging rows
-  if (L.w_bytes < stg_bytes) L.w_bytes = stg_bytes;
   L.b_bytes = (uint32_t)np * 32 / (pair ? 2 : 1);  // per K-step: this CTA's rows of B
-  L.off_w = C * L.tile_bytes;
-  L.off_ring = (L.off_w + L.w_bytes + 127) & ~127u;
-  L.off_desc = L.off_ring + stages * kStepsPerStage * L.b_bytes;
+  L.ring_bytes = stages * kStepsPerStage * L.b_bytes;
+  const uint32_t stg_bytes = (kBlurThreads / 32) * kLoadRows * kSeg * 2;  // the loader's staging (bf16)
+  L.off_ring = C * L.tile_bytes;
+  L.off_desc = L.off_ring + (L.ring_bytes > stg_bytes ? L.ring_bytes : stg_bytes);
   L.off_hsum = L.off_desc + 8 * nks;
-  L.off_part = (L.off_hsum + 4 * np + 15) & ~15u;  // [2][racc][128][C+1] epilogue partial sums
-  L.off_bar = L.off_part + 2u * racc * 128 * (C + 1) * 4;
-  L.total = L.off_bar + (2 * stages + 4) * 8 + 16;
+  L.off_part = (L.off_hsum + 4 * np + 15) & ~15u;  // [2 parity][3 parts][racc][C+1][128] partial sums
+  L.off_bar = L.off_part + 2u * 3 * racc * (C + 1) * 128 * 4;
+  L.total = L.off_bar + (2 * stages + 2) * 8 + 16;
   return L;
 }
 
 template <bool SRC_F32, int C, int RACC, bool PAIR>
 __global__ void __launch_bounds__(kBlurThreads, 1)
-    k_blur(const __grid_constant__ BlurArgs a, const __grid_constant__ CUtensorMap tmap_w,
-           const __grid_constant__ CUtensorMap tmap_b) {
+    k_blur(const __grid_constant__ BlurArgs a, const __grid_constant__ CUtensorMap tmap_b) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const BlurSmem L = blur_smem_layout(C, a.NC, a.RS, RACC, a.np, a.nks, PAIR, a.stages);
   const int kBlurStages = a.stages;
   const uint32_t sbo_src = (uint32_t)a.RS * 16;
-  uint8_t* wbuf = smem + L.off_w;
   uint8_t* ring = smem + L.off_ring;
   float* s_hsum = reinterpret_cast<float*>(smem + L.off_hsum);
   uint64_t* s_adesc = reinterpret_cast<uint64_t*>(smem + L.off_desc);
@@ -115,9 +113,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   uint64_t* empty = bars + kBlurStages;
   uint64_t* tfull = bars + 2 * kBlurStages;
   uint64_t* tempty = tfull + 1;  // TMEM free (on the MMA-issuing CTA; one arrival per epilogue warp)
-  uint64_t* wfull = tfull + 2;
-  uint64_t* wempty = tfull + 3;  // this CTA's w buffer free (kEpiWarps arrivals)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(wempty + 1);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
 
@@ -135,8 +131,6 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, PAIR ? 2 * kEpiWarps : kEpiWarps);
-    mbar_init(wfull, 1);
-    mbar_init(wempty, kEpiWarps);
     mbar_fence_init();
   }
   if (warp == 0) {
@@ -148,12 +142,11 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
 
   // ---- source tiles of every channel: chunk cc of row rl holds the 8 pixels at window
   // offsets cc + 16 j of source row y0 - c + rl (mirror boundary).  Each warp stages
-  // kLoadRows coalesced row segments at once (all their loads in flight together), then
-  // packs the chunks.
+  // kLoadRows row segments (bf16, all loads in flight together) in the not-yet-used B ring,
+  // then packs the chunks.
   {
-    constexpr int kLoadRows = 4;
-    constexpr int kSeg = 192;  // >= 128 + T - 1 for T <= 63
-    float* stg = reinterpret_cast<float*>(wbuf) + warp * kLoadRows * kSeg;
+    constexpr int kE = (kSeg + 31) / 32;
+    uint16_t* stg = reinterpret_cast<uint16_t*>(ring) + warp * kLoadRows * kSeg;
     const int rows_real = a.RB + a.T - 1;
     const int seg = 128 + a.T - 1;
     const int nwarps = kBlurThreads / 32;
@@ -161,33 +154,33 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       uint8_t* tile = smem + ch * L.tile_bytes;
       const size_t plane = ((size_t)f * C + ch) * HW;
       for (int rl0 = warp * kLoadRows; rl0 < a.RS; rl0 += nwarps * kLoadRows) {
-        float v[kLoadRows][(kSeg + 31) / 32];
+        uint16_t v[kLoadRows][kE];
 #pragma unroll
         for (int u = 0; u < kLoadRows; ++u) {
           const int rl = rl0 + u;
           const size_t rowb = plane + (size_t)reflect_idx(y0 - a.c + rl, a.H) * a.W;
 #pragma unroll
-          for (int e = 0; e < (kSeg + 31) / 32; ++e) {
+          for (int e = 0; e < kE; ++e) {
             const int i = lane + 32 * e;
-            v[u][e] = (rl < rows_real && i < seg) ? load_src<SRC_F32>(a.src, rowb + reflect_idx(x0 - a.c + i, a.W))
-                                                  : 0.f;
+            v[u][e] = (rl < rows_real && i < seg) ? load_src_bf16<SRC_F32>(a.src, rowb + reflect_idx(x0 - a.c + i, a.W))
+                                                  : (uint16_t)0;
           }
         }
 #pragma unroll
         for (int u = 0; u < kLoadRows; ++u)
 #pragma unroll
-          for (int e = 0; e < (kSeg + 31) / 32; ++e)
+          for (int e = 0; e < kE; ++e)
             if (lane + 32 * e < kSeg) stg[u * kSeg + lane + 32 * e] = v[u][e];
         __syncwarp();
         for (int u = 0; u < kLoadRows; ++u) {
           const int rl = rl0 + u;
           if (rl >= a.RS) break;
-          const float* sr = stg + u * kSeg;
+          const uint16_t* sr = stg + u * kSeg;
           for (int cc = lane; cc < a.NC; cc += 32) {
             uint4 q = make_uint4(0, 0, 0, 0);
             if (rl < rows_real)
-              q = make_uint4(pack_bf16x2(sr[cc], sr[cc + 16]), pack_bf16x2(sr[cc + 32], sr[cc + 48]),
-                             pack_bf16x2(sr[cc + 64], sr[cc + 80]), pack_bf16x2(sr[cc + 96], sr[cc + 112]));
+              q = make_uint4(sr[cc] | ((uint32_t)sr[cc + 16] << 16), sr[cc + 32] | ((uint32_t)sr[cc + 48] << 16),
+                             sr[cc + 64] | ((uint32_t)sr[cc + 80] << 16), sr[cc + 96] | ((uint32_t)sr[cc + 112] << 16));
             *reinterpret_cast<uint4*>(tile + (size_t)cc * sbo_src + rl * 16) = q;
           }
         }
@@ -208,40 +201,17 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   const uint32_t bbytes = L.b_bytes;
 
   if (warp == 0) {
-    // ---- TMA producer: B tiles stream continuously; the w rows of group rg are issued as
-    // soon as the epilogue has released group rg-1 (single w buffer).
+    // ---- TMA producer: the B tiles of every row group stream through the ring.
     uint32_t stage = 0, phase = 0;
-    const uint32_t s_wempty = smem_u32(wempty);
     const int bcopy = (int)((blockIdx.x / 2 + blockIdx.y * 7 + blockIdx.z * 13) % a.brep);
     const uint8_t* bsrc = a.bimg + (size_t)bcopy * a.bstride;
     const int brow0 = bcopy * a.brows;
-    auto issue_w = [&](int rg) {
-      int nrow = 0;
-      if (x0 < a.W)
-        for (int r = 0; r < RACC; ++r) nrow += (y0 + rg * RACC + r < a.H) ? 1 : 0;
-      mbar_arrive_expect_tx(wfull, (uint32_t)nrow * a.np * 128 * 2);
-      for (int r = 0; r < RACC; ++r) {
-        const int y = y0 + rg * RACC + r;
-        if (y < a.H && x0 < a.W) tma_load_2d(wbuf + (size_t)r * a.np * 256, &tmap_w, y * a.W + x0, f * a.np, wfull);
-      }
-    };
     for (int rg = 0; rg < n_rg; ++rg) {
-      bool w_done = false;
-      if (rg == 0) {
-        if (elect_one()) issue_w(0);
-        __syncwarp();
-        w_done = true;
-      }
       for (int st = 0; st < nst; ++st) {
-        if (!w_done && mbar_test_wait(s_wempty, (rg - 1) & 1)) {
-          if (elect_one()) issue_w(rg);
-          __syncwarp();
-          w_done = true;
-        }
         mbar_wait(&empty[stage], phase ^ 1);
         const int t0 = st * kStepsPerStage;
         const int nt = min(kStepsPerStage, a.nks - t0);
-        if (!(a.exp & 2) && elect_one()) {
+        if (elect_one()) {
           if (PAIR) {  // both CTAs load their half; the bytes count on the leader's barrier
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStepsPerStage * bbytes);
             tma_load_2d_pair(ring + stage * kStepsPerStage * bbytes, &tmap_b, 0,
@@ -257,44 +227,27 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
           phase ^= 1;
         }
       }
-      if (!w_done) {
-        mbar_wait(wempty, (rg - 1) & 1);
-        if (elect_one()) issue_w(rg);
-        __syncwarp();
-      }
     }
   } else if (warp == 1 && leader) {
-    // ---- MMA issuer (whole warp, one elected lane issues): C x RACC accumulators per K-step
+    // ---- MMA issuer (one elected lane): C x RACC accumulators per K-step, kStepsPerStage
+    // K-steps per ring stage so the issuing thread stays ahead of the tensor pipe.
     uint32_t stage = 0, phase = 0;
     const uint64_t ch_step = (uint64_t)(L.tile_bytes >> 4);
     const uint64_t b_desc_base = umma_desc(smem_u32(ring), 128, 256);
     if (tmem != 0) __trap();  // accumulators are addressed from column 0
     uint64_t w_full = 0, w_tempty = 0;
     const uint64_t t_mma0 = clk();
-    unsigned long long* tr = (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? a.trace : nullptr;
     for (int rg = 0; rg < n_rg; ++rg) {
       uint64_t t0c = clk();
       mbar_wait(tempty, (rg & 1) ^ 1);
-      const uint64_t t_ok = clk();
-      if (tr && lane == 0) tr[1600 + rg] = global_ns();
-      w_tempty += t_ok - t0c;
-      uint64_t fw = 0, fmax = 0, fmax_st = 0;
+      w_tempty += clk() - t0c;
       tc_fence_after();
       const uint64_t a_row_desc = (uint64_t)(rg * RACC);  // start address += rows of this group
       for (int st = 0; st < nst; ++st) {
-        uint64_t t1c = clk();
-        if (!(a.exp & 2)) mbar_wait(&full[stage], phase);
-        const uint64_t dw = clk() - t1c;
-        w_full += dw;
-        fw += dw;
-        if (dw > fmax) {
-          fmax = dw;
-          fmax_st = st;
-        }
+        const uint64_t t1c = clk();
+        mbar_wait(&full[stage], phase);
+        w_full += clk() - t1c;
         tc_fence_after();
-        // One elected lane issues.  TMEM accumulators sit at fixed columns (the CTA owns the
-        // whole TMEM, base 0); the K-step descriptors and the instruction descriptor come
-        // from the kernel-parameter bank, so the loop is a handful of uniform adds per MMA.
         const uint64_t bdesc0 = b_desc_base + (uint64_t)((stage * kStepsPerStage * bbytes) >> 4);
         const int t0 = st * kStepsPerStage;
         if (elect_one()) {
@@ -336,14 +289,6 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
           umma_commit(tfull);
       }
       __syncwarp();
-      if (tr && lane == 0) {
-        tr[1536 + rg] = global_ns();
-        tr[rg * 8 + 0] = t0c - t_start;
-        tr[rg * 8 + 1] = t_ok - t_start;
-        tr[rg * 8 + 2] = clk() - t_start;
-        tr[rg * 8 + 3] = fw;
-        tr[rg * 8 + 4] = fmax_st * 100000ull + fmax;
-      }
     }
     if (a.probe && lane == 0) {
       atomicAdd(&a.probe[1], (unsigned long long)w_full);
@@ -351,116 +296,132 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       atomicAdd(&a.probe[3], (unsigned long long)(clk() - t_mma0));
     }
   } else if (warp >= 2) {
-    // ---- epilogue warps 2..9: TMEM lane quarter = warp % 4; half h of the basis chunks.
-    // h = 1 leaves its partial sums in smem (double-buffered by group parity); h = 0 adds
-    // them, applies step 5 and stores.
+    // ---- epilogue warps 2..17: TMEM lane quarter qd = warp % 4; part h = 0..3 owns the
+    // 16-basis chunks 2h and 2h+1.  Each warp reads its accumulator columns, releases TMEM
+    // right after its last tcgen05.ld has landed (the next row group's MMAs start while the
+    // sums are formed), weights them with w (prefetched from HBM one group ahead, 16-byte
+    // loads of 8 bases), and parts 1-3 hand partial sums to part 0, which applies step 5.
     const int qd = warp & 3;
     const int h = (warp - 2) >> 2;
     const int m = qd * 32 + lane;
     const int q = 16 * (m & 7) + (m >> 3);
     const int x = x0 + q;
     const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
-    const uint16_t* wq = reinterpret_cast<const uint16_t*>(wbuf) + q;
     const uint32_t t_tempty_leader = PAIR ? mapa_shared(tempty, 0) : 0u;
     float* part = reinterpret_cast<float*>(smem + L.off_part);
-    const int nch = a.np / 16, half = (nch + 1) / 2;
-    const int cb0 = h ? half : 0, cb1 = h ? nch : half;
-    uint64_t e_wait = 0, e_work = 0, e_ld = 0, e_rel = 0;
+    const int nch = a.np / 16;
+    const int xt = blockIdx.x;
+    const size_t wrow = (size_t)a.ntx * a.np * 128;  // elements per image row of w
+    const uint16_t* wpix = a.w + ((size_t)f * a.H * a.ntx + xt) * a.np * 128 + (size_t)q * 8;
+    const bool xin = x0 < a.W;
+    uint4 wn[RACC][2][2];
+    auto load_w = [&](int rg) {
+#pragma unroll
+      for (int r = 0; r < RACC; ++r) {
+        const int y = y0 + rg * RACC + r;
+        const bool ok = xin && y < a.H;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int cb = 2 * h + c;
+#pragma unroll
+          for (int k8 = 0; k8 < 2; ++k8) {
+            wn[r][c][k8] = make_uint4(0, 0, 0, 0);
+            if (ok && cb < nch)
+              wn[r][c][k8] = __ldg(reinterpret_cast<const uint4*>(wpix + (size_t)y * wrow + (size_t)(2 * cb + k8) * 1024));
+          }
+        }
+      }
+    };
+    load_w(0);
+    // last (r, c) with a chunk: the release point
+    const int c_last = (2 * h + 1 < nch) ? 1 : 0;
+    const bool has_any = 2 * h < nch;
+    uint64_t e_wait = 0, e_work = 0, e_rel = 0;
     for (int rg = 0; rg < n_rg; ++rg) {
-      uint64_t t0c = clk();
+      uint4 wc[RACC][2][2];
+#pragma unroll
+      for (int r = 0; r < RACC; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          wc[r][c][0] = wn[r][c][0];
+          wc[r][c][1] = wn[r][c][1];
+        }
+      const uint64_t t0c = clk();
       mbar_wait(tfull, rg & 1);
-      mbar_wait(wfull, rg & 1);
       tc_fence_after();
-      uint64_t t1c = clk();
+      const uint64_t t1c = clk();
       e_wait += t1c - t0c;
-      if (a.exp & 1) {
+      auto release = [&]() {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(wempty);
           if (PAIR)
             mbar_arrive_cluster(t_tempty_leader);
           else
             mbar_arrive(tempty);
         }
-        continue;
-      }
+        e_rel += clk() - t1c;
+      };
+      if (!has_any) release();
       float accs[RACC][C + 1];
 #pragma unroll
       for (int r = 0; r < RACC; ++r) {
-        const uint16_t* wr = wq + (size_t)r * a.np * 128;
 #pragma unroll
         for (int ch = 0; ch <= C; ++ch) accs[r][ch] = 0.f;
-        for (int cb = cb0; cb < cb1; ++cb) {
-          uint32_t v[C][16];
 #pragma unroll
-          for (int ch = 0; ch < C; ++ch) tmem_ld16_issue(tl + (ch * RACC + r) * kAccStride + cb * 16, v[ch]);
-          float wf[16];
+        for (int c = 0; c < 2; ++c) {
+          const int cb = 2 * h + c;
+          if (cb < nch) {
+            uint32_t v[C][16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) wf[i] = bf16_to_f(wr[(cb * 16 + i) * 128]);
-          if (a.normalize) {
+            for (int ch = 0; ch < C; ++ch) tmem_ld16_issue(tl + (ch * RACC + r) * kAccStride + cb * 16, v[ch]);
+            float wf[16];
+            {
+              const uint32_t* wp = reinterpret_cast<const uint32_t*>(&wc[r][c][0]);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) accs[r][C] = fmaf(wf[i], s_hsum[cb * 16 + i], accs[r][C]);
+              for (int i = 0; i < 8; ++i) {
+                wf[2 * i] = __uint_as_float(wp[i] << 16);
+                wf[2 * i + 1] = __uint_as_float(wp[i] & 0xFFFF0000u);
+              }
+            }
+            if (a.normalize) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) accs[r][C] = fmaf(wf[i], s_hsum[cb * 16 + i], accs[r][C]);
+            }
+            tmem_wait_ld();
+            if (r == RACC - 1 && c == c_last) release();
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch)
+#pragma unroll
+              for (int i = 0; i < 16; ++i) accs[r][ch] = fmaf(wf[i], __uint_as_float(v[ch][i]), accs[r][ch]);
           }
-          const uint64_t tl0 = clk();
-          tmem_wait_ld();
-          e_ld += clk() - tl0;
-#pragma unroll
-          for (int ch = 0; ch < C; ++ch)
-#pragma unroll
-            for (int i = 0; i < 16; ++i) accs[r][ch] = fmaf(wf[i], __uint_as_float(v[ch][i]), accs[r][ch]);
         }
       }
-      // TMEM and w of this group are consumed by this warp.  h = 0 releases them only after
-      // its barrier wait, so h = 1 cannot reach the next group's barrier arrive first.
-      auto release = [&]() {
-        e_rel += clk() - t1c;
-        if (a.trace && warp == 2 && lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
-          a.trace[rg * 8 + 5] = t1c - t_start;
-          a.trace[rg * 8 + 6] = clk() - t_start;
-        }
-        const uint64_t q0 = clk();
-        tc_fence_before();
-        __syncwarp();
-        const uint64_t q1 = clk();
-        uint64_t q2 = q1;
-        if (lane == 0) {
-          mbar_arrive(wempty);
-          q2 = clk();
-          if (PAIR)
-            mbar_arrive_cluster(t_tempty_leader);
-          else
-            mbar_arrive(tempty);
-        }
-        const uint64_t q3 = clk();
-        if (a.trace && lane == 0 && (warp == 2 || warp == 6) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
-          unsigned long long* q = a.trace + 1700 + (warp == 6 ? 3 * 64 : 0) + rg * 3;
-          q[0] = q1 - q0;
-          q[1] = q2 - q1;
-          q[2] = q3 - q2;
-        }
-        if (a.trace && lane == 0 && blockIdx.x < 2 && blockIdx.y == 0 && blockIdx.z == 0)
-          a.trace[512 + (blockIdx.x * 64 + rg) * 8 + (warp - 2)] = global_ns();
-      };
-      float* pb = part + (size_t)(rg & 1) * RACC * 128 * (C + 1);
-      if (h == 1) {
-        release();
+      if (rg + 1 < n_rg) load_w(rg + 1);
+      // parts 1-3 -> shared memory (double-buffered by group parity, one named barrier per
+      // parity so a fast part cannot complete the other group's barrier)
+      float* pb = part + (size_t)(rg & 1) * 3 * RACC * (C + 1) * 128;
+      const int bar_id = 1 + (rg & 1);
+      if (h != 0) {
 #pragma unroll
         for (int r = 0; r < RACC; ++r)
 #pragma unroll
-          for (int ch = 0; ch <= C; ++ch) pb[((size_t)r * (C + 1) + ch) * 128 + m] = accs[r][ch];
-        asm volatile("bar.arrive 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+          for (int ch = 0; ch <= C; ++ch) pb[(((size_t)(h - 1) * RACC + r) * (C + 1) + ch) * 128 + m] = accs[r][ch];
+        asm volatile("bar.arrive %0, %1;" ::"r"(bar_id), "n"(kEpiWarps * 32) : "memory");
       } else {
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-        release();
+        asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kEpiWarps * 32) : "memory");
 #pragma unroll
         for (int r = 0; r < RACC; ++r) {
           const int y = y0 + rg * RACC + r;
+#pragma unroll
+          for (int p3 = 0; p3 < 3; ++p3)
+#pragma unroll
+            for (int ch = 0; ch <= C; ++ch) accs[r][ch] += pb[(((size_t)p3 * RACC + r) * (C + 1) + ch) * 128 + m];
           if (y < a.H && x < a.W) {
-            const float g = accs[r][C] + pb[((size_t)r * (C + 1) + C) * 128 + m];
+            const float g = accs[r][C];
 #pragma unroll
             for (int ch = 0; ch < C; ++ch) {
-              float o = accs[r][ch] + pb[((size_t)r * (C + 1) + ch) * 128 + m];
+              float o = accs[r][ch];
               if (a.normalize) o = o / g;
               if (a.sigma != 0.f) {
                 const int64_t fr = a.frame0 + f;
@@ -480,12 +441,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     if (a.probe && warp == 2 && lane == 0) {
       atomicAdd(&a.probe[4], (unsigned long long)e_wait);
       atomicAdd(&a.probe[5], (unsigned long long)e_work);
-      atomicAdd(&a.probe[8], (unsigned long long)e_ld);
-      atomicAdd(&a.probe[9], (unsigned long long)e_rel);
-    }
-    if (a.probe && warp == 6 && lane == 0) {
-      atomicAdd(&a.probe[10], (unsigned long long)e_ld);
-      atomicAdd(&a.probe[11], (unsigned long long)e_rel);
+      atomicAdd(&a.probe[8], (unsigned long long)e_rel);
     }
   }
   tc_fence_before();
@@ -505,8 +461,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
 }
 
 template <bool SRC_F32, int C, int RACC, bool PAIR>
-static int launch_blur_t(const BlurArgs& a, const CUtensorMap& tw, const CUtensorMap& tb, dim3 grid, size_t sm,
-                         cudaStream_t s) {
+static int launch_blur_t(const BlurArgs& a, const CUtensorMap& tb, dim3 grid, size_t sm, cudaStream_t s) {
   auto kern = k_blur<SRC_F32, C, RACC, PAIR>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   cudaLaunchConfig_t cfg = {};
@@ -521,18 +476,17 @@ static int launch_blur_t(const BlurArgs& a, const CUtensorMap& tw, const CUtenso
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, a, tw, tb);
+  cudaLaunchKernelEx(&cfg, kern, a, tb);
   return (int)cudaGetLastError();
 }
 
 template <bool SRC_F32, bool PAIR>
-static int launch_blur_c(int C, const BlurArgs& a, const CUtensorMap& tw, const CUtensorMap& tb, dim3 grid,
-                         size_t sm, cudaStream_t s) {
+static int launch_blur_c(int C, const BlurArgs& a, const CUtensorMap& tb, dim3 grid, size_t sm, cudaStream_t s) {
   switch (C) {
-    case 1: return launch_blur_t<SRC_F32, 1, 4, PAIR>(a, tw, tb, grid, sm, s);
-    case 2: return launch_blur_t<SRC_F32, 2, 2, PAIR>(a, tw, tb, grid, sm, s);
-    case 3: return launch_blur_t<SRC_F32, 3, 1, PAIR>(a, tw, tb, grid, sm, s);
-    default: return launch_blur_t<SRC_F32, 4, 1, PAIR>(a, tw, tb, grid, sm, s);
+    case 1: return launch_blur_t<SRC_F32, 1, 4, PAIR>(a, tb, grid, sm, s);
+    case 2: return launch_blur_t<SRC_F32, 2, 2, PAIR>(a, tb, grid, sm, s);
+    case 3: return launch_blur_t<SRC_F32, 3, 1, PAIR>(a, tb, grid, sm, s);
+    default: return launch_blur_t<SRC_F32, 4, 1, PAIR>(a, tb, grid, sm, s);
   }
 }
 
@@ -542,6 +496,7 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   BlurArgs a;
   a.src = src;
   a.out = out;
+  a.w = p->d_w;
   a.bimg = g.bimg;
   a.adesc = g.adesc;
   a.idesc = umma_idesc_bf16(g.pair ? 256 : 128, g.np, true, false);
@@ -551,6 +506,7 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.bstride = g.bstride;
   a.H = p->H;
   a.W = p->W;
+  a.ntx = p->ntx;
   a.T = g.T;
   a.c = g.c;
   a.NC = g.NC;
@@ -565,15 +521,6 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.normalize = p->normalize;
   a.clamp01 = p->clamp01;
   a.probe = nullptr;
-  a.exp = getenv("P2S_BLUR_EXP") ? atoi(getenv("P2S_BLUR_EXP")) : 0;
-  static unsigned long long* trace = nullptr;
-  const bool want_trace = getenv("P2S_BLUR_TRACE") != nullptr;
-  a.trace = nullptr;
-  if (want_trace) {
-    if (!trace) cudaMalloc(&trace, 2400 * sizeof(unsigned long long));
-    cudaMemsetAsync(trace, 0, 2400 * sizeof(unsigned long long), s);
-    a.trace = trace;
-  }
   static unsigned long long* probe = nullptr;
   const bool want_probe = getenv("P2S_BLUR_PROBE") != nullptr;
   if (want_probe) {
@@ -587,37 +534,16 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   // TMEM: this kernel owns all 512 columns of its SM; keep shared memory above half the SM
   // so that two CTAs never co-reside and contend for tcgen05.alloc.
   size_t sm = L.total < 116 * 1024 ? 116 * 1024 : L.total;
-  int gx = (p->W + 127) / 128;
+  int gx = p->ntx;
   if (pair) gx = (gx + 1) / 2 * 2;  // whole CTA pairs; a trailing dummy CTA stores nothing
   dim3 grid(gx, (p->H + g.RB - 1) / g.RB, F);
   int rc;
   if (pair)
-    rc = src_f32 ? launch_blur_c<true, true>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s)
-                 : launch_blur_c<false, true>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s);
+    rc = src_f32 ? launch_blur_c<true, true>(p->C, a, p->tmap_b, grid, sm, s)
+                 : launch_blur_c<false, true>(p->C, a, p->tmap_b, grid, sm, s);
   else
-    rc = src_f32 ? launch_blur_c<true, false>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s)
-                 : launch_blur_c<false, false>(p->C, a, p->tmap_w, p->tmap_b, grid, sm, s);
-  if (want_trace) {  // debug: per-group timeline of CTA (0,0,0)
-    static unsigned long long h[2400];
-    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    fprintf(stderr, "[blur trace] rg: mma_wait_start tempty_ok issue_end full_wait (max@st) | epi tfull_ok release\n");
-    for (int rg = 0; rg < (a.RB + g.racc - 1) / g.racc && rg < 64; ++rg)
-      fprintf(stderr, "[blur trace] %2d: %8llu %8llu %8llu %6llu (%llu@%llu) | %8llu %8llu\n", rg, h[rg * 8], h[rg * 8 + 1],
-              h[rg * 8 + 2], h[rg * 8 + 3], h[rg * 8 + 4] % 100000ull, h[rg * 8 + 4] / 100000ull, h[rg * 8 + 5],
-              h[rg * 8 + 6]);
-    // release times (ns) of the 8 epilogue warps of both CTAs relative to the MMA warp's
-    // commit-of-tfull time of the same group (globaltimer)
-    for (int rg = 0; rg < 8; ++rg) {
-      fprintf(stderr, "[blur trace] rg %d release-ns after tfull commit: cta0", rg);
-      for (int w = 0; w < 8; ++w) fprintf(stderr, " %lld", (long long)(h[512 + rg * 8 + w] - h[1536 + rg]));
-      fprintf(stderr, " | cta1");
-      for (int w = 0; w < 8; ++w) fprintf(stderr, " %lld", (long long)(h[512 + (64 + rg) * 8 + w] - h[1536 + rg]));
-      fprintf(stderr, " | next tempty_ok %lld | cyc fence/arr_w/arr_t w2 %llu %llu %llu w6 %llu %llu %llu\n",
-              (long long)(h[1600 + rg + 1] - h[1536 + rg]), h[1700 + rg * 3], h[1701 + rg * 3], h[1702 + rg * 3],
-              h[1700 + 192 + rg * 3], h[1701 + 192 + rg * 3], h[1702 + 192 + rg * 3]);
-    }
-  }
+    rc = src_f32 ? launch_blur_c<true, false>(p->C, a, p->tmap_b, grid, sm, s)
+                 : launch_blur_c<false, false>(p->C, a, p->tmap_b, grid, sm, s);
   if (want_probe) {  // debug: per-CTA averages of the phase cycle counters
     unsigned long long h[12];
     cudaMemcpyAsync(h, probe, sizeof(h), cudaMemcpyDeviceToHost, s);
@@ -625,8 +551,8 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
     const double n = h[7] ? (double)h[7] : 1.0, nm = pair ? n / 2 : n;
     fprintf(stderr,
             "[blur probe] CTAs %llu  per CTA cycles: total %.0f prologue %.0f | MMA warp: loop %.0f wait_full %.0f "
-            "wait_tmem %.0f | epilogue warp: wait %.0f work %.0f (tmem_wait_ld %.0f, to release %.0f; h1: %.0f, %.0f)\n",
-            h[7], h[6] / n, h[0] / n, h[3] / nm, h[1] / nm, h[2] / nm, h[4] / n, h[5] / n, h[8] / n, h[9] / n, h[10] / n, h[11] / n);
+            "wait_tmem %.0f | epilogue warp 2: wait %.0f work %.0f (tfull to release %.0f)\n",
+            h[7], h[6] / n, h[0] / n, h[3] / nm, h[1] / nm, h[2] / nm, h[4] / n, h[5] / n, h[8] / n);
   }
   return rc;
 }

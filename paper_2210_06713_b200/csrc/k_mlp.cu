@@ -14,11 +14,14 @@
 //   layer 3: A2 [128 x n2] K-major, B = W3 image
 // Epilogues read TMEM with tcgen05.ld (32 lanes x 16 columns per warp), add bias,
 // ReLU, repack bf16 into the next layer's A operand; the last one writes the basis
-// weights w [F][n3][HWp] bf16 (k-major planes, fetched per row by the blur's 2-D TMA).
+// weights w as [F][H][ntx][n3/8][128 px][8] bf16: each 128-pixel row tile is one
+// contiguous block (one bulk store), and the blur epilogue thread of a pixel reads 8
+// consecutive bases with one 16-byte load.
 // Persistent grid, one CTA per SM holding the weight images once in shared memory and
 // running four independent 128-pixel tile pipelines (one per warpgroup, 128 TMEM columns
 // each), so the tensor core always has another warpgroup's GEMM to run while one
-// warpgroup is in an epilogue; the output tile leaves through one 2-D TMA store.
+// warpgroup is in an epilogue; the output tile leaves through one bulk copy.  Tiles are
+// 128-pixel segments of one image row (the blur's x-tiles).
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
@@ -28,11 +31,11 @@ namespace p2s {
 
 struct MlpArgs {
   const uint16_t* X;    // bf16 [F][nin][HW]
-  uint16_t* wout;       // bf16 [F][n3][HWp] (k-major planes)
+  uint16_t* wout;       // bf16 [F][H][ntx][n3/8][128][8]
   const uint8_t* blob;  // W1img | W2img | W3img | b1 | b2 | b3
   int nin, k1, n1, n2, n3;
   uint32_t off_w2, off_w3, off_b1, off_b2, off_b3, blob_bytes;
-  int HW, HWp, F, tiles_per_frame;
+  int HW, H, W, ntx, F, tiles_per_frame;
   int bias_folded;  // A1 column nin is the constant 1; biases live in the weight images
 };
 
@@ -83,24 +86,34 @@ __device__ __forceinline__ void wg_sync(int wg) {  // named barrier of one 128-t
   asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
 }
 
-// A1 tile (nin planes x 128 pixels, MN-major, k linear at 16 B) for pixel block pix0 of frame f.
-__device__ __forceinline__ void load_a1(const MlpArgs& a, uint8_t* A1, int f, int pix0, int ltid, bool async) {
+// A1 tile (nin planes x 128 pixels, MN-major, k linear at 16 B): pixels [pix0, pix0 + n) of
+// frame f (one row segment, n <= 128; the rest of the tile is zero).
+__device__ __forceinline__ void load_a1(const MlpArgs& a, uint8_t* A1, int f, int pix0, int n, int ltid, bool async) {
   const uint16_t* Xf = a.X + (size_t)f * a.nin * a.HW;
   for (int idx = ltid; idx < a.nin * 16; idx += 128) {
     const int k = idx % a.nin, g = idx / a.nin;
-    const int pix = pix0 + 8 * g;
-    const uint16_t* src = Xf + (size_t)k * a.HW + pix;
+    const int o = 8 * g;
+    const uint16_t* src = Xf + (size_t)k * a.HW + pix0 + o;
     uint8_t* dst = A1 + g * (a.k1 * 16) + k * 16;
-    if (async) {  // HW % 8 == 0: whole 16-byte chunks, zero-filled past the image
-      cp_async16(dst, pix < a.HW ? src : a.X, pix < a.HW ? 16u : 0u);
+    if (async) {  // W % 8 == 0: whole 16-byte chunks, zero-filled past the row segment
+      cp_async16(dst, o < n ? src : a.X, o < n ? 16u : 0u);
     } else {
       uint16_t t[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) t[e] = (pix + e < a.HW) ? src[e] : (uint16_t)0;
+      for (int e = 0; e < 8; ++e) t[e] = (o + e < n) ? src[e] : (uint16_t)0;
       *reinterpret_cast<uint4*>(dst) =
           make_uint4(t[0] | (t[1] << 16), t[2] | (t[3] << 16), t[4] | (t[5] << 16), t[6] | (t[7] << 16));
     }
   }
+}
+
+// Tile index -> (frame, first pixel, pixel count); tiles are 128-pixel segments of rows.
+__device__ __forceinline__ void tile_pixels(const MlpArgs& a, int tile, int& f, int& pix0, int& n) {
+  f = tile / a.tiles_per_frame;
+  const int r = tile - f * a.tiles_per_frame;
+  const int y = r / a.ntx, xt = r - y * a.ntx;
+  pix0 = y * a.W + xt * 128;
+  n = min(128, a.W - xt * 128);
 }
 
 constexpr int kMlpWG = 4;  // independent 128-pixel tile pipelines per CTA
@@ -109,7 +122,7 @@ constexpr int kMlpWG = 4;  // independent 128-pixel tile pipelines per CTA
 // columns, mbarrier), sharing one resident copy of the weight images; while one warpgroup
 // runs an epilogue the tensor core serves the others.
 __global__ void __launch_bounds__(128 * kMlpWG, 1)
-    k_mlp(const MlpArgs a, const __grid_constant__ CUtensorMap tmap_w) {
+    k_mlp(const MlpArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sw = smem;  // weight blob
   const uint32_t blob_al = (a.blob_bytes + 127) & ~127u;
@@ -166,18 +179,17 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
   const uint32_t id3 = umma_idesc_bf16(128, a.n3, false, false);
   uint32_t phase = 0;
   const int ntiles = a.F * a.tiles_per_frame;
-  const bool async = (a.HW % 8) == 0;
+  const bool async = (a.W % 8) == 0;
   const int stride = nwg * gridDim.x;
 
   int tile = nwg * blockIdx.x + wg;
   if (tile < ntiles) {
-    const int f = tile / a.tiles_per_frame;
-    load_a1(a, A1, f, (tile - f * a.tiles_per_frame) * 128, ltid, async);
+    int f, pix0, n;
+    tile_pixels(a, tile, f, pix0, n);
+    load_a1(a, A1, f, pix0, n, ltid, async);
   }
   cp_async_commit();
   for (; tile < ntiles; tile += stride) {
-    const int f = tile / a.tiles_per_frame;
-    const int pix0 = (tile - f * a.tiles_per_frame) * 128;
     cp_async_wait<0>();  // this tile's A1 (issued during the previous tile's layers 2-3)
     fence_async_smem();
     tc_fence_before();
@@ -197,8 +209,9 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     {  // A1 is free once layer 1 has completed: prefetch the next tile's inputs
       const int nxt = tile + stride;
       if (nxt < ntiles) {
-        const int fn = nxt / a.tiles_per_frame;
-        load_a1(a, A1, fn, (nxt - fn * a.tiles_per_frame) * 128, ltid, async);
+        int fn, pn, nn;
+        tile_pixels(a, nxt, fn, pn, nn);
+        load_a1(a, A1, fn, pn, nn, ltid, async);
       }
       cp_async_commit();
     }
@@ -238,17 +251,15 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    // w tile -> A2 as [n3][128 px] bf16, then one 2-D TMA store into the k-major planes.
-    // Lanes 2i and 2i+1 (adjacent pixels) swap halves of their 16-value chunk so each
-    // writes one 32-bit word (2 pixels) per basis row: 8 stores per chunk instead of 16.
+    // w tile -> A2 as [n3/8][128 px][8] bf16 (16-byte stores, consecutive lanes adjacent),
+    // then one bulk copy of the whole tile.
     {
-      uint32_t* st = reinterpret_cast<uint32_t*>(A2) + (m >> 1);
-      const bool odd = lane & 1;
+      uint4* st = reinterpret_cast<uint4*>(A2) + m;
       for (int c0 = 0; c0 < a.n3; c0 += 16) {
         uint32_t r[16];
         tmem_ld16_issue(taddr + c0, r);
         tmem_wait_ld();
-        uint32_t pk[8];  // pack (value i, value i+1) -> bf16x2 of this pixel
+        uint32_t pk[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           float v0 = __uint_as_float(r[2 * i]), v1 = __uint_as_float(r[2 * i + 1]);
@@ -258,20 +269,15 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
           }
           pk[i] = pack_bf16x2(v0, v1);
         }
-        // even lane keeps rows c0+2i (its low halves) and receives the neighbour's low halves;
-        // odd lane keeps rows c0+2i+1 (high halves) and receives the neighbour's high halves
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t other = __shfl_xor_sync(0xffffffffu, pk[i], 1);
-          const uint32_t word = odd ? __byte_perm(other, pk[i], 0x7632) : __byte_perm(pk[i], other, 0x5410);
-          st[(c0 + 2 * i + (odd ? 1 : 0)) * 64] = word;
-        }
+        st[(c0 / 8) * 128] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        st[(c0 / 8 + 1) * 128] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
     }
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
-    if (ltid == 0) tma_store_2d(&tmap_w, pix0, f * a.n3, A2);
+    // tile index == (f * H + y) * ntx + xt: the output block of this row tile
+    if (ltid == 0) bulk_s2g(a.wout + (size_t)tile * a.n3 * 128, A2, (uint32_t)a.n3 * 256);
   }
   if (ltid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
@@ -298,10 +304,12 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   a.off_b3 = (uint32_t)g.off_b3;
   a.blob_bytes = (uint32_t)g.blob_bytes;
   a.HW = p->H * p->W;
-  a.HWp = p->HWp;
+  a.H = p->H;
+  a.W = p->W;
+  a.ntx = p->ntx;
   a.bias_folded = g.bias_folded ? 1 : 0;
   a.F = F;
-  a.tiles_per_frame = (a.HW + 127) / 128;
+  a.tiles_per_frame = p->H * p->ntx;
   const int nmax = std::max(std::max(g.n1, g.n2), g.n3);
   const int cols_wg = nmax <= 32 ? 32 : nmax <= 64 ? 64 : nmax <= 128 ? 128 : 256;
   const size_t blob_al = (g.blob_bytes + 127) & ~(size_t)127;
@@ -313,7 +321,7 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   const int ntiles = F * a.tiles_per_frame;
   int grid = p->num_sms;  // persistent: one CTA (nwg tile pipelines) per SM
   if (nwg * grid > ntiles) grid = (ntiles + nwg - 1) / nwg;
-  k_mlp<<<grid, 128 * nwg, sm, s>>>(a, p->tmap_w);
+  k_mlp<<<grid, 128 * nwg, sm, s>>>(a);
   return (int)cudaGetLastError();
 }
 

@@ -230,6 +230,13 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, int c0, int c1, c
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// 1-D bulk copy shared -> global (TMA engine), committed as its own bulk group.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 __device__ __forceinline__ void tma_store_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }

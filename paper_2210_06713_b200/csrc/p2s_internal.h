@@ -104,9 +104,8 @@ struct p2s_plan_s {
   uint16_t* d_X = nullptr;      // bf16 [mb][nslots][H*W] (simulate) / [mb][Z-3][H*W] (blur API)
   float* d_tilt = nullptr;      // [mb][2][H*W]
   uint16_t* d_Iw = nullptr;     // bf16 [mb][C][H][W]
-  uint16_t* d_w = nullptr;      // bf16 [mb][n3][HWp] (k-major planes)
-  int HWp = 0;                  // plane stride of d_w (H*W rounded up to 8)
-  CUtensorMap tmap_w;           // 2-D TMA view of d_w: [mb*n3 rows][HWp], box 128 x n3
+  uint16_t* d_w = nullptr;      // bf16 [mb][H][ntx][n3/8][128 px][8]: per 128-pixel row tile, 8-basis chunks
+  int ntx = 0;                  // 128-pixel tiles per image row
   CUtensorMap tmap_b;           // 2-D TMA view of bg.bimg2: rows of 256 B, box 2 K-steps of one half
   float* d_img = nullptr;       // staging for the host entry point [mb][C][H][W]
   float* d_out = nullptr;       // staging for the host entry point [mb][C][H][W]
