@@ -93,6 +93,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# Step 5 (reading Q16) runs with additive sensor noise (Philox, sigma below) and the clamp
+# to [0, 1].  PSF-sum normalisation stays off: with random-init P2S weights the sum
+# g = sum_k w_k is zero-mean-ish (|g| < 0.01 at ~3% of pixels), so dividing by it is
+# ill-conditioned; it is exercised by tests/test_gpu_parity.py::test_simulate_step5_vs_oracle.
+STEP5 = dict(noise_sigma=0.01, normalize_psf_sum=False, clamp01=True)
+
 WORKLOADS = {
     # BASELINE.json configs[2]: the metric's 512x512 RGB headline, fits one GPU
     "cfg3_512": dict(H=512, W=512, C=3, F=64, d_over_r0=3.0, K=100, T=33, ar_alpha=0.0,
@@ -153,7 +159,8 @@ def oracle_sample(w, n_blur_px=2048, seed=SEED, frame=0):
     xs = rng.integers(0, W, n_blur_px)
     pipeline.blur_at(Iw, wts[:, ys, xs].T, basis, ys, xs)
     t2 = time.perf_counter()
-    pipeline.step5(np.zeros((C, H, W)), wts, basis, seed, frame, sigma=0.0)
+    pipeline.step5(np.zeros((C, H, W)), wts, basis, seed, frame, sigma=STEP5["noise_sigma"],
+                   normalize=STEP5["normalize_psf_sum"], clamp01=STEP5["clamp01"])
     t3 = time.perf_counter()
     frame_s = (t1 - t0) + (t2 - t1) * (H * W / n_blur_px) + (t3 - t2)
     desc = (f"oracle (fp64 numpy) steps 1-3+5 on one full {H}x{W}x{C} frame, Eq.9 blur on {n_blur_px} "
@@ -194,6 +201,7 @@ def config_dict(w, args, world):
     return {"workload": f"{args.workload}: {w['desc']}", "H": w["H"], "W": w["W"], "C": w["C"],
             "frames_per_gpu_per_step": w["F"], "global_batch": w["F"] * world, "d_over_r0": w["d_over_r0"],
             "Z": 36, "K": w["K"], "T": w["T"], "mlp": f"33-100-100-{w['K']}", "ar_alpha": w["ar_alpha"],
+            "step5": "noise sigma={noise_sigma} + clamp01 (normalisation off: random-init weights)".format(**STEP5),
             "parallelism": f"frames dp{world}", "l2": "no flush: per-step working set "
             "(spectrum + fields + weights, GBs) far exceeds the 126 MB L2"}
 
@@ -231,7 +239,7 @@ def main():
     mlp = synth.mlp_weights(K, seed=0)
     img_np = synth.image(H, W, C, seed=0)
     plan = Plan(PlanConfig(H=H, W=W, C=C, d_over_r0=w["d_over_r0"], K=K, taps=T, ar_alpha=w["ar_alpha"],
-                           max_batch=F, device=local), basis, mlp)
+                           max_batch=F, device=local, **STEP5), basis, mlp)
     dev = torch.device("cuda", local)
     img = torch.from_numpy(img_np).to(dev)
     out = torch.empty((F, C, H, W), device=dev)

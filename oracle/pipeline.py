@@ -210,6 +210,24 @@ def step5(out, w, basis, seed, frame, sigma=0.0, normalize=False, clamp01=False)
     return out
 
 
+def step5_at(out_at, w_at, basis, seed, frame, ys, xs, W, sigma=0.0, normalize=False, clamp01=False):
+    """step5 evaluated at sample pixels only: out_at [C][n] (Eq.9 at (ys, xs)), w_at [n][K].
+    Same arithmetic as step5 (reading Q16) with the pixel index y*W + x as noise counter."""
+    out = np.array(out_at, dtype=np.float64)
+    C = out.shape[0]
+    if normalize:
+        g = np.asarray(w_at, dtype=np.float64) @ basis.reshape(basis.shape[0], -1).astype(np.float64).sum(1)
+        out = out / g[None]
+    if sigma != 0.0:
+        idx = np.asarray(ys) * W + np.asarray(xs)
+        for ch in range(C):
+            (g1, _), _ = gaussians(idx, ch, STREAM_OUTPUT_NOISE, frame, seed)
+            out[ch] = out[ch] + sigma * g1
+    if clamp01:
+        out = np.clip(out, 0.0, 1.0)
+    return out
+
+
 def simulate(img, img_frame_stride_is_zero, seed, frame0, F, sqrtS, L, basis, layers, kappa,
              alpha=0.0, sigma=0.0, normalize=False, clamp01=False, return_intermediates=False):
     """Steps 1-5 for frames frame0 .. frame0+F-1.  img is [F|1][C][H][W]."""

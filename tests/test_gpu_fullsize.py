@@ -31,9 +31,12 @@ def _plan(H, W, C, dr0, K, T, **kw):
 
 
 def test_512_rgb_bench_config_vs_oracle_sampled():
+    """bench.py's workload and step-5 configuration (noise sigma, clamp)."""
+    import bench
     H = W = 512
     C, K, T, dr0, F = 3, 100, 33, 3.0, 2
-    plan, basis, mlp = _plan(H, W, C, dr0, K, T, max_batch=64)
+    st5 = bench.STEP5
+    plan, basis, mlp = _plan(H, W, C, dr0, K, T, max_batch=64, **st5)
     s_px, kappa = optics.geometry()
     sq, _ = correlation.sqrt_psd_tables(H, W, s_px, 36)
     plan.import_sqrtS(sq)
@@ -56,7 +59,9 @@ def test_512_rgb_bench_config_vs_oracle_sampled():
         assert worst <= 1e-4, worst
         Iw = pipeline.warp(img, a[1], a[2], kappa)
         w_at = pipeline.mlp(a[3:, ys, xs][:, :, None], layers)[:, :, 0].T
-        ref = pipeline.blur_at(Iw, w_at, basis, ys, xs)
+        ref = pipeline.step5_at(pipeline.blur_at(Iw, w_at, basis, ys, xs), w_at, basis, SEED, 7 + f, ys, xs, W,
+                                sigma=st5["noise_sigma"], normalize=st5["normalize_psf_sum"],
+                                clamp01=st5["clamp01"])
         for c in range(C):
             assert rel_l2(got[f, c, ys, xs], ref[c]) <= 2e-2
 

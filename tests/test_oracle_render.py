@@ -146,6 +146,20 @@ def test_step5_normalise_noise_clamp():
     assert cl.min() >= 0 and cl.max() <= 1
 
 
+def test_step5_at_sampled_pixels_equals_full_frame():
+    """step5_at (used at full sizes) evaluated at sample pixels equals step5 on the frame."""
+    K, T, H, W = 4, 5, 30, 44
+    h = synth.basis(K, T, seed=2).astype(np.float64)
+    rng = np.random.default_rng(9)
+    w = rng.uniform(-0.2, 1.0, (K, H, W))
+    out = rng.uniform(-0.5, 1.5, (3, H, W))
+    ys, xs = rng.integers(0, H, 50), rng.integers(0, W, 50)
+    for kw in (dict(sigma=0.05), dict(normalize=True, clamp01=True), dict(sigma=0.1, normalize=True, clamp01=True)):
+        full = pipeline.step5(out, w, h, 17, 4, **kw)
+        at = pipeline.step5_at(out[:, ys, xs], w[:, ys, xs].T, h, 17, 4, ys, xs, W, **kw)
+        assert np.allclose(at, full[:, ys, xs], rtol=0, atol=1e-12)
+
+
 # ------------------------------------------------------------------ end to end
 def _small_plan(H, W, N=36, d_over_r0=2.0, s_px=0.02625):
     A0 = optics.noll_covariance(N, d_over_r0)
