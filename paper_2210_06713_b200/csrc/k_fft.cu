@@ -216,6 +216,28 @@ __device__ __forceinline__ void reg_pass(float2 (&v)[8], int j, const float2* __
   }
   dft_inv<8>(v);
 }
+// Per-pass twiddle table (same values as tw[r * k * N / (8 NS)]) laid out [r-1][k] so that
+// consecutive butterflies read consecutive entries (no bank conflicts): NS = 8 at offset 0
+// (7 x 8 entries), NS = 64 at offset 56 (7 x 64 entries); 504 entries in all.
+template <int NS>
+__device__ __forceinline__ constexpr int twp_base() { return NS == 8 ? 0 : 56; }
+__device__ __forceinline__ void build_twp(float2* __restrict__ twp, const float2* __restrict__ tw, int tid, int nt) {
+  for (int i = tid; i < 504; i += nt) {
+    const bool second = i >= 56;
+    const int ns = second ? 64 : 8, o = second ? i - 56 : i;
+    const int r = 1 + o / ns, k = o % ns;
+    twp[i] = __ldg(&tw[r * k * (kRegN / (8 * ns))]);
+  }
+}
+template <int NS>
+__device__ __forceinline__ void reg_pass_t(float2 (&v)[8], int j, const float2* __restrict__ twp) {
+  if (NS > 1) {
+    const int k = j & (NS - 1);
+#pragma unroll
+    for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], twp[twp_base<NS>() + (r - 1) * NS + k]);
+  }
+  dft_inv<8>(v);
+}
 // Stockham output position of point r of butterfly j after the pass with span NS.
 template <int NS>
 __device__ __forceinline__ int reg_out(int j, int r) {
@@ -305,17 +327,17 @@ __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
 // owns butterfly t of row ky and butterfly (64 - t) % 64 of row P - ky, which holds exactly
 // the mirror bins of its own: one Philox draw feeds both (the mirror takes the conjugate).
 template <int NG>
-__global__ void __launch_bounds__(64 * NG) k_rows_pair512(RowArgs a) {
+__global__ void __launch_bounds__(64 * NG, 3) k_rows_pair512(RowArgs a) {
   constexpr int N = kRegN, B = kRegB, XL = N + N / 8;
   extern __shared__ __align__(16) unsigned char smem[];
-  float2* tw = reinterpret_cast<float2*>(smem);  // [N]
+  float2* tw = reinterpret_cast<float2*>(smem);  // [N] per-pass twiddle table (build_twp)
   float2* sS = tw + N;                           // [2][N] sqrt(S) of both rows
   float2* xb = sS + 2 * N;                       // [NG][2][XL] exchange buffers
   const int ky = blockIdx.x, p = blockIdx.y;
   const int k1 = ky ? a.P - ky : 0;
   const size_t plane = (size_t)p * a.P * N;
+  build_twp(tw, a.fq.tw, threadIdx.x, 64 * NG);
   for (int i = threadIdx.x; i < N; i += 64 * NG) {
-    tw[i] = __ldg(&a.fq.tw[i]);
     sS[i] = __ldg(&a.sqrtS[plane + (size_t)ky * N + i]);
     sS[N + i] = __ldg(&a.sqrtS[plane + (size_t)k1 * N + i]);
   }
@@ -341,8 +363,8 @@ __global__ void __launch_bounds__(64 * NG) k_rows_pair512(RowArgs a) {
       else
         w[(8 - r) & 7] = spectrum(sS[N + B * ((8 - r) & 7)], zc);
     }
-    reg_pass<1>(u, t, tw);
-    reg_pass<1>(w, tm, tw);
+    reg_pass_t<1>(u, t, tw);
+    reg_pass_t<1>(w, tm, tw);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       x0[xi(reg_out<1>(t, r))] = u[r];
@@ -355,8 +377,8 @@ __global__ void __launch_bounds__(64 * NG) k_rows_pair512(RowArgs a) {
       w[r] = x1[xi(tm + B * r)];
     }
     gsync();
-    reg_pass<8>(u, t, tw);
-    reg_pass<8>(w, tm, tw);
+    reg_pass_t<8>(u, t, tw);
+    reg_pass_t<8>(w, tm, tw);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       x0[xi(reg_out<8>(t, r))] = u[r];
@@ -369,8 +391,8 @@ __global__ void __launch_bounds__(64 * NG) k_rows_pair512(RowArgs a) {
       w[r] = x1[xi(tm + B * r)];
     }
     gsync();
-    reg_pass<64>(u, t, tw);
-    reg_pass<64>(w, tm, tw);
+    reg_pass_t<64>(u, t, tw);
+    reg_pass_t<64>(w, tm, tw);
     float2* dst = a.Zout + (size_t)fi * a.npairs * a.P * N + plane;
 #pragma unroll
     for (int r = 0; r < 8; ++r) dst[(size_t)ky * N + t + B * r] = u[r];
