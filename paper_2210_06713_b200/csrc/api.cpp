@@ -162,7 +162,7 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   g.stages = se ? std::max(2, std::min(12, atoi(se))) : (g.pair ? 4 : 3);
   g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, g.nks, p->H, g.pair, g.stages);
   g.RS = g.RB + 8 * G;
-  const uint32_t sbo = (uint32_t)g.RS * 16;
+  const uint32_t sbo = (uint32_t)blur_rs_pad(g.RS) * 16;
   struct Grp { int tx, gi; uint32_t off; };
   std::vector<Grp> groups;
   for (int tx = T - 1; tx >= 0; --tx)

@@ -32,7 +32,6 @@
 
 namespace p2s {
 
-constexpr int kMaxStages = 12;
 constexpr int kStepsPerStage = kBlurStepsPerStage;  // K-steps (B tiles) moved per ring stage
 constexpr int kEpiWarps = 16;      // four warps per TMEM lane quarter, each owning two 16-basis chunks
 constexpr int kBlurThreads = 64 + 32 * kEpiWarps;  // warp 0 TMA producer, warp 1 MMA issuer, epilogue
@@ -84,7 +83,7 @@ struct BlurSmem {
 __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int racc, int np, int nks, bool pair,
                                                      int stages) {
   BlurSmem L;
-  L.tile_bytes = ((uint32_t)NC * RS * 16 + 127) & ~127u;
+  L.tile_bytes = ((uint32_t)NC * blur_rs_pad(RS) * 16 + 127) & ~127u;
   L.b_bytes = (uint32_t)np * 32 / (pair ? 2 : 1);  // per K-step: this CTA's rows of B
   L.ring_bytes = stages * kStepsPerStage * L.b_bytes;
   const uint32_t stg_bytes = (kBlurThreads / 32) * kLoadRows * kSeg * 2;  // the loader's staging (bf16)
@@ -104,7 +103,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const BlurSmem L = blur_smem_layout(C, a.NC, a.RS, RACC, a.np, a.nks, PAIR, a.stages);
   const int kBlurStages = a.stages;
-  const uint32_t sbo_src = (uint32_t)a.RS * 16;
+  const uint32_t sbo_src = (uint32_t)blur_rs_pad(a.RS) * 16;
   uint8_t* ring = smem + L.off_ring;
   float* s_hsum = reinterpret_cast<float*>(smem + L.off_hsum);
   uint64_t* s_adesc = reinterpret_cast<uint64_t*>(smem + L.off_desc);
@@ -140,7 +139,8 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       tmem_alloc(tslot, 512);
   }
 
-  // ---- source tiles of every channel: chunk cc of row rl holds the 8 pixels at window
+  {
+    // ---- source tiles of every channel: chunk cc of row rl holds the 8 pixels at window
   // offsets cc + 16 j of source row y0 - c + rl (mirror boundary).  Each warp stages
   // kLoadRows row segments (bf16, all loads in flight together) in the not-yet-used B ring,
   // then packs the chunks.
@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
         __syncwarp();
       }
     }
+  }
   }
   fence_async_smem();
   tc_fence_before();

@@ -53,6 +53,12 @@ struct MlpGeom {
 #define P2S_KSPS 4
 #endif
 constexpr int kBlurStepsPerStage = P2S_KSPS;
+// Height (in 16-byte rows) of one chunk column of the blur's source tile: RS rounded up to
+// odd, so that the 16-byte stores of consecutive chunk columns fall in different banks.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline constexpr int blur_rs_pad(int RS) { return RS | 1; }
 
 struct BlurGeom {
   int T = 0, c = 0;        // taps, centre
