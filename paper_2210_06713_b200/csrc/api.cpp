@@ -329,6 +329,11 @@ static void free_plan(p2s_plan_s* p) {
   cudaFree(p->d_mlp_plain);
   cudaFree(p->bg.bimg);
   cudaFree(p->bg.bimg2);
+  if (p->copy_stream) {
+    cudaStreamDestroy(p->copy_stream);
+    cudaEventDestroy(p->ev_sub);
+    cudaEventDestroy(p->ev_copied);
+  }
   cudaFree(p->bg.koff);
   cudaFree(p->bg.adesc);
   cudaFree(p->bg.klbo);
@@ -662,8 +667,18 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
   DeviceGuard guard(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t img_floats = (size_t)p->C * p->H * p->W;
+  if (!p->copy_stream) {
+    P2S_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    P2S_CUDA(cudaEventCreateWithFlags(&p->ev_sub, cudaEventDisableTiming), "cudaEventCreate");
+    P2S_CUDA(cudaEventCreateWithFlags(&p->ev_copied, cudaEventDisableTiming), "cudaEventCreate");
+  }
+  // The device->host copy of each sub-batch runs on a second stream while the next
+  // sub-batch computes, so the PCIe transfer of the outputs hides behind the kernels.
+  const int sub = std::max(1, std::min(p->max_batch, 8));
+  bool pending = false;
   for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
     const int F = std::min(p->max_batch, nframes - i0);
+    if (pending) P2S_CUDA(cudaStreamWaitEvent(s, p->ev_copied, 0), "wait copies");  // d_out / d_img reuse
     if (img_frame_stride == 0) {
       P2S_CUDA(cudaMemcpyAsync(p->d_img, img_host, img_floats * 4, cudaMemcpyHostToDevice, s), "H2D img");
     } else {
@@ -672,13 +687,22 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
                                  img_floats * 4, cudaMemcpyHostToDevice, s),
                  "H2D img");
     }
-    p2s_status st = p2s_simulate_frames(p, p->d_img, img_frame_stride ? (int64_t)img_floats : 0, seed,
-                                        frame0 + i0, F, p->d_out, stream);
-    if (st != P2S_OK) return st;
-    P2S_CUDA(cudaMemcpyAsync(out_host + (size_t)i0 * img_floats, p->d_out, (size_t)F * img_floats * 4,
-                             cudaMemcpyDeviceToHost, s),
-             "D2H out");
+    for (int j0 = 0; j0 < F; j0 += sub) {
+      const int Fs = std::min(sub, F - j0);
+      p2s_status st = p2s_simulate_frames(p, p->d_img + (img_frame_stride ? (size_t)j0 * img_floats : 0),
+                                          img_frame_stride ? (int64_t)img_floats : 0, seed, frame0 + i0 + j0, Fs,
+                                          p->d_out + (size_t)j0 * img_floats, stream);
+      if (st != P2S_OK) return st;
+      P2S_CUDA(cudaEventRecord(p->ev_sub, s), "event record");
+      P2S_CUDA(cudaStreamWaitEvent(p->copy_stream, p->ev_sub, 0), "wait sub-batch");
+      P2S_CUDA(cudaMemcpyAsync(out_host + (size_t)(i0 + j0) * img_floats, p->d_out + (size_t)j0 * img_floats,
+                               (size_t)Fs * img_floats * 4, cudaMemcpyDeviceToHost, p->copy_stream),
+               "D2H out");
+    }
+    P2S_CUDA(cudaEventRecord(p->ev_copied, p->copy_stream), "event record");
+    pending = true;
   }
+  P2S_CUDA(cudaStreamSynchronize(p->copy_stream), "copy stream sync");
   P2S_CUDA(cudaStreamSynchronize(s), "stream sync");
   return P2S_OK;
 }
