@@ -165,6 +165,19 @@ p2s_status p2s_plan_stage_times(p2s_plan p, double* ms, int64_t* launches);
 /* Replace the plan's sqrt(S_j) (host float [Z-1][P][Q], same layout as export). */
 p2s_status p2s_plan_import_sqrtS(p2s_plan p, const float* sqrtS);
 
+/* Validation battery: empirical spatial auto-correlation of sampled
+ * Zernike coefficient fields, the statistic the sampler is built to reproduce (homogeneous
+ * A_jj(s); mixed model E[a_j(x) a_j(x+s)] = sum_k L_jk^2 c_k(s), Eq.10
+ * P:318-330; tilt j = 2, 3 and the differential tilt variance 2(A_22(0) - A_22(s)),
+ * P:523-532).
+ *   zern  : device float [nframes][Z][H][W] (the p2s_sample_zernike layout of this plan).
+ *   out   : device double [Z][2][max_lag]; out[j][0][l] = mean a_j(y,x) a_j(y,(x+l) mod W),
+ *           out[j][1][l] = mean a_j(y,x) a_j((y+l) mod H,x), over all frames and pixels
+ *           (periodic lags: the fields are periodic when the FFT grid equals the image).
+ *   max_lag in [1, 64].  Stream-ordered; a temporary partial-sum buffer is allocated and
+ *   freed on the stream.  Errors: P2S_ERR_INVALID_ARGUMENT for bad sizes / NULL. */
+p2s_status p2s_field_autocorr(p2s_plan p, const float* zern, int nframes, int max_lag, double* out, void* stream);
+
 /* Device Philox4x32-10 test fill: out (dev uint32 [n][4]) <- philox(counter =
  * (i, c1, c2, c3), key = (k0, k1)) for i = 0..n-1. */
 p2s_status p2s_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,

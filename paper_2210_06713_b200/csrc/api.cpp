@@ -707,6 +707,22 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
   return P2S_OK;
 }
 
+extern "C" p2s_status p2s_field_autocorr(p2s_plan p, const float* zern, int nframes, int max_lag, double* out,
+                                         void* stream) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (!zern || !out) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (nframes < 1 || max_lag < 1 || max_lag > 64 || max_lag > p->H || max_lag > p->W)
+    return set_error(P2S_ERR_INVALID_ARGUMENT, "nframes >= 1 and 1 <= max_lag <= min(64, H, W) required");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  double* partial = nullptr;
+  P2S_CUDA(cudaMallocAsync(&partial, acorr_partial_bytes(nframes, p->Z, p->W, max_lag), s), "cudaMallocAsync");
+  const int rc = launch_acorr(zern, nframes, p->Z, p->H, p->W, max_lag, partial, out, s);
+  cudaFreeAsync(partial, s);
+  if (rc != 0) return set_error(P2S_ERR_CUDA, std::string("k_acorr: ") + cudaGetErrorString((cudaError_t)rc));
+  return P2S_OK;
+}
+
 extern "C" p2s_status p2s_plan_info(p2s_plan p, int* P, int* Q, size_t* ws, double* clamped, int* max_batch) {
   if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
   if (P) *P = p->P;

@@ -142,6 +142,8 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s);
 int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0,
                 float* out, cudaStream_t s);
 int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair, int stages);
+size_t acorr_partial_bytes(int F, int Z, int W, int L);
+int launch_acorr(const float* zern, int F, int Z, int H, int W, int L, double* partial, double* out, cudaStream_t s);
 int launch_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int64_t n, uint32_t* out,
                        cudaStream_t s);
 }  // namespace p2s
