@@ -116,6 +116,13 @@ __device__ __forceinline__ void tile_pixels(const MlpArgs& a, int tile, int& f, 
   n = min(128, a.W - xt * 128);
 }
 
+// One layer GEMM: nsteps K-steps of 16; descriptors advance by 256 bytes (16 in the
+// 16-byte-unit address field) per step, so the issuing thread does one add per operand.
+__device__ __forceinline__ void mlp_issue_layer(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, int nsteps) {
+#pragma unroll 8
+  for (int s = 0; s < nsteps; ++s) umma_bf16(tmem, da + (uint64_t)(16 * s), db + (uint64_t)(16 * s), idesc, s > 0);
+}
+
 constexpr int kMlpWG = 4;  // independent 128-pixel tile pipelines per CTA
 
 // kMlpWG warpgroups per CTA, each an independent tile pipeline (own A1, A2, 128 TMEM
@@ -174,6 +181,9 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
   const float* b3 = reinterpret_cast<const float*>(sw + a.off_b3);
   const uint32_t sA1 = smem_u32(A1), sA2 = smem_u32(A2);
   const uint32_t sW1 = smem_u32(sw), sW2 = smem_u32(sw + a.off_w2), sW3 = smem_u32(sw + a.off_w3);
+  const uint64_t dA1 = umma_desc(sA1, 128, a.k1 * 16), dW1 = umma_desc(sW1, 128, (a.k1 / 8) * 128);
+  const uint64_t dA2a = umma_desc(sA2, 128, (a.n1 / 8) * 128), dW2 = umma_desc(sW2, 128, (a.n1 / 8) * 128);
+  const uint64_t dA2b = umma_desc(sA2, 128, (a.n2 / 8) * 128), dW3 = umma_desc(sW3, 128, (a.n2 / 8) * 128);
   const uint32_t id1 = umma_idesc_bf16(128, a.n1, true, false);
   const uint32_t id2 = umma_idesc_bf16(128, a.n2, false, false);
   const uint32_t id3 = umma_idesc_bf16(128, a.n3, false, false);
@@ -198,9 +208,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     if (ltid == 0) {
       tma_store_wait_read();  // the previous tile's w store has finished reading A2
       tc_fence_after();
-      for (int s = 0; s < a.k1 / 16; ++s)
-        umma_bf16(tmem, umma_desc(sA1 + s * 256, 128, a.k1 * 16), umma_desc(sW1 + s * 256, 128, (a.k1 / 8) * 128),
-                  id1, s > 0);
+      mlp_issue_layer(tmem, dA1, dW1, id1, a.k1 / 16);
       umma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -225,9 +233,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     // ---- layer 2
     if (ltid == 0) {
       tc_fence_after();
-      for (int s = 0; s < a.n1 / 16; ++s)
-        umma_bf16(tmem, umma_desc(sA2 + s * 256, 128, (a.n1 / 8) * 128),
-                  umma_desc(sW2 + s * 256, 128, (a.n1 / 8) * 128), id2, s > 0);
+      mlp_issue_layer(tmem, dA2a, dW2, id2, a.n1 / 16);
       umma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -243,9 +249,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     // ---- layer 3
     if (ltid == 0) {
       tc_fence_after();
-      for (int s = 0; s < a.n2 / 16; ++s)
-        umma_bf16(tmem, umma_desc(sA2 + s * 256, 128, (a.n2 / 8) * 128),
-                  umma_desc(sW3 + s * 256, 128, (a.n2 / 8) * 128), id3, s > 0);
+      mlp_issue_layer(tmem, dA2b, dW3, id3, a.n2 / 16);
       umma_commit(bar);
     }
     mbar_wait(bar, phase);
