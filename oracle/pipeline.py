@@ -68,9 +68,38 @@ def white_spectral_noise(seed: int, frame: int, P: int, Q: int, N: int = N_MODES
     return eta
 
 
+def flow_phase_1d(n: int, s: float) -> np.ndarray:
+    """Shift factor of one axis for a translation by s pixels (reading Q23): bin k gets
+    exp(-2 pi i f_k s) with the signed frequency f_k = k/n (k < n/2), (k-n)/n (k > n/2);
+    the Nyquist bin k = n/2 (its own mirror) gets the real cos(pi s), so the shifted
+    spectrum stays Hermitian and the fields stay real.  For integer s this is exactly
+    the periodic roll by s."""
+    k = np.arange(n)
+    ks = np.where(k <= n // 2, k, k - n).astype(np.float64)
+    ph = np.exp(-2j * np.pi * ks * s / n)
+    if n % 2 == 0:
+        ph[n // 2] = np.cos(np.pi * s)
+    return ph
+
+
+def frozen_flow_noise(seed: int, t: int, P: int, Q: int, flow, N: int = N_MODES) -> np.ndarray:
+    """Frozen flow: the coefficient fields of frame t are the frame-0 fields
+    translated by t * (vx, vy) pixels, a(x, t) = a(x - v t, 0), on the periodic grid.  In
+    the spectral domain that is the frame-0 noise times the per-axis shift factors."""
+    vx, vy = flow
+    eta = white_spectral_noise(seed, 0, P, Q, N)
+    ph = np.outer(flow_phase_1d(P, vy * t), flow_phase_1d(Q, vx * t))
+    return eta * ph[None]
+
+
 def spectral_noise_sequence(seed: int, frame0: int, F: int, P: int, Q: int,
-                            alpha: float = 0.0, N: int = N_MODES):
-    """eta_t for t = frame0 .. frame0+F-1 (AR(1) replayed from t = 0 if alpha != 0)."""
+                            alpha: float = 0.0, N: int = N_MODES, flow=None):
+    """eta_t for t = frame0 .. frame0+F-1 (AR(1) replayed from t = 0 if alpha != 0; frozen
+    flow if flow = (vx, vy) px/frame is nonzero)."""
+    if flow is not None and (flow[0] != 0.0 or flow[1] != 0.0):
+        for t in range(frame0, frame0 + F):
+            yield frozen_flow_noise(seed, t, P, Q, flow, N)
+        return
     if alpha == 0.0:
         for t in range(frame0, frame0 + F):
             yield white_spectral_noise(seed, t, P, Q, N)
@@ -108,12 +137,12 @@ def mix(f: np.ndarray, L: np.ndarray) -> np.ndarray:
     return a
 
 
-def sample_zernike(seed, frame0, F, sqrtS, L, H, W, alpha=0.0):
+def sample_zernike(seed, frame0, F, sqrtS, L, H, W, alpha=0.0, flow=None):
     """a [F][N][H][W] for frames frame0 .. frame0+F-1 (step 1)."""
     P, Q = sqrtS.shape[-2:]
     N = L.shape[0]
     out = np.empty((F, N, H, W))
-    for i, eta in enumerate(spectral_noise_sequence(seed, frame0, F, P, Q, alpha, N)):
+    for i, eta in enumerate(spectral_noise_sequence(seed, frame0, F, P, Q, alpha, N, flow)):
         out[i] = mix(fields_from_noise(eta, sqrtS, H, W), L)
     return out
 

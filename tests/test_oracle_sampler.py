@@ -253,3 +253,33 @@ def test_clamped_psd_fraction_reported():
     f64 = corr.psd_from_kernel(corr.autocorrelation_kernels(64, 64, s_px, N=3)[0])[2]
     f256 = corr.psd_from_kernel(corr.autocorrelation_kernels(256, 256, s_px, N=3)[0])[2]
     assert 0 < f256 < f64 < 0.1
+
+
+# ------------------------------------------------------------------ frozen flow (NEXT-3)
+def test_frozen_flow_integer_velocity_is_a_periodic_roll():
+    """frame t is the frame-0 field translated by v t; for integer v t the
+    spectral shift factors reproduce np.roll exactly (the Nyquist cos(pi s) = (-1)^s)."""
+    from oracle import pipeline, optics, correlation
+    P, Q, N = 12, 16, 36
+    sq, _ = correlation.sqrt_psd_tables(P, Q, optics.geometry()[0], N)
+    L = optics.noll_cholesky(optics.noll_covariance(N, 2.0))
+    a = pipeline.sample_zernike(7, 0, 4, sq, L, P, Q, flow=(2.0, -1.0))
+    for t in range(4):
+        assert np.allclose(a[t], np.roll(a[0], (-1 * t, 2 * t), axis=(1, 2)), atol=1e-12)
+
+
+def test_frozen_flow_fractional_shifts_compose_and_stay_real():
+    from oracle import pipeline
+    n = 10
+    for s1, s2 in ((0.3, 0.45), (1.25, -0.7)):
+        p = pipeline.flow_phase_1d(n, s1) * pipeline.flow_phase_1d(n, s2)
+        q = pipeline.flow_phase_1d(n, s1 + s2)
+        assert np.allclose(p[np.arange(n) != n // 2], q[np.arange(n) != n // 2], atol=1e-12)
+        ph = pipeline.flow_phase_1d(n, s1)
+        k = np.arange(n)
+        assert np.allclose(ph[(n - k) % n], np.conj(ph), atol=1e-15)  # Hermitian: real fields
+    # band-limited translation of a pure tone is exact at any sub-pixel shift
+    x = np.arange(n)
+    f = np.cos(2 * np.pi * 3 * x / n + 0.4)
+    g = np.real(np.fft.ifft(np.fft.fft(f) * pipeline.flow_phase_1d(n, 0.37)))
+    assert np.allclose(g, np.cos(2 * np.pi * 3 * (x - 0.37) / n + 0.4), atol=1e-12)
