@@ -109,6 +109,9 @@ WORKLOADS = {
                     desc="3840x2160 RGB, 2 frames/GPU per step, D/r0=5, Z=36, K=100 bases 33x33"),
     "cfg2_256": dict(H=256, W=256, C=1, F=100, d_over_r0=3.0, K=100, T=33, ar_alpha=0.95,
                      desc="256x256 gray, 100-frame AR(0.95) sequence, D/r0=3, K=100 bases 33x33"),
+    # NEXT-3: the frozen-flow temporal model on the headline geometry
+    "cfg3_512_flow": dict(H=512, W=512, C=3, F=64, d_over_r0=3.0, K=100, T=33, ar_alpha=0.0, flow=(0.5, 0.25),
+                          desc="512x512 RGB, 64-frame frozen-flow sequence (0.5, 0.25) px/frame, D/r0=3, K=100"),
 }
 
 
@@ -239,7 +242,7 @@ def main():
     mlp = synth.mlp_weights(K, seed=0)
     img_np = synth.image(H, W, C, seed=0)
     plan = Plan(PlanConfig(H=H, W=W, C=C, d_over_r0=w["d_over_r0"], K=K, taps=T, ar_alpha=w["ar_alpha"],
-                           max_batch=F, device=local, **STEP5), basis, mlp)
+                           max_batch=F, device=local, flow=w.get("flow", (0.0, 0.0)), **STEP5), basis, mlp)
     dev = torch.device("cuda", local)
     img = torch.from_numpy(img_np).to(dev)
     out = torch.empty((F, C, H, W), device=dev)

@@ -77,6 +77,11 @@ typedef struct {
   int    normalize_psf_sum; /* step 5: divide by sum_k w_k sum_u h_k, default 0      */
   int    clamp01;           /* step 5: clamp output to [0,1], default 0             */
   int    device;            /* CUDA ordinal the plan is bound to; 0 = current device */
+  float  flow_px_per_frame[2]; /* frozen flow: (vx, vy) pixels per
+                              * frame; nonzero selects it: the fields of frame t are those of
+                              * frame 0 of the sequence translated by t (vx, vy) on the periodic
+                              * grid (exact sub-pixel shift in the spectral domain, Q23).
+                              * Exclusive with ar_alpha.  Default (0, 0). */
 } p2s_options;
 
 /* Build a plan (P:312-330 generation setup; runs once, off the per-frame clock).
@@ -106,7 +111,8 @@ p2s_status p2s_plan_destroy(p2s_plan p);
  * sequence `seed`.  Plane 0 (piston) is 0; plane j-1 holds Noll mode j.
  * With ar_alpha != 0 the spectral noise follows eta_t = alpha eta_{t-1} +
  * sqrt(1-alpha^2) xi_t from t = 0 (replayed on the device when frame0 does not
- * continue the previous call). */
+ * continue the previous call).  With frozen flow, frame t is the translation of frame 0
+ * (stateless: any frame range, any batch split). */
 p2s_status p2s_sample_zernike(p2s_plan p, uint64_t seed, int64_t frame0, int nframes,
                               float* zern, void* stream);
 

@@ -431,6 +431,10 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
   const int h2 = o.mlp_hidden[1] > 0 ? o.mlp_hidden[1] : 100;
   if (h1 > 256 || h2 > 256) return set_error(P2S_ERR_INVALID_ARGUMENT, "mlp_hidden must be <= 256");
   if (!(o.ar_alpha >= 0.f && o.ar_alpha < 1.f)) return set_error(P2S_ERR_INVALID_ARGUMENT, "ar_alpha in [0,1)");
+  if (!std::isfinite(o.flow_px_per_frame[0]) || !std::isfinite(o.flow_px_per_frame[1]))
+    return set_error(P2S_ERR_INVALID_ARGUMENT, "flow_px_per_frame must be finite");
+  if ((o.flow_px_per_frame[0] != 0.f || o.flow_px_per_frame[1] != 0.f) && o.ar_alpha != 0.f)
+    return set_error(P2S_ERR_INVALID_ARGUMENT, "frozen flow and ar_alpha are exclusive");
   const double D = o.aperture_m > 0 ? o.aperture_m : 0.1;
   const double lam = o.wavelength_m > 0 ? o.wavelength_m : 525e-9;
   const int pad = o.pad > 0 ? o.pad : 1;
@@ -447,6 +451,8 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
   p->s_px = o.s_per_px > 0 ? o.s_per_px : L_m * (lam / (2.0 * D)) / D;
   p->kappa = o.tilt_px_per_rad > 0 ? o.tilt_px_per_rad : 4.0 / 3.14159265358979323846;
   p->ar_alpha = o.ar_alpha;
+  p->flow_vx = o.flow_px_per_frame[0];
+  p->flow_vy = o.flow_px_per_frame[1];
   p->noise_sigma = o.noise_sigma;
   p->normalize = o.normalize_psf_sum;
   p->clamp01 = o.clamp01;

@@ -258,7 +258,24 @@ struct RowArgs {
   float alpha, calpha;
   int64_t t_start;      // first frame evolved (AR replay starts at 0)
   int load_state;       // AR: state holds eta_{frame0-1}
+  int flow;             // frozen flow: frame-0 noise translated by (vx, vy) * frame pixels
+  double vx, vy;
 };
+
+// Frozen flow (reading Q23): shift factor of bin k of an n-point axis for a
+// translation by s pixels: exp(-2 pi i f_k s) with the signed frequency f_k, and the real
+// cos(pi s) at the Nyquist bin (its own mirror), so the spectrum stays Hermitian.  The
+// phase is reduced in fp64 before the fp32 sincos.
+__device__ __forceinline__ float2 flow_phase(int k, int n, double s) {
+  if (k == 0) return make_float2(1.f, 0.f);
+  if (2 * k == n) return make_float2((float)cospi(s), 0.f);
+  const int ks = 2 * k < n ? k : k - n;
+  double a = (double)ks * s / (double)n;
+  a -= rint(a);
+  float sn, cs;
+  sincospif((float)(-2.0 * a), &sn, &cs);
+  return make_float2(cs, sn);
+}
 
 // Unit-variance Hermitian noise zeta (eta / sqrt(PQ/2)) for both modes of pair p at bin (ky, kx).
 __device__ __forceinline__ float4 spectral_noise(int ky, int kx, int P, int Q, int p, int64_t frame, uint32_t k0,
@@ -305,11 +322,20 @@ __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
   __syncthreads();
   for (int t = 0; t < a.F; ++t) {
     const int64_t fr = a.frame0 + t;
+    const int64_t fr_noise = a.flow ? 0 : fr;  // frozen flow: one realisation, translated
+    const float2 phy = a.flow ? flow_phase(ky, a.P, a.vy * (double)fr) : make_float2(1.f, 0.f);
     for (int kx = threadIdx.x; kx < Q; kx += NT) {
-      const float4 z = spectral_noise(ky, kx, a.P, Q, p, fr, a.k0, a.k1);
+      const float4 z = spectral_noise(ky, kx, a.P, Q, p, fr_noise, a.k0, a.k1);
       const int km = kx ? Q - kx : 0;
-      X[pidx(2 * kx)] = spectrum(sS[kx], z);
-      X[pidx(2 * km + 1)] = spectrum(sS[Q + km], make_float4(z.x, -z.y, z.z, -z.w));  // mirror: conjugate noise
+      float2 y0 = spectrum(sS[kx], z);
+      float2 y1 = spectrum(sS[Q + km], make_float4(z.x, -z.y, z.z, -z.w));  // mirror: conjugate noise
+      if (a.flow) {  // the mirror bin's factor is the conjugate (Hermitian shift factors)
+        const float2 ph = cmul(phy, flow_phase(kx, Q, a.vx * (double)fr));
+        y0 = cmul(y0, ph);
+        y1 = cmul(y1, make_float2(ph.x, -ph.y));
+      }
+      X[pidx(2 * kx)] = y0;
+      X[pidx(2 * km + 1)] = y1;
     }
     __syncthreads();
     const float2* R = smem_ifft<NT>(X, Xb, &fpl, 1);
@@ -350,18 +376,28 @@ __global__ void __launch_bounds__(64 * NG, 3) k_rows_pair512(RowArgs a) {
   auto xi = [](int i) { return i + (i >> 3); };  // exchange padding: conflict-free pass writes
   for (int fi = g; fi < a.F; fi += NG) {
     const int64_t fr = a.frame0 + fi;
+    const int64_t fr_noise = a.flow ? 0 : fr;  // frozen flow: one realisation, translated
+    float2 phy = make_float2(1.f, 0.f);
+    if (a.flow) phy = flow_phase(ky, a.P, a.vy * (double)fr);
     float2 u[8], w[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int kx = t + B * r;
-      const float4 z = spectral_noise(ky, kx, a.P, N, p, fr, a.k0, a.k1);
+      const float4 z = spectral_noise(ky, kx, a.P, N, p, fr_noise, a.k0, a.k1);
       u[r] = spectrum(sS[kx], z);
       const float4 zc = make_float4(z.x, -z.y, z.z, -z.w);
       // mirror bin (N - kx) % N = tm + 64 (7 - r) for t > 0, 64 ((8 - r) % 8) for t == 0
+      const int rm = t ? 7 - r : (8 - r) & 7;
+      float2 wv = spectrum(sS[N + tm + B * rm], zc);
+      if (a.flow) {  // the mirror bin's factor is the conjugate (Hermitian shift factors)
+        const float2 ph = cmul(phy, flow_phase(kx, N, a.vx * (double)fr));
+        u[r] = cmul(u[r], ph);
+        wv = cmul(wv, make_float2(ph.x, -ph.y));
+      }
       if (t)
-        w[7 - r] = spectrum(sS[N + tm + B * (7 - r)], zc);
+        w[7 - r] = wv;
       else
-        w[(8 - r) & 7] = spectrum(sS[N + B * ((8 - r) & 7)], zc);
+        w[(8 - r) & 7] = wv;
     }
     reg_pass_t<1>(u, t, tw);
     reg_pass_t<1>(w, tm, tw);
@@ -474,6 +510,9 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
   a.calpha = sqrtf(1.0f - pl->ar_alpha * pl->ar_alpha);
   a.t_start = ar ? replay_from : frame0;
   a.load_state = (ar && ar_mode == 0) ? 1 : 0;
+  a.flow = (pl->flow_vx != 0.0 || pl->flow_vy != 0.0) ? 1 : 0;
+  a.vx = pl->flow_vx;
+  a.vy = pl->flow_vy;
   if (ar) {
     dim3 grid(pl->P, pl->npairs);
     size_t sm = ((size_t)2 * pl->Q + 2 * padded_len(pl->Q)) * sizeof(float2) + (size_t)pl->Q * sizeof(float4) + 16;

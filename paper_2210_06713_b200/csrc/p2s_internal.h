@@ -88,6 +88,7 @@ struct p2s_plan_s {
   int nslots = 0, npairs = 0, h1 = 0, h2 = 0;
   double d_over_r0 = 0, L_m = 0, s_px = 0, kappa = 0;
   float ar_alpha = 0, noise_sigma = 0;
+  double flow_vx = 0, flow_vy = 0;  // frozen flow, pixels per frame (0 = off)
   int normalize = 0, clamp01 = 0, device = 0, max_batch = 0;
   double clamped_max = 0;
   std::vector<double> A0, Lc;      // Z x Z

@@ -38,7 +38,7 @@ class Options(ctypes.Structure):
                 ("s_per_px", ctypes.c_double), ("tilt_px_per_rad", ctypes.c_double), ("pad", ctypes.c_int),
                 ("mlp_hidden", ctypes.c_int * 2), ("max_batch", ctypes.c_int), ("ar_alpha", ctypes.c_float),
                 ("noise_sigma", ctypes.c_float), ("normalize_psf_sum", ctypes.c_int), ("clamp01", ctypes.c_int),
-                ("device", ctypes.c_int)]
+                ("device", ctypes.c_int), ("flow_px_per_frame", ctypes.c_float * 2)]
 
 
 def _load():
@@ -138,6 +138,7 @@ class PlanConfig:
     normalize_psf_sum: bool = False
     clamp01: bool = False
     device: int = 0
+    flow: tuple = (0.0, 0.0)  # frozen flow (vx, vy) pixels per frame (NEXT-3)
     extra: dict = field(default_factory=dict)
 
 
@@ -162,6 +163,7 @@ class Plan:
         o.normalize_psf_sum = int(cfg.normalize_psf_sum)
         o.clamp01 = int(cfg.clamp01)
         o.device = cfg.device
+        o.flow_px_per_frame[0], o.flow_px_per_frame[1] = cfg.flow
         self._h = ctypes.c_void_p()
         _check(lib.p2s_plan_create(ctypes.byref(self._h), cfg.H, cfg.W, cfg.C, float(cfg.d_over_r0),
                                    float(cfg.L_m), cfg.Z, cfg.K, basis.ctypes.data, mlp.ctypes.data, ctypes.byref(o)))

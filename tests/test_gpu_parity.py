@@ -285,3 +285,56 @@ def test_invalid_arguments_fail_loudly():
     with pytest.raises(P2SError):
         Plan(PlanConfig(H=64, W=64, C=1, d_over_r0=-1.0, K=16, taps=17), synth.basis(16, 17),
              synth.mlp_weights(16))
+
+
+# ------------------------------------------------------------------ frozen flow (NEXT-3)
+@pytest.mark.parametrize("H,W,flow,frame0", [(64, 96, (1.5, -0.75), 3), (96, 512, (-2.25, 0.5), 0),
+                                              (512, 96, (0.3, 1.0), 7)])
+def test_frozen_flow_sample_zernike_vs_oracle(H, W, flow, frame0):
+    """P:418-420: frame t = frame 0 translated by t v (spectral shift factors, reading Q23);
+    covers the generic and the register-resident 512-point row kernels."""
+    F = 3
+    plan, _, _, sq, L = make_plan(H, W, 1, 2.0, 16, 17, flow=flow)
+    z = torch.empty((F, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, frame0, F, z)
+    torch.cuda.synchronize()
+    got = z.cpu().numpy()
+    ref = pipeline.sample_zernike(SEED, frame0, F, sq, L, H, W, flow=flow)
+    worst = max(rel_l2(got[f, j], ref[f, j]) for f in range(F) for j in range(1, 36))
+    assert worst <= 1e-4, worst
+
+
+def test_frozen_flow_integer_velocity_rolls_frame0():
+    H, W = 48, 64
+    plan, *_ = make_plan(H, W, 1, 3.0, 16, 17, flow=(3.0, -2.0))
+    z = torch.empty((4, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 0, 4, z)
+    torch.cuda.synchronize()
+    a = z.cpu().numpy()
+    for t in range(1, 4):
+        assert rel_l2(a[t], np.roll(a[0], (-2 * t, 3 * t), axis=(1, 2))) < 1e-5
+
+
+def test_frozen_flow_simulate_vs_oracle():
+    H, W, C, K, T, F = 64, 64, 3, 16, 17, 2
+    flow = (0.5, 1.25)
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T, flow=flow)
+    img = synth.image(H, W, C, seed=3)
+    out = torch.empty((F, C, H, W), device="cuda")
+    plan.simulate_frames(cuda(img), 0, SEED, 5, F, out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    s_px, kappa = optics.geometry()
+    layers = synth.unpack_mlp(mlp, K)
+    a = pipeline.sample_zernike(SEED, 5, F, sq, L, H, W, flow=flow)
+    for f in range(F):
+        Iw = pipeline.warp(img, a[f, 1], a[f, 2], kappa)
+        ref = pipeline.blur(Iw, pipeline.mlp(a[f, 3:], layers), basis)
+        for c in range(C):
+            assert rel_l2(got[f, c], ref[c]) <= 2e-2
+
+
+def test_frozen_flow_with_ar_is_rejected():
+    from paper_2210_06713_b200 import P2SError
+    with pytest.raises(P2SError):
+        make_plan(32, 32, 1, 2.0, 16, 17, flow=(1.0, 0.0), ar_alpha=0.5)
