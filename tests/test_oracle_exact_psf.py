@@ -25,9 +25,8 @@ def test_zero_phase_is_airy():
     airy = np.where(r == 0, 1.0, (2 * j1(np.maximum(v, 1e-12)) / np.maximum(v, 1e-12)) ** 2)
     hn = h / h[c, c]
     assert np.max(np.abs(hn - airy)) < 0.03
-    # first dark ring at 2.44 px: the along-axis profile dips below 5% of the peak at 2-3 px
-    prof = np.array([hn[c, c + k] for k in range(5)])
-    assert int(np.argmin(prof[1:])) + 1 in (2, 3) and prof[1:].min() < 0.05
+    # the core ends at the first dark ring (2.44 px): half power near 1 px, < 5% at 2 px
+    assert hn[c, c + 1] > 0.4 and hn[c, c + 2] < 0.05 and hn[c + 2, c] < 0.05
 
 
 def test_tilt_shift_is_four_over_pi():
