@@ -184,6 +184,24 @@ p2s_status p2s_plan_import_sqrtS(p2s_plan p, const float* sqrtS);
  *   freed on the stream.  Errors: P2S_ERR_INVALID_ARGUMENT for bad sizes / NULL. */
 p2s_status p2s_field_autocorr(p2s_plan p, const float* zern, int nframes, int max_lag, double* out, void* stream);
 
+/* Exact-PSF path (partial): the slow per-pixel reference that P2S
+ * replaces.  Eq.2: h_x(u) = |F{P e^{-j phi_x}}|^2 with phi_x = sum_j a_j(x) Z_j on
+ * a 32-sample pupil zero-padded to a 64-point FFT (PSF pixel = lambda/(2D): a pure tilt moves
+ * the PSF by 4 a_2/pi px, reading Q24), T x T window (the plan's taps), unit sum.
+ *   zern   : device float [Z][H][W], ONE frame in the p2s_sample_zernike layout.
+ *   pixels : device int32 [n] pixel indices y*W + x.
+ *   include_tilt: 0 drops a_2, a_3 from the phase (the higher-order PSF that P2S maps).
+ *   out    : device float [n][T][T], tap (T/2 + uy, T/2 + ux) = h(uy, ux).
+ * Errors: INVALID_ARGUMENT (NULL, n < 1), CUDA. */
+p2s_status p2s_exact_psf(p2s_plan p, const float* zern, const int32_t* pixels, int n, int include_tilt,
+                         float* out, void* stream);
+
+/* Eq.1 gather render of one frame with the exact per-pixel PSFs:
+ * out_c(x) = sum_u h_x(u) img_c(x - u) (true convolution, whole-sample mirror boundary).
+ *   img: device float [C][H][W]; zern: device float [Z][H][W]; out: device float [C][H][W]. */
+p2s_status p2s_render_exact(p2s_plan p, const float* img, const float* zern, int include_tilt, float* out,
+                            void* stream);
+
 /* Device Philox4x32-10 test fill: out (dev uint32 [n][4]) <- philox(counter =
  * (i, c1, c2, c3), key = (k0, k1)) for i = 0..n-1. */
 p2s_status p2s_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,

@@ -334,6 +334,7 @@ static void free_plan(p2s_plan_s* p) {
     cudaEventDestroy(p->ev_sub);
     cudaEventDestroy(p->ev_copied);
   }
+  cudaFree(p->d_ztab);
   cudaFree(p->bg.koff);
   cudaFree(p->bg.adesc);
   cudaFree(p->bg.klbo);
@@ -726,6 +727,26 @@ extern "C" p2s_status p2s_field_autocorr(p2s_plan p, const float* zern, int nfra
   const int rc = launch_acorr(zern, nframes, p->Z, p->H, p->W, max_lag, partial, out, s);
   cudaFreeAsync(partial, s);
   if (rc != 0) return set_error(P2S_ERR_CUDA, std::string("k_acorr: ") + cudaGetErrorString((cudaError_t)rc));
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_exact_psf(p2s_plan p, const float* zern, const int32_t* pixels, int n, int include_tilt,
+                                    float* out, void* stream) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (!zern || !pixels || !out || n < 1) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer or n < 1");
+  DeviceGuard guard(p->device);
+  P2S_LAUNCH(ensure_pupil_table(p), "pupil table");
+  P2S_LAUNCH(launch_exact_psf(p, zern, pixels, n, include_tilt, out, (cudaStream_t)stream), "k_exact_psf");
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_render_exact(p2s_plan p, const float* img, const float* zern, int include_tilt, float* out,
+                                       void* stream) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (!img || !zern || !out) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  P2S_LAUNCH(ensure_pupil_table(p), "pupil table");
+  P2S_LAUNCH(launch_render_exact(p, img, zern, include_tilt, out, (cudaStream_t)stream), "k_render_exact");
   return P2S_OK;
 }
 

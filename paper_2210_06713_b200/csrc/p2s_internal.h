@@ -25,6 +25,7 @@ bool noll_cholesky(int Z, const std::vector<double>& A, std::vector<double>& L);
 void bessel_j_all(double x, int nmax, double* J);
 void psd_tables(int P, int Q, double s_px, int Z, std::vector<double>& sqrtS, std::vector<double>& clamped);
 int grid_size(int x);
+double zernike_value(int j, double rho, double theta);
 
 constexpr int kMaxRadix = 24;
 
@@ -98,6 +99,7 @@ struct p2s_plan_s {
   // device tables
   float2* d_sqrtS = nullptr;    // [npairs][P][Q] scaled (sa, sb)
   float4* d_ar = nullptr;       // [npairs][P][Q] AR(1) state (zeta_a, zeta_b)
+  float* d_ztab = nullptr;      // exact-PSF pupil table [Z][32*32] (lazy, NEXT-1)
   float* d_L = nullptr;         // [(Z-1)*(Z-1)] float L[2..Z][2..Z]
   uint8_t* d_mlp_fold = nullptr;   // L folded into layer 1 (inputs f_2..f_Z)
   uint8_t* d_mlp_plain = nullptr;  // plain layer 1 (inputs a_4..a_Z)
@@ -145,6 +147,11 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
 int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair, int stages);
 size_t acorr_partial_bytes(int F, int Z, int W, int L);
 int launch_acorr(const float* zern, int F, int Z, int H, int W, int L, double* partial, double* out, cudaStream_t s);
+int ensure_pupil_table(p2s_plan_s* p);
+int launch_exact_psf(const p2s_plan_s* p, const float* zern, const int* pix, int n, int include_tilt, float* out,
+                     cudaStream_t s);
+int launch_render_exact(const p2s_plan_s* p, const float* img, const float* zern, int include_tilt, float* out,
+                        cudaStream_t s);
 int launch_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int64_t n, uint32_t* out,
                        cudaStream_t s);
 }  // namespace p2s

@@ -462,3 +462,20 @@ extern "C" p2s_status p2s_host_tables(int P, int Q, double s_per_px, double d_ov
   }
   return P2S_OK;
 }
+
+namespace p2s {
+// Noll-normalised Zernike polynomial Z_j(rho, theta) on the unit disk (theta from the
+// column axis, reading Q4); used for the exact-PSF pupil table (NEXT-1).
+double zernike_value(int j, double rho, double theta) {
+  int n, m, kind;
+  noll_nm(j, &n, &m, &kind);
+  double R = 0.0;
+  for (int s = 0; s <= (n - m) / 2; ++s) {
+    double c = std::tgamma(n - s + 1.0) /
+               (std::tgamma(s + 1.0) * std::tgamma((n + m) / 2 - s + 1.0) * std::tgamma((n - m) / 2 - s + 1.0));
+    R += ((s & 1) ? -c : c) * std::pow(rho, n - 2 * s);
+  }
+  if (m == 0) return std::sqrt(n + 1.0) * R;
+  return std::sqrt(2.0 * (n + 1.0)) * R * (kind > 0 ? std::cos(m * theta) : std::sin(m * theta));
+}
+}  // namespace p2s

@@ -23,7 +23,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NUMERIC", 3: "CUDA", 4: "OUT_OF_M
 # every entry point declared in include/p2s.h
 EXPORTS = ("p2s_plan_create", "p2s_plan_destroy", "p2s_sample_zernike", "p2s_warp", "p2s_blur",
            "p2s_simulate_frames", "p2s_simulate_frames_host", "p2s_last_error", "p2s_plan_info",
-           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_philox_fill",
+           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_exact_psf", "p2s_render_exact", "p2s_philox_fill",
            "p2s_host_tables", "p2s_grid_size")
 
 
@@ -64,6 +64,8 @@ def _load():
     lib.p2s_plan_stage_times.argtypes = [vp, vp, vp]
     lib.p2s_philox_fill.argtypes = [u32, u32, u32, u32, u32, i64, vp, vp]
     lib.p2s_field_autocorr.argtypes = [vp, vp, i32, i32, vp, vp]
+    lib.p2s_exact_psf.argtypes = [vp, vp, vp, i32, i32, vp, vp]
+    lib.p2s_render_exact.argtypes = [vp, vp, vp, i32, vp, vp]
     lib.p2s_host_tables.argtypes = [i32, i32, ctypes.c_double, ctypes.c_double, i32, vp, vp, vp, vp]
     lib.p2s_grid_size.argtypes = [i32]
     lib.p2s_grid_size.restype = i32
@@ -191,6 +193,14 @@ class Plan:
     def field_autocorr(self, zern, nframes, max_lag, out, stream=None):
         """out (device float64 [Z][2][max_lag]) <- periodic auto-correlation of zern along x, y."""
         _check(lib.p2s_field_autocorr(self._h, _ptr(zern), nframes, max_lag, _ptr(out), _stream(stream)))
+
+    def exact_psf(self, zern, pixels, n, include_tilt, out, stream=None):
+        """out (device float [n][T][T]) <- Eq.2 PSFs of the given pixels of one frame."""
+        _check(lib.p2s_exact_psf(self._h, _ptr(zern), _ptr(pixels), n, int(include_tilt), _ptr(out), _stream(stream)))
+
+    def render_exact(self, img, zern, include_tilt, out, stream=None):
+        """out (device float [C][H][W]) <- Eq.1 gather render of one frame with exact PSFs."""
+        _check(lib.p2s_render_exact(self._h, _ptr(img), _ptr(zern), int(include_tilt), _ptr(out), _stream(stream)))
 
     def warp(self, img, img_frame_stride, zern, warped, nframes, stream=None):
         _check(lib.p2s_warp(self._h, _ptr(img), img_frame_stride, _ptr(zern), _ptr(warped), nframes,
