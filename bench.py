@@ -297,6 +297,13 @@ def main():
     if rank == 0:
         peaks = load_peaks()
         work = algorithmic_work(w)
+        if stages.get("k_warp", (0.0, 0))[1] == 0:
+            # step 2 fused into the 512-point column kernel: its bytes move there (Iw written
+            # and the image read instead of the fp32 tilt planes)
+            kind, amount = work["k_cols"]
+            HW, C, F = w["H"] * w["W"], w["C"], w["F"]
+            work["k_cols"] = (kind, amount - F * 2 * HW * 4 + F * C * HW * 2 + C * HW * 4)
+            del work["k_warp"]
         st = {}
         for name, (kind, amount) in work.items():
             tot_ms, n = stages[name]

@@ -644,11 +644,13 @@ extern "C" p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t 
     const int F = std::min(p->max_batch, nframes - i0);
     p2s_status st = run_step1(p, seed, frame0 + i0, F, s);
     if (st != P2S_OK) return st;
+    bool warp_fused = false;  // 512-point columns: step 2 runs inside the column kernel
     {
       StageScope sc(p, 1, s);
-      P2S_LAUNCH(launch_cols(p, F, 1, nullptr, s), "k_cols");
+      P2S_LAUNCH(launch_cols(p, F, 1, nullptr, s, img + (size_t)i0 * img_frame_stride, img_frame_stride, &warp_fused),
+                 "k_cols");
     }
-    {
+    if (!warp_fused) {
       StageScope sc(p, 2, s);
       P2S_LAUNCH(launch_warp_sim(p, F, img + (size_t)i0 * img_frame_stride, img_frame_stride, s), "k_warp");
     }

@@ -552,7 +552,39 @@ struct ColArgs {
   float* zern;        // mode 0: [F][Z][H][W]
   uint16_t* X;        // mode 1: bf16 [F][nslots][H*W]
   float* tilt;        // mode 1: [F][2][H*W]
+  // mode 1, fused step 2 (512-point columns): the mode-pair-0 CTAs hold f_2, f_3 and warp
+  // the image directly (no tilt planes): Iw(x) = bilinear(I, x + (cx f2, cy0 f2 + cy1 f3))
+  int fuse_warp;
+  const float* img;   // [F or 1][C][H][W]
+  int64_t img_stride; // floats between frames (0 = broadcast)
+  int C;
+  float cx, cy0, cy1;
+  uint16_t* Iw;       // bf16 [F][C][H][W]
 };
+
+// Step 2 at one pixel (the arithmetic of k_warp: clamp-to-edge bilinear gather).
+__device__ __forceinline__ void warp_pixel(const ColArgs& a, int f, int y, int x, float u, float v) {
+  const int HW = a.H * a.W;
+  const float X = (float)x + a.cx * u;
+  const float Y = (float)y + a.cy0 * u + a.cy1 * v;
+  const float fx = floorf(X), fy = floorf(Y);
+  const float tx = X - fx, ty = Y - fy;
+  int xa = (int)fmaxf(fminf(fx, (float)(a.W - 1)), -1.f);
+  int ya = (int)fmaxf(fminf(fy, (float)(a.H - 1)), -1.f);
+  const int xb = min(xa + 1, a.W - 1), yb = min(ya + 1, a.H - 1);
+  xa = max(xa, 0);
+  ya = max(ya, 0);
+  const float* I = a.img + (size_t)f * a.img_stride;
+  const int pix = y * a.W + x;
+#pragma unroll 1
+  for (int c = 0; c < a.C; ++c) {
+    const float* Ic = I + (size_t)c * HW;
+    const float i00 = __ldg(&Ic[ya * a.W + xa]), i01 = __ldg(&Ic[ya * a.W + xb]);
+    const float i10 = __ldg(&Ic[yb * a.W + xa]), i11 = __ldg(&Ic[yb * a.W + xb]);
+    const float val = (1.f - ty) * ((1.f - tx) * i00 + tx * i01) + ty * ((1.f - tx) * i10 + tx * i11);
+    a.Iw[((size_t)f * a.C + c) * HW + pix] = f_to_bf16(val);
+  }
+}
 
 template <int MODE, int NT>
 __global__ void __launch_bounds__(NT) k_cols(ColArgs a) {
@@ -663,11 +695,12 @@ __global__ void __launch_bounds__(512) k_cols512(ColArgs a) {
   }
   reg_pass<64>(u, j0, tw);
   reg_pass<64>(w, j1, tw);
-  if (x >= a.W) return;
+  const bool fused_warp_cta = MODE == 1 && a.fuse_warp && p == 0;  // uniform per CTA
+  if (x >= a.W && !fused_warp_cta) return;
   const int sa = 2 * p, sb = 2 * p + 1;
   const size_t HW = (size_t)a.H * a.W;
   auto put = [&](int yy, float2 v) {
-    if (yy >= a.H) return;
+    if (yy >= a.H || x >= a.W) return;
     const size_t pix = (size_t)yy * a.W + x;
     if (MODE == 0) {
       float* z = a.zern + (size_t)f * a.Z * HW;
@@ -677,13 +710,40 @@ __global__ void __launch_bounds__(512) k_cols512(ColArgs a) {
       uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
       Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
       if (sb < a.nslots) Xo[(size_t)sb * HW + pix] = f_to_bf16(v.y);
-      if (p == 0) {
+      if (p == 0 && !a.fuse_warp) {
         float* tl = a.tilt + (size_t)f * 2 * HW;
         tl[pix] = v.x;
         tl[HW + pix] = v.y;
       }
     }
   };
+  if (fused_warp_cta) {
+    // fused step 2: stash f_2, f_3 of the 16 columns in the (now free) exchange buffer,
+    // then warp with the field registers dead (keeps the kernel's register budget)
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      xb[(j0 + B * r) * TC + c] = u[r];
+      xb[(j1 + B * r) * TC + c] = w[r];
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      put(j0 + B * r, u[r]);
+      put(j1 + B * r, w[r]);
+    }
+    __syncwarp();
+    if (x < a.W) {
+#pragma unroll 1
+      for (int r = 0; r < 16; ++r) {
+        const int yy = (r & 1 ? j1 : j0) + B * (r >> 1);
+        if (yy < a.H) {
+          const float2 v = xb[yy * TC + c];
+          warp_pixel(a, f, yy, x, v.x, v.y);
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     put(j0 + B * r, u[r]);
@@ -691,7 +751,8 @@ __global__ void __launch_bounds__(512) k_cols512(ColArgs a) {
   }
 }
 
-int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t s) {
+int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t s, const float* img,
+                int64_t img_stride, bool* warp_fused) {
   ColArgs a;
   fill_fft_args(a.fp, pl->fp);
   a.Zin = pl->d_Z;
@@ -708,7 +769,21 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   a.zern = zern;
   a.X = pl->d_X;
   a.tilt = pl->d_tilt;
+  a.fuse_warp = 0;
+  if (warp_fused) *warp_fused = false;
   if (reg512(pl->fp) && getenv_flag("P2S_FFT_GENERIC") == 0) {
+    if (mode == 1 && img && warp_fused && getenv_flag("P2S_NO_WARP_FUSION") == 0) {
+      const int Z = pl->Z;
+      a.fuse_warp = 1;
+      a.img = img;
+      a.img_stride = img_stride;
+      a.C = pl->C;
+      a.cx = (float)(pl->kappa * pl->Lc[1 * Z + 1]);
+      a.cy0 = (float)(pl->kappa * pl->Lc[2 * Z + 1]);
+      a.cy1 = (float)(pl->kappa * pl->Lc[2 * Z + 2]);
+      a.Iw = pl->d_Iw;
+      *warp_fused = true;
+    }
     dim3 grid((pl->W + 15) / 16, pl->npairs, F);  // only the W cropped columns are needed
     size_t sm = (size_t)kRegN * 17 * sizeof(float2);
     if (mode == 0) {

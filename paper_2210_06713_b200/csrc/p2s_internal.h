@@ -135,7 +135,8 @@ namespace p2s {
 // ---- kernel launchers (k_*.cu); all return cudaGetLastError() as int ----
 int launch_rows(const p2s_plan_s* p, uint64_t seed, int64_t frame0, int F, bool ar, int ar_mode,
                 int64_t replay_from, cudaStream_t s);
-int launch_cols(const p2s_plan_s* p, int F, int mode, float* zern, cudaStream_t s);
+int launch_cols(const p2s_plan_s* p, int F, int mode, float* zern, cudaStream_t s, const float* img = nullptr,
+                int64_t img_stride = 0, bool* warp_fused = nullptr);
 int launch_mix(const p2s_plan_s* p, int F, float* zern, cudaStream_t s);
 int launch_zern_to_x(const p2s_plan_s* p, int F, const float* zern, cudaStream_t s);
 int launch_warp_f32(const p2s_plan_s* p, int F, const float* img, int64_t stride, const float* zern, float* out,
