@@ -129,6 +129,13 @@ p2s_status p2s_warp(p2s_plan p, const float* img, int64_t img_frame_stride, cons
 p2s_status p2s_blur(p2s_plan p, const float* warped, const float* zern, uint64_t seed,
                     int64_t frame0, float* out, int nframes, void* stream);
 
+/* Steps 4-5 with caller-supplied basis weights instead of the MLP (e.g. the exact
+ * projection of each pixel's PSF on the basis, NEXT-1):
+ *   out (dev float [nframes][C][H][W]) <- step5(sum_k weights_k(x) (h_k (*) warped_c)(x)).
+ *   weights: dev float [nframes][K][H][W] (the plan's K). */
+p2s_status p2s_blur_weights(p2s_plan p, const float* warped, const float* weights, uint64_t seed,
+                            int64_t frame0, float* out, int nframes, void* stream);
+
 /* Steps 1-5 fused: out (dev float [nframes][C][H][W]) for frames frame0.. of sequence seed.
  * img as in p2s_warp.  Equivalent to sample_zernike -> warp -> blur up to rounding
  * (L is folded into the MLP's first layer; tensor-core stages run in bf16 with
@@ -201,6 +208,14 @@ p2s_status p2s_exact_psf(p2s_plan p, const float* zern, const int32_t* pixels, i
  *   img: device float [C][H][W]; zern: device float [Z][H][W]; out: device float [C][H][W]. */
 p2s_status p2s_render_exact(p2s_plan p, const float* img, const float* zern, int include_tilt, float* out,
                             void* stream);
+
+/* Host-only: PSF basis by principal components (Eq.7; NEXT-1 part).
+ *   psfs  : host float [n][T*T] PSF database (e.g. p2s_exact_psf at sampled pixels).
+ *   basis : host float [M+1][T*T] out: row 0 the mean PSF, rows 1..M the M leading principal
+ *           components (unit L2 norm, ordered by variance, largest entry positive).
+ *   residual: optional out, fraction of the centred database energy the M components miss.
+ * fp64 covariance, block iteration + Rayleigh-Ritz.  Errors: INVALID_ARGUMENT. */
+p2s_status p2s_fit_basis(const float* psfs, int n, int T, int M, float* basis, double* residual);
 
 /* Device Philox4x32-10 test fill: out (dev uint32 [n][4]) <- philox(counter =
  * (i, c1, c2, c3), key = (k0, k1)) for i = 0..n-1. */

@@ -76,3 +76,24 @@ def render_exact(img: np.ndarray, a: np.ndarray, T: int, include_tilt: bool = Tr
             patch = img[:, py[:, None], px[None, :]]
             out[:, y, x] = np.einsum("tu,ctu->c", h, patch)
     return out
+
+
+def pca_basis(psfs: np.ndarray, M: int):
+    """Eq.7: mean PSF + the M leading principal components of a PSF database
+    (plain definition: eigen-decomposition of the sample covariance).  psfs [n][T][T] ->
+    (basis [M+1][T][T] with row 0 the mean, components unit-norm, largest entry positive;
+    residual = fraction of the centred energy not captured)."""
+    X = np.asarray(psfs, dtype=np.float64).reshape(psfs.shape[0], -1)
+    mu = X.mean(0)
+    Xc = X - mu
+    C = Xc.T @ Xc
+    evals, evecs = np.linalg.eigh(C)
+    idx = np.argsort(evals)[::-1][:M]
+    V = evecs[:, idx].T
+    for r in range(M):
+        if V[r, np.argmax(np.abs(V[r]))] < 0:
+            V[r] = -V[r]
+    T = psfs.shape[1]
+    basis = np.concatenate([mu[None], V]).reshape(M + 1, T, T)
+    res = max(0.0, 1.0 - evals[idx].sum() / np.trace(C)) if np.trace(C) > 0 else 0.0
+    return basis, res

@@ -631,6 +631,24 @@ extern "C" p2s_status p2s_blur(p2s_plan p, const float* warped, const float* zer
   return P2S_OK;
 }
 
+extern "C" p2s_status p2s_blur_weights(p2s_plan p, const float* warped, const float* weights, uint64_t seed,
+                                       int64_t frame0, float* out, int nframes, void* stream) {
+  CHECK_PLAN();
+  if (nframes == 0) return P2S_OK;
+  if (!warped || !weights || !out) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t HW = (size_t)p->H * p->W;
+  for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
+    const int F = std::min(p->max_batch, nframes - i0);
+    P2S_LAUNCH(launch_pack_weights(p, F, weights + (size_t)i0 * p->K * HW, s), "k_pack_weights");
+    P2S_LAUNCH(launch_blur(p, F, warped + (size_t)i0 * p->C * HW, true, seed, frame0 + i0,
+                           out + (size_t)i0 * p->C * HW, s),
+               "k_blur");
+  }
+  return P2S_OK;
+}
+
 extern "C" p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t img_frame_stride, uint64_t seed,
                                           int64_t frame0, int nframes, float* out, void* stream) {
   CHECK_PLAN();

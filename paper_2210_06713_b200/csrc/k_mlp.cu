@@ -290,6 +290,43 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
   if (warp == 0) tmem_dealloc(*tslot, ncols);
 }
 
+// User-supplied basis weights (p2s_blur_weights): fp32 planes [F][K][H][W] -> the blur's
+// bf16 row-tile layout [F][H][ntx][np/8][128][8] (bases >= K and pixels >= W are zero).
+__global__ void k_pack_weights(const float* __restrict__ wts, int K, int np, int H, int W, int ntx,
+                               uint16_t* __restrict__ out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 8-basis chunk of one pixel
+  const int nk8 = np / 8;
+  const size_t per_row = (size_t)ntx * nk8 * 128;
+  const int f = blockIdx.y;
+  if (i >= (size_t)H * per_row) return;
+  const int y = (int)(i / per_row);
+  size_t r = i - (size_t)y * per_row;
+  const int xt = (int)(r / ((size_t)nk8 * 128));
+  r -= (size_t)xt * nk8 * 128;
+  const int k8 = (int)(r / 128), px = (int)(r % 128);
+  const int x = xt * 128 + px;
+  uint32_t pk[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float v[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = k8 * 8 + 2 * e + h;
+      v[h] = (k < K && x < W) ? __ldg(&wts[(((size_t)f * K + k) * H + y) * W + x]) : 0.f;
+    }
+    pk[e] = pack_bf16x2(v[0], v[1]);
+  }
+  reinterpret_cast<uint4*>(out + (size_t)f * H * per_row * 8)[i] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+}
+
+int launch_pack_weights(const p2s_plan_s* p, int F, const float* wts, cudaStream_t s) {
+  const int np = p->mg_fold.n3;
+  const size_t n = (size_t)p->H * p->ntx * (np / 8) * 128;
+  dim3 grid((unsigned)((n + 255) / 256), F);
+  k_pack_weights<<<grid, 256, 0, s>>>(wts, p->K, np, p->H, p->W, p->ntx, p->d_w);
+  return (int)cudaGetLastError();
+}
+
 int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   const MlpGeom& g = folded ? p->mg_fold : p->mg_plain;
   MlpArgs a;

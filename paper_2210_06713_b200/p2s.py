@@ -23,7 +23,8 @@ _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NUMERIC", 3: "CUDA", 4: "OUT_OF_M
 # every entry point declared in include/p2s.h
 EXPORTS = ("p2s_plan_create", "p2s_plan_destroy", "p2s_sample_zernike", "p2s_warp", "p2s_blur",
            "p2s_simulate_frames", "p2s_simulate_frames_host", "p2s_last_error", "p2s_plan_info",
-           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_exact_psf", "p2s_render_exact", "p2s_philox_fill",
+           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_exact_psf", "p2s_render_exact", "p2s_fit_basis", "p2s_blur_weights",
+           "p2s_philox_fill",
            "p2s_host_tables", "p2s_grid_size")
 
 
@@ -65,6 +66,8 @@ def _load():
     lib.p2s_philox_fill.argtypes = [u32, u32, u32, u32, u32, i64, vp, vp]
     lib.p2s_field_autocorr.argtypes = [vp, vp, i32, i32, vp, vp]
     lib.p2s_exact_psf.argtypes = [vp, vp, vp, i32, i32, vp, vp]
+    lib.p2s_fit_basis.argtypes = [vp, i32, i32, i32, vp, vp]
+    lib.p2s_blur_weights.argtypes = [vp, vp, vp, u64, i64, vp, i32, vp]
     lib.p2s_render_exact.argtypes = [vp, vp, vp, i32, vp, vp]
     lib.p2s_host_tables.argtypes = [i32, i32, ctypes.c_double, ctypes.c_double, i32, vp, vp, vp, vp]
     lib.p2s_grid_size.argtypes = [i32]
@@ -84,9 +87,12 @@ def _check(st):
 
 
 def _ptr(x):
-    """Device pointer of a torch tensor (or an int address)."""
+    """Device pointer of a torch tensor (or an int address).  The C ABI takes dense
+    row-major buffers, so a non-contiguous tensor is an error (never silently re-laid)."""
     if isinstance(x, int):
         return ctypes.c_void_p(x)
+    if hasattr(x, "is_contiguous") and not x.is_contiguous():
+        raise ValueError("p2s: tensor arguments must be contiguous (row-major); use .contiguous()")
     return ctypes.c_void_p(x.data_ptr())
 
 
@@ -112,6 +118,16 @@ def host_tables(P, Q, s_per_px, d_over_r0, Z=36, want_sqrtS=True):
     _check(lib.p2s_host_tables(P, Q, float(s_per_px), float(d_over_r0), Z, A0.ctypes.data, L.ctypes.data,
                                sq.ctypes.data if want_sqrtS else None, cl.ctypes.data if want_sqrtS else None))
     return A0, L, sq, cl
+
+
+def fit_basis(psfs, M):
+    """PCA basis of a PSF database (host float32 [n][T][T]) -> (basis [M+1][T][T], residual)."""
+    psfs = np.ascontiguousarray(psfs, dtype=np.float32)
+    n, T = psfs.shape[0], psfs.shape[1]
+    basis = np.empty((M + 1, T, T), dtype=np.float32)
+    res = ctypes.c_double()
+    _check(lib.p2s_fit_basis(psfs.ctypes.data, n, T, M, basis.ctypes.data, ctypes.byref(res)))
+    return basis, res.value
 
 
 def philox_fill(c1, c2, c3, k0, k1, n, out, stream=None):
@@ -193,6 +209,11 @@ class Plan:
     def field_autocorr(self, zern, nframes, max_lag, out, stream=None):
         """out (device float64 [Z][2][max_lag]) <- periodic auto-correlation of zern along x, y."""
         _check(lib.p2s_field_autocorr(self._h, _ptr(zern), nframes, max_lag, _ptr(out), _stream(stream)))
+
+    def blur_weights(self, warped, weights, seed, frame0, out, nframes, stream=None):
+        """Steps 4-5 with given per-pixel basis weights (device float [F][K][H][W])."""
+        _check(lib.p2s_blur_weights(self._h, _ptr(warped), _ptr(weights), seed, frame0, _ptr(out), nframes,
+                                    _stream(stream)))
 
     def exact_psf(self, zern, pixels, n, include_tilt, out, stream=None):
         """out (device float [n][T][T]) <- Eq.2 PSFs of the given pixels of one frame."""

@@ -1,0 +1,49 @@
+"""PCA PSF basis (Eq.7, NEXT-1 part): the library's host fit (p2s_fit_basis, C++) against
+the oracle's plain eigen-decomposition, and the oracle against a known low-rank database."""
+import numpy as np
+import pytest
+
+from oracle import exact_psf
+
+
+def test_oracle_pca_recovers_known_low_rank_structure():
+    rng = np.random.default_rng(1)
+    T, n = 7, 400
+    d = T * T
+    Q, _ = np.linalg.qr(rng.standard_normal((d, 3)))
+    mu = rng.uniform(size=d)
+    coeff = rng.standard_normal((n, 3)) * np.array([3.0, 2.0, 1.0])
+    X = mu + coeff @ Q.T
+    basis, res = exact_psf.pca_basis(X.reshape(n, T, T), 3)
+    assert res < 1e-12
+    assert np.allclose(basis[0].ravel(), X.mean(0), atol=1e-12)
+    P = basis[1:].reshape(3, d)
+    assert np.allclose(P @ P.T, np.eye(3), atol=1e-10)
+    # same subspace as the generating one
+    assert np.allclose(np.linalg.svd(P @ Q, compute_uv=False), 1.0, atol=1e-8)
+
+
+def test_library_fit_matches_oracle_on_exact_psfs():
+    from paper_2210_06713_b200 import fit_basis
+    rng = np.random.default_rng(2)
+    T, n, M = 9, 300, 6
+    psfs = []
+    for _ in range(n):
+        a = np.zeros(36)
+        a[3:15] = 0.3 * rng.standard_normal(12)  # higher-order aberrations, Noll 4..15
+        psfs.append(exact_psf.exact_psf(a, T, include_tilt=False))
+    psfs = np.asarray(psfs)
+    got, res = fit_basis(psfs.astype(np.float32), M)
+    ref, res_ref = exact_psf.pca_basis(psfs.astype(np.float32).astype(np.float64), M)
+    assert np.allclose(got[0], ref[0], atol=1e-7)
+    G, R = got[1:].reshape(M, -1).astype(np.float64), ref[1:].reshape(M, -1)
+    assert np.allclose(G @ G.T, np.eye(M), atol=1e-5)
+    # component by component (well-separated leading eigenvalues): same direction
+    assert np.all(np.abs(np.sum(G * R, axis=1)) > 1 - 1e-4)
+    assert abs(res - res_ref) < 1e-6
+
+
+def test_fit_basis_rejects_bad_arguments():
+    from paper_2210_06713_b200 import P2SError, fit_basis
+    with pytest.raises(P2SError):
+        fit_basis(np.zeros((3, 5, 5), np.float32), 3)  # M >= n

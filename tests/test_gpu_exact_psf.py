@@ -74,3 +74,58 @@ def test_exact_tilt_reproduces_the_warp():
     u = np.arange(T) - T // 2
     cx = (h.sum(0) * u).sum()
     assert abs(cx + optics.geometry()[1] * 0.3) < 0.02
+
+
+def test_pca_basis_projection_render_fidelity(tmp_path):
+    """NEXT-1 chain on the GPU: exact PSFs (Eq.2) of sampled Zernike fields form a database,
+    the library fits the PCA basis (Eq.7), each pixel of a held-out frame is projected on
+    it (the ideal P2S weights), and the P2S blur with those weights is compared with the
+    exact Eq.1 render of the same warped image (tilt carried by the warp in both).  SPEC's
+    acceptance target for the P2S render is PSNR >= 40 dB."""
+    import json
+    import os
+    from paper_2210_06713_b200 import Plan, PlanConfig, fit_basis
+    H = W = 128
+    T, M, dr0 = 33, 32, 2.0
+    plan = _plan(H, W, 1, T, dr0)
+    z = torch.empty((4, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 0, 4, z)
+    rng = np.random.default_rng(5)
+    db = []
+    for f in range(3):
+        pix = rng.choice(H * W, 1024, replace=False).astype(np.int32)
+        out = torch.empty((pix.size, T, T), device="cuda")
+        plan.exact_psf(z[f], torch.from_numpy(pix).cuda(), pix.size, False, out)
+        db.append(out.cpu().numpy())
+    basis, residual = fit_basis(np.concatenate(db), M)
+    # held-out frame: exact PSFs of every pixel, projected on the basis
+    allpix = torch.arange(H * W, dtype=torch.int32, device="cuda")
+    psf = torch.empty((H * W, T, T), device="cuda")
+    plan.exact_psf(z[3], allpix, H * W, False, psf)
+    h = psf.cpu().numpy().reshape(H * W, -1).astype(np.float64)
+    mu, Phi = basis[0].reshape(-1).astype(np.float64), basis[1:].reshape(M, -1).astype(np.float64)
+    beta = (h - mu) @ Phi.T
+    recon = mu + beta @ Phi
+    psf_rel = np.linalg.norm(recon - h) / np.linalg.norm(h - mu)
+    weights = np.ascontiguousarray(np.concatenate([np.ones((1, H * W)), beta.T]).reshape(1, M + 1, H, W),
+                                   dtype=np.float32)
+    pb = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=dr0, K=M + 1, taps=T), basis.astype(np.float32),
+              synth.mlp_weights(M + 1, seed=1))
+    img = torch.from_numpy(synth.image(H, W, 1, seed=6)).cuda()
+    warped = torch.empty((1, 1, H, W), device="cuda")
+    pb.warp(img, 0, z[3:4], warped, 1)
+    p2s = torch.empty((1, 1, H, W), device="cuda")
+    pb.blur_weights(warped, torch.from_numpy(weights).cuda(), SEED, 0, p2s, 1)
+    exact = torch.empty((1, H, W), device="cuda")
+    plan.render_exact(warped[0], z[3], False, exact)
+    torch.cuda.synchronize()
+    a, b = p2s.cpu().numpy()[0, 0], exact.cpu().numpy()[0]
+    psnr = 10 * np.log10(1.0 / np.mean((a - b) ** 2))
+    report = {"H": H, "W": W, "T": T, "M": M, "d_over_r0": dr0, "database_psfs": 3 * 1024,
+              "pca_residual_energy": residual, "heldout_psf_rel_err": float(psf_rel), "psnr_db": float(psnr)}
+    dst = os.environ.get("P2S_NEXT1_REPORT")
+    if dst:
+        with open(dst, "w") as f:
+            json.dump(report, f, indent=1)
+    assert psf_rel < np.sqrt(residual) + 0.02, report
+    assert psnr >= 40.0, report

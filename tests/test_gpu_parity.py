@@ -276,6 +276,13 @@ def test_simulate_host_entry_matches_device_entry():
     assert np.array_equal(dev.cpu().numpy(), host)
 
 
+def test_non_contiguous_tensor_is_rejected():
+    plan, *_ = make_plan(32, 32, 1, 2.0, 16, 17)
+    z = torch.empty((1, 36, 32, 64), device="cuda")[..., ::2]  # strided view
+    with pytest.raises(ValueError):
+        plan.sample_zernike(SEED, 0, 1, z)
+
+
 def test_invalid_arguments_fail_loudly():
     from paper_2210_06713_b200 import P2SError, Plan, PlanConfig
     with pytest.raises(P2SError):
