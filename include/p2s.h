@@ -217,6 +217,16 @@ p2s_status p2s_render_exact(p2s_plan p, const float* img, const float* zern, int
  * fp64 covariance, block iteration + Rayleigh-Ritz.  Errors: INVALID_ARGUMENT. */
 p2s_status p2s_fit_basis(const float* psfs, int n, int T, int M, float* basis, double* residual);
 
+/* Host-only: fit the output layer of the P2S network (NEXT-1 readout training).  Keeps W1,
+ * b1, W2, b2 of the packed MLP `mlp_in` (p2s_plan_create layout, input n_in, hidden h1, h2,
+ * output K) and solves (W3, b3) by ridge regression (lambda on W3 only) from the second
+ * hidden layer's activations at the inputs a (host float [n][n_in], Zernike a_4..a_Z) to the
+ * target basis weights beta (host float [n][K], e.g. projections of exact PSFs on the basis).
+ *   mlp_out: host float, packed like mlp_in.  rel_residual: optional ||X Theta - beta||/||beta||.
+ * Errors: INVALID_ARGUMENT, NUMERIC (singular normal equations). */
+p2s_status p2s_fit_readout(const float* mlp_in, int n_in, int h1, int h2, int K, const float* a,
+                           const float* beta, int n, double lambda, float* mlp_out, double* rel_residual);
+
 /* Device Philox4x32-10 test fill: out (dev uint32 [n][4]) <- philox(counter =
  * (i, c1, c2, c3), key = (k0, k1)) for i = 0..n-1. */
 p2s_status p2s_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,

@@ -97,3 +97,21 @@ def pca_basis(psfs: np.ndarray, M: int):
     basis = np.concatenate([mu[None], V]).reshape(M + 1, T, T)
     res = max(0.0, 1.0 - evals[idx].sum() / np.trace(C)) if np.trace(C) > 0 else 0.0
     return basis, res
+
+
+def fit_readout(layers, a: np.ndarray, beta: np.ndarray, lam: float):
+    """Ridge regression of the MLP output layer (NEXT-1 readout training), plain definition:
+    X = [relu(W2 relu(W1 a + b1) + b2), 1]; Theta = argmin ||X Theta - beta||^2 +
+    lam ||Theta[:-1]||^2, solved by lstsq on the stacked system.  layers = unpack_mlp(...)
+    (W3, b3 are replaced).  Returns (W3 [K][h2], b3 [K], relative residual)."""
+    (W1, b1), (W2, b2), _ = layers
+    h = np.maximum(np.asarray(a, np.float64) @ W1.T + b1, 0.0)
+    h = np.maximum(h @ W2.T + b2, 0.0)
+    X = np.concatenate([h, np.ones((h.shape[0], 1))], axis=1)
+    d = X.shape[1]
+    reg = np.sqrt(lam) * np.eye(d)[:-1]  # bias not shrunk
+    A = np.concatenate([X, reg])
+    B = np.concatenate([np.asarray(beta, np.float64), np.zeros((d - 1, beta.shape[1]))])
+    Th = np.linalg.lstsq(A, B, rcond=None)[0]
+    res = np.linalg.norm(X @ Th - beta) / np.linalg.norm(beta)
+    return Th[:-1].T, Th[-1], res

@@ -171,3 +171,90 @@ extern "C" p2s_status p2s_fit_basis(const float* psfs, int n, int T, int M, floa
   if (residual) *residual = trace > 0 ? std::max(0.0, 1.0 - kept / trace) : 0.0;
   return P2S_OK;
 }
+
+// Readout fit for the P2S network (NEXT-1): keep the hidden layers of a packed MLP and
+// solve the output layer (W3, b3) by ridge regression from the second hidden layer's
+// activations to target basis weights beta (e.g. projections of exact PSFs on the PCA
+// basis): (X^T X + lambda I) Theta = X^T beta with X = [h2(a), 1], fp64 Cholesky.
+extern "C" p2s_status p2s_fit_readout(const float* mlp_in, int n_in, int h1, int h2, int K, const float* a,
+                                      const float* beta, int n, double lambda, float* mlp_out,
+                                      double* rel_residual) {
+  if (!mlp_in || !a || !beta || !mlp_out || n_in < 1 || h1 < 1 || h2 < 1 || K < 1 || n < 1 || lambda < 0)
+    return set_error(P2S_ERR_INVALID_ARGUMENT, "p2s_fit_readout: bad argument");
+  const size_t oW1 = 0, ob1 = oW1 + (size_t)h1 * n_in, oW2 = ob1 + h1, ob2 = oW2 + (size_t)h2 * h1,
+               oW3 = ob2 + h2, ob3 = oW3 + (size_t)K * h2, total = ob3 + K;
+  const int d = h2 + 1;
+  std::vector<double> G((size_t)d * d, 0.0), R((size_t)d * K, 0.0);
+  std::vector<double> Xall((size_t)n * d);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < n; ++i) {
+    std::vector<double> z1(h1);
+    for (int u = 0; u < h1; ++u) {
+      double s = mlp_in[ob1 + u];
+      for (int k = 0; k < n_in; ++k) s += (double)mlp_in[oW1 + (size_t)u * n_in + k] * a[(size_t)i * n_in + k];
+      z1[u] = s > 0 ? s : 0.0;
+    }
+    double* x = Xall.data() + (size_t)i * d;
+    for (int v = 0; v < h2; ++v) {
+      double s = mlp_in[ob2 + v];
+      for (int u = 0; u < h1; ++u) s += (double)mlp_in[oW2 + (size_t)v * h1 + u] * z1[u];
+      x[v] = s > 0 ? s : 0.0;
+    }
+    x[h2] = 1.0;
+  }
+  for (int i = 0; i < n; ++i) {
+    const double* x = Xall.data() + (size_t)i * d;
+    for (int p = 0; p < d; ++p) {
+      if (x[p] == 0.0) continue;
+      for (int q = 0; q < d; ++q) G[(size_t)p * d + q] += x[p] * x[q];
+      for (int k = 0; k < K; ++k) R[(size_t)p * K + k] += x[p] * beta[(size_t)i * K + k];
+    }
+  }
+  for (int p = 0; p < h2; ++p) G[(size_t)p * d + p] += lambda;  // the bias is not shrunk
+  // Cholesky G = C C^T (in place, lower), then two triangular solves per output
+  std::vector<double> C = G;
+  for (int j = 0; j < d; ++j) {
+    double s = C[(size_t)j * d + j];
+    for (int k = 0; k < j; ++k) s -= C[(size_t)j * d + k] * C[(size_t)j * d + k];
+    if (!(s > 0.0)) return set_error(P2S_ERR_NUMERIC, "p2s_fit_readout: normal matrix not positive definite");
+    C[(size_t)j * d + j] = std::sqrt(s);
+    for (int i = j + 1; i < d; ++i) {
+      double t = C[(size_t)i * d + j];
+      for (int k = 0; k < j; ++k) t -= C[(size_t)i * d + k] * C[(size_t)j * d + k];
+      C[(size_t)i * d + j] = t / C[(size_t)j * d + j];
+    }
+  }
+  std::vector<double> Th((size_t)d * K);
+  for (int k = 0; k < K; ++k) {
+    std::vector<double> y(d);
+    for (int i = 0; i < d; ++i) {
+      double t = R[(size_t)i * K + k];
+      for (int j = 0; j < i; ++j) t -= C[(size_t)i * d + j] * y[j];
+      y[i] = t / C[(size_t)i * d + i];
+    }
+    for (int i = d - 1; i >= 0; --i) {
+      double t = y[i];
+      for (int j = i + 1; j < d; ++j) t -= C[(size_t)j * d + i] * Th[(size_t)j * K + k];
+      Th[(size_t)i * K + k] = t / C[(size_t)i * d + i];
+    }
+  }
+  std::memcpy(mlp_out, mlp_in, sizeof(float) * oW3);
+  for (int k = 0; k < K; ++k) {
+    for (int v = 0; v < h2; ++v) mlp_out[oW3 + (size_t)k * h2 + v] = (float)Th[(size_t)v * K + k];
+    mlp_out[ob3 + k] = (float)Th[(size_t)h2 * K + k];
+  }
+  if (rel_residual) {
+    double num = 0.0, den = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < K; ++k) {
+        double p = 0.0;
+        for (int q = 0; q < d; ++q) p += Xall[(size_t)i * d + q] * Th[(size_t)q * K + k];
+        const double b = beta[(size_t)i * K + k];
+        num += (p - b) * (p - b);
+        den += b * b;
+      }
+    *rel_residual = den > 0 ? std::sqrt(num / den) : 0.0;
+  }
+  (void)total;
+  return P2S_OK;
+}

@@ -23,7 +23,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NUMERIC", 3: "CUDA", 4: "OUT_OF_M
 # every entry point declared in include/p2s.h
 EXPORTS = ("p2s_plan_create", "p2s_plan_destroy", "p2s_sample_zernike", "p2s_warp", "p2s_blur",
            "p2s_simulate_frames", "p2s_simulate_frames_host", "p2s_last_error", "p2s_plan_info",
-           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_exact_psf", "p2s_render_exact", "p2s_fit_basis", "p2s_blur_weights",
+           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_exact_psf", "p2s_render_exact", "p2s_fit_basis", "p2s_fit_readout", "p2s_blur_weights",
            "p2s_philox_fill",
            "p2s_host_tables", "p2s_grid_size")
 
@@ -67,6 +67,7 @@ def _load():
     lib.p2s_field_autocorr.argtypes = [vp, vp, i32, i32, vp, vp]
     lib.p2s_exact_psf.argtypes = [vp, vp, vp, i32, i32, vp, vp]
     lib.p2s_fit_basis.argtypes = [vp, i32, i32, i32, vp, vp]
+    lib.p2s_fit_readout.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, ctypes.c_double, vp, vp]
     lib.p2s_blur_weights.argtypes = [vp, vp, vp, u64, i64, vp, i32, vp]
     lib.p2s_render_exact.argtypes = [vp, vp, vp, i32, vp, vp]
     lib.p2s_host_tables.argtypes = [i32, i32, ctypes.c_double, ctypes.c_double, i32, vp, vp, vp, vp]
@@ -128,6 +129,19 @@ def fit_basis(psfs, M):
     res = ctypes.c_double()
     _check(lib.p2s_fit_basis(psfs.ctypes.data, n, T, M, basis.ctypes.data, ctypes.byref(res)))
     return basis, res.value
+
+
+def fit_readout(mlp, a, beta, hidden=(100, 100), lam=1e-3):
+    """Ridge fit of the MLP output layer: mlp (packed float32), a [n][n_in], beta [n][K] ->
+    (packed float32 with fitted W3, b3, relative residual)."""
+    mlp = np.ascontiguousarray(mlp, dtype=np.float32)
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    beta = np.ascontiguousarray(beta, dtype=np.float32)
+    out = np.empty_like(mlp)
+    res = ctypes.c_double()
+    _check(lib.p2s_fit_readout(mlp.ctypes.data, a.shape[1], hidden[0], hidden[1], beta.shape[1], a.ctypes.data,
+                               beta.ctypes.data, a.shape[0], float(lam), out.ctypes.data, ctypes.byref(res)))
+    return out, res.value
 
 
 def philox_fill(c1, c2, c3, k0, k1, n, out, stream=None):

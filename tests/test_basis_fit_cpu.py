@@ -47,3 +47,29 @@ def test_fit_basis_rejects_bad_arguments():
     from paper_2210_06713_b200 import P2SError, fit_basis
     with pytest.raises(P2SError):
         fit_basis(np.zeros((3, 5, 5), np.float32), 3)  # M >= n
+
+
+def test_readout_fit_recovers_an_exact_linear_readout():
+    """Targets that ARE a linear readout of the hidden features are fitted exactly (lam = 0),
+    and the library's Cholesky solve equals the oracle's lstsq on general targets."""
+    import synth
+    from paper_2210_06713_b200 import fit_readout
+    K = 7
+    mlp = synth.mlp_weights(K, seed=4)
+    layers = synth.unpack_mlp(mlp, K)
+    rng = np.random.default_rng(7)
+    a = 0.5 * rng.standard_normal((600, 33))
+    (W1, b1), (W2, b2), (W3, b3) = layers
+    h = np.maximum(np.maximum(a @ W1.T + b1, 0) @ W2.T + b2, 0)
+    target = h @ W3.T + b3
+    out, res = fit_readout(mlp, a, target, lam=0.0)
+    assert res < 1e-4
+    l2 = synth.unpack_mlp(out, K)
+    assert np.allclose(l2[2][0], W3, atol=1e-3) and np.allclose(l2[2][1], b3, atol=1e-3)
+    assert np.array_equal(out[: mlp.size - K * 100 - K], mlp[: mlp.size - K * 100 - K])  # hidden layers kept
+    beta = rng.standard_normal((600, K))
+    out, res = fit_readout(mlp, a, beta, lam=0.1)
+    W3o, b3o, res_o = exact_psf.fit_readout(layers, a.astype(np.float32), beta.astype(np.float32), 0.1)
+    l2 = synth.unpack_mlp(out, K)
+    assert np.allclose(l2[2][0], W3o, atol=2e-4) and np.allclose(l2[2][1], b3o, atol=2e-4)
+    assert abs(res - res_o) < 1e-6

@@ -129,3 +129,66 @@ def test_pca_basis_projection_render_fidelity(tmp_path):
             json.dump(report, f, indent=1)
     assert psf_rel < np.sqrt(residual) + 0.02, report
     assert psnr >= 40.0, report
+
+
+def test_trained_readout_p2s_simulator_vs_exact(tmp_path):
+    """NEXT-1 end to end: the P2S network's output layer is fitted (ridge) so that
+    MLP(a_4..a_36) reproduces the PCA projections of exact PSFs; a plan with the PCA basis and
+    the fitted network then runs the full five-step simulator, which is compared with the
+    exact Eq.1 render of the same frame (tilt included there, carried by the warp in P2S)
+    and with the exact tilt-free render of the warped image (isolates the network + basis)."""
+    import json
+    import os
+    from paper_2210_06713_b200 import Plan, PlanConfig, fit_basis, fit_readout
+    H = W = 128
+    T, M, dr0 = 33, 32, 2.0
+    plan = _plan(H, W, 1, T, dr0)
+    F = 7
+    z = torch.empty((F, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 0, F, z)
+    rng = np.random.default_rng(11)
+    psfs, avec = [], []
+    for f in range(F - 1):
+        pix = rng.choice(H * W, 2048, replace=False).astype(np.int32)
+        out = torch.empty((pix.size, T, T), device="cuda")
+        plan.exact_psf(z[f], torch.from_numpy(pix).cuda(), pix.size, False, out)
+        psfs.append(out.cpu().numpy())
+        avec.append(z[f].cpu().numpy().reshape(36, -1)[3:, pix].T)
+    psfs, avec = np.concatenate(psfs), np.concatenate(avec)
+    basis, residual = fit_basis(psfs[:4096], M)
+    mu, Phi = basis[0].reshape(-1).astype(np.float64), basis[1:].reshape(M, -1).astype(np.float64)
+    beta = np.concatenate([np.ones((psfs.shape[0], 1)), (psfs.reshape(len(psfs), -1) - mu) @ Phi.T], axis=1)
+    mlp0 = synth.mlp_weights(M + 1, seed=2)
+    mlp, fit_res = fit_readout(mlp0, avec, beta, lam=1e-4)
+    pb = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=dr0, K=M + 1, taps=T), np.ascontiguousarray(basis, np.float32), mlp)
+    sq, _ = correlation.sqrt_psd_tables(pb.P, pb.Q, optics.geometry()[0], 36)
+    pb.import_sqrtS(sq)
+    img = torch.from_numpy(synth.image(H, W, 1, seed=6)).cuda()
+    f = F - 1  # held out
+    sim = torch.empty((1, 1, H, W), device="cuda")
+    pb.simulate_frames(img, 0, SEED, f, 1, sim)
+    exact = torch.empty((1, H, W), device="cuda")
+    plan.render_exact(img, z[f], True, exact)
+    warped = torch.empty((1, 1, H, W), device="cuda")
+    pb.warp(img, 0, z[f:f + 1], warped, 1)
+    blurred = torch.empty((1, 1, H, W), device="cuda")
+    pb.blur(warped, z[f:f + 1], SEED, f, blurred, 1)
+    exact_nt = torch.empty((1, H, W), device="cuda")
+    plan.render_exact(warped[0], z[f], False, exact_nt)
+    torch.cuda.synchronize()
+
+    def psnr(a, b):
+        return float(10 * np.log10(1.0 / np.mean((a - b) ** 2)))
+    s, e = sim.cpu().numpy()[0, 0], exact.cpu().numpy()[0]
+    report = {"H": H, "W": W, "T": T, "M": M, "d_over_r0": dr0, "train_psfs": int(psfs.shape[0]),
+              "pca_residual_energy": residual, "readout_rel_residual": fit_res,
+              "psnr_simulator_vs_exact_eq1_db": psnr(s, e),
+              "psnr_p2s_blur_vs_exact_tiltfree_on_warped_db": psnr(blurred.cpu().numpy()[0, 0],
+                                                                    exact_nt.cpu().numpy()[0]),
+              "psnr_unblurred_input_vs_exact_db": psnr(img.cpu().numpy()[0], e)}
+    dst = os.environ.get("P2S_NEXT1_TRAINED_REPORT")
+    if dst:
+        with open(dst, "w") as fh:
+            json.dump(report, fh, indent=1)
+    assert report["psnr_p2s_blur_vs_exact_tiltfree_on_warped_db"] >= 35.0, report
+    assert report["psnr_simulator_vs_exact_eq1_db"] > report["psnr_unblurred_input_vs_exact_db"], report
