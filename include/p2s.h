@@ -227,6 +227,21 @@ p2s_status p2s_fit_basis(const float* psfs, int n, int T, int M, float* basis, d
 p2s_status p2s_fit_readout(const float* mlp_in, int n_in, int h1, int h2, int K, const float* a,
                            const float* beta, int n, double lambda, float* mlp_out, double* rel_residual);
 
+/* Validation battery: approximation energies of P:369-397, host fp64.
+ * A_ij(s, phi) = E[a_i(x) a_j(x+s)] of the single-screen model (Hankel form of P:234-238
+ * generalised to i != j), A~ = L diag(c_k) L^T the block-diagonal model of Eq.10 with
+ * c_k = A_kk / A_kk(0).  On the grid s_i = s_max i / ns, ns = max(2, round(n_per_unit s_max)):
+ *   E[i]  = Int_0^{s_i} Int_0^{2pi} tr(A^T A) s' dphi ds'      (modes mode_lo..Z)
+ *   Et[i] = the same with A~,   Em[i] = the same with |tr(A^T A - A~^T A~)|,
+ * radial integral by the cumulative trapezoid.  angle_mean = 0: the printed formulas (the
+ * angular integral as the exact mean over 32 uniform angles); 1: reading Q25 (functions
+ * averaged over the angle before squaring).  s in units of D; D/r0 sets the scale.
+ * Outputs: s_out, E, Et, Em host double [ns+1] (caller-owned).  Errors:
+ * P2S_ERR_INVALID_ARGUMENT for Z outside [4, 66], mode_lo outside [2, Z], s_max <= 0,
+ * n_per_unit < 1 or NULL outputs. */
+p2s_status p2s_correlation_energies(int Z, double d_over_r0, double s_max, int n_per_unit, int angle_mean,
+                                    int mode_lo, double* s_out, double* E, double* Et, double* Em);
+
 /* Device Philox4x32-10 test fill: out (dev uint32 [n][4]) <- philox(counter =
  * (i, c1, c2, c3), key = (k0, k1)) for i = 0..n-1. */
 p2s_status p2s_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
