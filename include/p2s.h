@@ -191,6 +191,25 @@ p2s_status p2s_plan_import_sqrtS(p2s_plan p, const float* sqrtS);
  *   freed on the stream.  Errors: P2S_ERR_INVALID_ARGUMENT for bad sizes / NULL. */
 p2s_status p2s_field_autocorr(p2s_plan p, const float* zern, int nframes, int max_lag, double* out, void* stream);
 
+/* Validation battery: aperture statistics of the sampled Zernike
+ * vectors -- the phase structure function (Fig. struct_fun, against Eq.4) and the
+ * long/short-exposure OTFs H_LE = E[H], H_SE = E[H] of the tilt-corrected phase, H the
+ * pupil autocorrelation.  Pupil: the 32-sample disc of reading Q24.  Every
+ * (frame, pixel) pair is one sample: phi = sum_j a_j Z_j, its residual after the
+ * least-squares plane over the disc, and per lag xi = (dy, dx), dy in [0, 32),
+ * dx in [-31, 31], Delta = phi(x) - phi(x + xi), M the disc mask:
+ *   out[0][dy][dx+31] = mean over samples of sum_x M M' Delta^2 / sum_x M M'  (0 if no overlap)
+ *   out[1][dy][dx+31] = mean of sum_x M M' cos(Delta) / sum_x M         (Re H / H(0), LE)
+ *   out[2][dy][dx+31] = the same for the plane residual                  (SE)
+ *   zern   : device float [nframes][Z][H][W] (the p2s_sample_zernike layout), Z <= 72.
+ *   pixels : device int32 [npix] pixel indices y*W + x used in every frame.
+ *   out    : device double [3][32][63].
+ * Stream-ordered; a temporary partial-sum buffer is allocated and freed on the stream.
+ * Per-sample sums in fp32, across samples in fp64, deterministic.  Errors:
+ * P2S_ERR_INVALID_ARGUMENT for NULL / nframes < 1 / npix < 1. */
+p2s_status p2s_aperture_stats(p2s_plan p, const float* zern, int nframes, const int32_t* pixels, int npix,
+                              double* out, void* stream);
+
 /* Exact-PSF path (partial): the slow per-pixel reference that P2S
  * replaces.  Eq.2: h_x(u) = |F{P e^{-j phi_x}}|^2 with phi_x = sum_j a_j(x) Z_j on
  * a 32-sample pupil zero-padded to a 64-point FFT (PSF pixel = lambda/(2D): a pure tilt moves

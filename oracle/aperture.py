@@ -140,8 +140,8 @@ def model_stats(A0: np.ndarray, Dp: int = PUPIL_D):
             z1, z2 = _overlap(zp, dy, dx)
             r1, r2 = _overlap(zr, dy, dx)
             dz, dr = z1 - z2, r1 - r2
-            v = np.einsum("iyx,ij,jyx->yx", dz, A0, dz)
-            vr = np.einsum("iyx,ij,jyx->yx", dr, A0, dr)
+            v = (dz * np.tensordot(A0, dz, axes=(1, 0))).sum(axis=0)  # dZ^T A0 dZ per position
+            vr = (dr * np.tensordot(A0, dr, axes=(1, 0))).sum(axis=0)
             SF[dy, i] = (w * v).sum() / cnt[dy, i]
             LE[dy, i] = (w * np.exp(-0.5 * v)).sum() / n0
             SE[dy, i] = (w * np.exp(-0.5 * vr)).sum() / n0

@@ -770,6 +770,23 @@ extern "C" p2s_status p2s_render_exact(p2s_plan p, const float* img, const float
   return P2S_OK;
 }
 
+extern "C" p2s_status p2s_aperture_stats(p2s_plan p, const float* zern, int nframes, const int32_t* pixels,
+                                         int npix, double* out, void* stream) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (!zern || !pixels || !out) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (nframes < 1 || npix < 1) return set_error(P2S_ERR_INVALID_ARGUMENT, "nframes >= 1 and npix >= 1 required");
+  if (p->Z > 72) return set_error(P2S_ERR_UNSUPPORTED, "Z <= 72 required");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  P2S_LAUNCH(ensure_pupil_table(p), "pupil table");
+  double* partial = nullptr;
+  P2S_CUDA(cudaMallocAsync(&partial, aperture_partial_bytes((int64_t)nframes * npix), s), "cudaMallocAsync");
+  const int rc = launch_aperture(p, zern, nframes, pixels, npix, partial, out, s);
+  cudaFreeAsync(partial, s);
+  if (rc != 0) return set_error(P2S_ERR_CUDA, std::string("k_aperture: ") + cudaGetErrorString((cudaError_t)rc));
+  return P2S_OK;
+}
+
 extern "C" p2s_status p2s_plan_info(p2s_plan p, int* P, int* Q, size_t* ws, double* clamped, int* max_batch) {
   if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
   if (P) *P = p->P;

@@ -150,6 +150,9 @@ int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair,
 size_t acorr_partial_bytes(int F, int Z, int W, int L);
 int launch_acorr(const float* zern, int F, int Z, int H, int W, int L, double* partial, double* out, cudaStream_t s);
 int ensure_pupil_table(p2s_plan_s* p);
+size_t aperture_partial_bytes(int64_t nsamples);
+int launch_aperture(const p2s_plan_s* p, const float* zern, int nframes, const int* pix, int npix, double* partial,
+                    double* out, cudaStream_t s);
 int launch_exact_psf(const p2s_plan_s* p, const float* zern, const int* pix, int n, int include_tilt, float* out,
                      cudaStream_t s);
 int launch_render_exact(const p2s_plan_s* p, const float* img, const float* zern, int include_tilt, float* out,
