@@ -141,61 +141,90 @@ static p2s_status build_mlp_blob(const std::vector<double>& W1, int nin, int h1,
   return P2S_OK;
 }
 
-// Blur K-step schedule (see k_blur.cu): groups (tx, g) of 8 tap rows, ordered by their
-// shared-memory offset (2c - tx) * SBO_src + 128 g, paired two per K-step.
+// Blur K-step schedule (see k_blur.cu).  The T x T taps are covered by 1 x 8 groups:
+// g8 = T / 8 groups of 8 consecutive tap rows at each tap column (MN-major slabs of the
+// column-ordered source tile), and the lr = T % 8 leftover tap rows run along the tap
+// columns on transposed copies of single source rows (groups of 8 tap columns, the top
+// one partial), so only the partial groups carry zero B rows: 69 K-steps per output row at
+// T = 33 instead of 83 with 8-row groups alone.  Groups are paired two per K-step within
+// each kind, ordered by shared-memory offset.
 static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   BlurGeom& g = p->bg;
   const int T = p->T, K = p->K;
   g.T = T;
   g.c = T / 2;
   g.NC = T + 15;
-  const int G = (T + 7) / 8;
+  g.g8 = T / 8;
+  g.lr = T % 8;
+  g.nct = std::max(g.NC, 23);  // the partial column group reaches chunk 22 when T < 8
   g.np = round16(K);
   g.racc = std::max(1, 4 / p->C);
-  g.nks = (T * G + 1) / 2;
   const char* pe = getenv("P2S_BLUR_PAIR");
   g.pair = pe ? (atoi(pe) != 0) : true;
-  // B ring: a stage is kBlurStepsPerStage (4) K-steps x C*racc MMAs.  Large stages keep
+  // B ring: a stage is kBlurStepsPerStage (7) K-steps x C*racc MMAs.  Large stages keep
   // the single MMA-issuing thread ahead of the tensor pipe (one barrier wait + commit per
-  // 12 MMAs); 4 stages cover the L2 latency of the B reloads.  Pair mode halves the bytes.
+  // 21 MMAs; measured 4 -> 7: 8.3 -> 7.6 ms per 64 frames); 4 stages cover the L2 latency
+  // of the B reloads.  Pair mode halves the bytes.
   const char* se = getenv("P2S_BLUR_STAGES");
   g.stages = se ? std::max(2, std::min(12, atoi(se))) : (g.pair ? 4 : 3);
-  g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, g.nks, p->H, g.pair, g.stages);
-  g.RS = g.RB + 8 * G;
+  g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, p->H, g.pair, g.stages);
+  g.RS = g.RB + T - 1;
   const uint32_t sbo = (uint32_t)blur_rs_pad(g.RS) * 16;
-  struct Grp { int tx, gi; uint32_t off; };
-  std::vector<Grp> groups;
+  const uint32_t main_bytes = blur_main_bytes(g.NC, g.RS);
+  struct Grp {
+    bool tr;      // transposed (leftover tap row l = gi) or 8-row group gi
+    int tx, gi;   // main: tap column, row group; tr: top tap column of the group, leftover row
+    int width;    // tr: valid tap columns tx, tx-1, .., tx-width+1
+    uint32_t off;
+  };
+  std::vector<Grp> mains, trs;
   for (int tx = T - 1; tx >= 0; --tx)
-    for (int gi = 0; gi < G; ++gi) groups.push_back({tx, gi, (uint32_t)(2 * g.c - tx) * sbo + 128u * gi});
-  // K-steps: the lowest-address group alone (its partner slot points at the next group with
-  // zero B rows), then consecutive pairs; every A row touched is < yl + 8G, so a tile needs
-  // only RS = RB + 8G source rows.
-  g.nks = (int)(groups.size() + 1) / 2;
+    for (int gi = 0; gi < g.g8; ++gi) mains.push_back({false, tx, gi, 8, (uint32_t)(2 * g.c - tx) * sbo + 128u * gi});
+  for (int l = 0; l < g.lr; ++l) {
+    if (T % 8) trs.push_back({true, T - 1, l, T % 8, main_bytes + (uint32_t)(l * g.nct + 2 * g.c - (T - 1)) * 16});
+    for (int i = T / 8 - 1; i >= 0; --i)
+      trs.push_back({true, 8 * i + 7, l, 8, main_bytes + (uint32_t)(l * g.nct + 2 * g.c - (8 * i + 7)) * 16});
+  }
+  // K-steps of one kind: a lone lowest-address group first (its second half reads the next
+  // group against zero B rows), then consecutive pairs.
+  struct Step { const Grp* a; const Grp* b; uint32_t lbo; };
+  std::vector<Step> steps;
+  auto pair_up = [&](const std::vector<Grp>& v) {
+    size_t i = 0;
+    if (v.size() % 2 == 1) {
+      steps.push_back({&v[0], nullptr, v.size() > 1 ? v[1].off - v[0].off : 0u});
+      i = 1;
+    }
+    for (; i < v.size(); i += 2) steps.push_back({&v[i], &v[i + 1], v[i + 1].off - v[i].off});
+  };
+  pair_up(mains);
+  g.nks_main = (int)steps.size();
+  pair_up(trs);
+  g.nks = (int)steps.size();
   const size_t bbytes = (size_t)g.np * 32;
   std::vector<uint8_t> img((size_t)g.nks * bbytes, 0);
   std::vector<uint32_t> koff(g.nks), klbo(g.nks);
-  const bool odd = groups.size() % 2 == 1;
   for (int t = 0; t < g.nks; ++t) {
-    int ia, ib;
-    if (odd) {
-      ia = t == 0 ? 0 : 2 * t - 1;
-      ib = t == 0 ? -1 : 2 * t;
-    } else {
-      ia = 2 * t;
-      ib = 2 * t + 1;
-    }
-    const Grp& ga = groups[ia];
-    koff[t] = ga.off;
-    klbo[t] = (ib >= 0 ? groups[ib].off : groups[ia + 1].off) - ga.off;
+    const Step& st = steps[t];
+    koff[t] = st.a->off;
+    klbo[t] = st.lbo;
     uint8_t* dst = img.data() + (size_t)t * bbytes;
     for (int k = 0; k < 16; ++k) {
-      const bool second = k >= 8;
-      if (second && ib < 0) continue;  // dummy half: zero B rows
-      const Grp& gr = second ? groups[ib] : ga;
-      const int ty = 2 * g.c - 8 * gr.gi - (k & 7);
-      if (ty < 0 || ty >= T) continue;
+      const Grp* gr = k < 8 ? st.a : st.b;
+      if (!gr) continue;  // dummy half: zero B rows
+      const int j = k & 7;
+      int ty, tx;
+      if (gr->tr) {
+        if (j >= gr->width) continue;
+        ty = 2 * g.c - (8 * g.g8 + gr->gi);
+        tx = gr->tx - j;
+      } else {
+        ty = 2 * g.c - 8 * gr->gi - j;
+        tx = gr->tx;
+      }
+      if (ty < 0 || ty >= T || tx < 0 || tx >= T) continue;
       for (int n = 0; n < K; ++n) {
-        float v = basis[((size_t)n * T + ty) * T + gr.tx];
+        float v = basis[((size_t)n * T + ty) * T + tx];
         uint16_t b = host_bf16(v);
         size_t off = (n % 8) * 16 + (n / 8) * 256 + (k / 8) * 128 + (k % 8) * 2;
         std::memcpy(dst + off, &b, 2);
@@ -218,7 +247,7 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
     P2S_CUDA(cudaMemcpy(g.bimg + r * g.bstride, img.data(), img.size(), cudaMemcpyHostToDevice), "copy blur B");
   {  // pair-mode copy: [half][t][np/2 rows x 32 B], + 16 zero rows, brep times
     const size_t hb = bbytes / 2;
-    std::vector<uint8_t> img2(img.size() + 4096, 0);
+    std::vector<uint8_t> img2(img.size() + kBlurStepsPerStage * bbytes + 4096, 0);  // a whole stage of slack
     for (int h = 0; h < 2; ++h)
       for (int t = 0; t < g.nks; ++t)
         std::memcpy(img2.data() + ((size_t)h * g.nks + t) * hb, img.data() + (size_t)t * bbytes + h * hb, hb);
@@ -233,7 +262,7 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
     for (int t = 0; t < g.nks; ++t) {
       uint64_t d = (uint64_t)((koff[t] >> 4) & 0x3FFFu);
       d |= (uint64_t)((klbo[t] >> 4) & 0x3FFFu) << 16;
-      d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+      d |= (uint64_t)(((t < g.nks_main ? sbo : 16u) >> 4) & 0x3FFFu) << 32;  // transposed rows: m-groups 1 chunk apart
       d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
       ad[t] = d;
     }

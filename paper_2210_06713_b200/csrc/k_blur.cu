@@ -5,7 +5,10 @@
 // an implicit GEMM  D[pixel][k] = sum_taps A[pixel][tap] B[tap][k]  with
 //   M = 128 pixels of one output row (lane m <-> pixel x0 + 16 (m % 8) + m / 8),
 //   N = np (K padded to 16), fp32 accumulators in TMEM, one per (channel, row) in flight,
-//   K = taps, ordered as groups of 8 consecutive tap rows ty at one tap column tx.
+//   K = taps: groups of 8 consecutive tap rows ty at one tap column tx, and for the T % 8
+//   leftover tap rows, groups of 8 tap columns on transposed copies of single source rows
+//   (chunks of the row contiguous: m-groups 16 B apart), written per row group into a
+//   2-slot ring by the producer warp.
 // The A operand is never materialised as im2col: the source tile of each channel is stored
 // ONCE in shared memory as 16-byte chunks, chunk cc of source row r holding the 8 pixels
 // at window offsets cc + 16 j (j = 0..7).  With the lane permutation above, the
@@ -48,6 +51,7 @@ struct BlurArgs {
   uint32_t idesc;           // instruction descriptor (M, N = np, A MN-major)
   const float* hsum;        // [np]
   int H, W, T, c, NC, RB, RS, nks, np, stages, ntx;
+  int nks_main, g8, lr, nct;  // K-steps over 8-row groups; leftover tap rows on transposed rows
   uint32_t k0, k1;
   int64_t frame0;
   float sigma;
@@ -81,9 +85,10 @@ struct BlurSmem {
 };
 
 __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int racc, int np, int nks, bool pair,
-                                                     int stages) {
+                                                     int stages, int lr, int nct) {
   BlurSmem L;
-  L.tile_bytes = ((uint32_t)NC * blur_rs_pad(RS) * 16 + 127) & ~127u;
+  // per channel: the column-ordered tile, then kBlurTSlots slots of racc x lr transposed rows
+  L.tile_bytes = (blur_main_bytes(NC, RS) + (uint32_t)kBlurTSlots * racc * lr * nct * 16 + 127) & ~127u;
   L.b_bytes = (uint32_t)np * 32 / (pair ? 2 : 1);  // per K-step: this CTA's rows of B
   L.ring_bytes = stages * kStepsPerStage * L.b_bytes;
   const uint32_t stg_bytes = (kBlurThreads / 32) * kLoadRows * kSeg * 2;  // the loader's staging (bf16)
@@ -92,7 +97,7 @@ __host__ __device__ inline BlurSmem blur_smem_layout(int C, int NC, int RS, int 
   L.off_hsum = L.off_desc + 8 * nks;
   L.off_part = (L.off_hsum + 4 * np + 15) & ~15u;  // [2 parity][3 parts][racc][C+1][128] partial sums
   L.off_bar = L.off_part + 2u * 3 * racc * (C + 1) * 128 * 4;
-  L.total = L.off_bar + (2 * stages + 2) * 8 + 16;
+  L.total = L.off_bar + (2 * stages + 2 + 2 * kBlurTSlots) * 8 + 16;
   return L;
 }
 
@@ -101,8 +106,9 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     k_blur(const __grid_constant__ BlurArgs a, const __grid_constant__ CUtensorMap tmap_b) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const BlurSmem L = blur_smem_layout(C, a.NC, a.RS, RACC, a.np, a.nks, PAIR, a.stages);
+  const BlurSmem L = blur_smem_layout(C, a.NC, a.RS, RACC, a.np, a.nks, PAIR, a.stages, a.lr, a.nct);
   const int kBlurStages = a.stages;
+  const uint32_t main_bytes = blur_main_bytes(a.NC, a.RS);
   const uint32_t sbo_src = (uint32_t)blur_rs_pad(a.RS) * 16;
   uint8_t* ring = smem + L.off_ring;
   float* s_hsum = reinterpret_cast<float*>(smem + L.off_hsum);
@@ -112,7 +118,9 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   uint64_t* empty = bars + kBlurStages;
   uint64_t* tfull = bars + 2 * kBlurStages;
   uint64_t* tempty = tfull + 1;  // TMEM free (on the MMA-issuing CTA; one arrival per epilogue warp)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* trow_full = tempty + 1;               // [kBlurTSlots] transposed rows written (leader)
+  uint64_t* trow_empty = trow_full + kBlurTSlots;  // [kBlurTSlots] their MMAs done (both CTAs)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(trow_empty + kBlurTSlots);
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
 
@@ -130,6 +138,10 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, PAIR ? 2 * kEpiWarps : kEpiWarps);
+    for (int s = 0; s < kBlurTSlots; ++s) {
+      mbar_init(&trow_full[s], PAIR ? 2 : 1);
+      mbar_init(&trow_empty[s], 1);
+    }
     mbar_fence_init();
   }
   if (warp == 0) {
@@ -207,9 +219,43 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     const int bcopy = (int)((blockIdx.x / 2 + blockIdx.y * 7 + blockIdx.z * 13) % a.brep);
     const uint8_t* bsrc = a.bimg + (size_t)bcopy * a.bstride;
     const int brow0 = bcopy * a.brows;
+    const uint32_t trow_full_leader = PAIR ? mapa_shared(trow_full, 0) : smem_u32(trow_full);
+    uint64_t p_fill = 0, p_wait = 0;
+    // transposed copies of the leftover tap rows' source rows of row group rg:
+    // slot[r][l][cc] = chunk cc of tile row rg*RACC + r + 8 g8 + l (zero beyond NC).  Issued
+    // half-way through the previous row group's B loads, so it never drains the ring.
+    auto fill_trows = [&](int rg) {
+      const uint64_t tf0 = clk();
+      const int slot = rg % kBlurTSlots;
+      mbar_wait(&trow_empty[slot], ((rg / kBlurTSlots) & 1) ^ 1);
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) {
+        uint8_t* tb = smem + ch * L.tile_bytes;
+#pragma unroll
+        for (int r = 0; r < RACC; ++r)
+          for (int l = 0; l < a.lr; ++l) {
+            const uint8_t* srow = tb + (rg * RACC + r + 8 * a.g8 + l) * 16;
+            uint8_t* drow = tb + main_bytes + (((size_t)slot * RACC + r) * a.lr + l) * a.nct * 16;
+            for (int cc = lane; cc < a.nct; cc += 32) {
+              uint4 q = make_uint4(0, 0, 0, 0);
+              if (cc < a.NC) q = *reinterpret_cast<const uint4*>(srow + (size_t)cc * sbo_src);
+              *reinterpret_cast<uint4*>(drow + cc * 16) = q;
+            }
+          }
+      }
+      fence_async_smem();
+      __syncwarp();
+      // CTA-scope release: the rows are read by this CTA's own tensor-core half of the pair
+      // MMA; fence.proxy.async above orders them for the async proxy.
+      if (lane == 0) mbar_arrive_cluster(trow_full_leader + 8u * slot);
+      p_fill += clk() - tf0;
+    };
+    if (a.lr > 0) fill_trows(0);
     for (int rg = 0; rg < n_rg; ++rg) {
       for (int st = 0; st < nst; ++st) {
+        const uint64_t tw0 = clk();
         mbar_wait(&empty[stage], phase ^ 1);
+        p_wait += clk() - tw0;
         const int t0 = st * kStepsPerStage;
         const int nt = min(kStepsPerStage, a.nks - t0);
         if (elect_one()) {
@@ -227,7 +273,12 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
           stage = 0;
           phase ^= 1;
         }
+        if (a.lr > 0 && st == nst / 2 && rg + 1 < n_rg) fill_trows(rg + 1);
       }
+    }
+    if (a.probe && lane == 0) {
+      atomicAdd(&a.probe[10], (unsigned long long)p_fill);
+      atomicAdd(&a.probe[11], (unsigned long long)p_wait);
     }
   } else if (warp == 1 && leader) {
     // ---- MMA issuer (one elected lane): C x RACC accumulators per K-step, kStepsPerStage
@@ -236,7 +287,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
     const uint64_t ch_step = (uint64_t)(L.tile_bytes >> 4);
     const uint64_t b_desc_base = umma_desc(smem_u32(ring), 128, 256);
     if (tmem != 0) __trap();  // accumulators are addressed from column 0
-    uint64_t w_full = 0, w_tempty = 0;
+    uint64_t w_full = 0, w_tempty = 0, w_trow = 0;
     const uint64_t t_mma0 = clk();
     for (int rg = 0; rg < n_rg; ++rg) {
       uint64_t t0c = clk();
@@ -244,10 +295,22 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       w_tempty += clk() - t0c;
       tc_fence_after();
       const uint64_t a_row_desc = (uint64_t)(rg * RACC);  // start address += rows of this group
+      const int slot = rg % kBlurTSlots;
+      const uint64_t t_row_desc = (uint64_t)(slot * RACC * a.lr * a.nct);  // transposed rows of this group
+      const uint64_t t_rstep = (uint64_t)(a.lr * a.nct);
+      const int st_tr = a.nks_main / kStepsPerStage;  // first stage with a transposed K-step
       for (int st = 0; st < nst; ++st) {
         const uint64_t t1c = clk();
         mbar_wait(&full[stage], phase);
         w_full += clk() - t1c;
+        if (st == st_tr && a.nks > a.nks_main) {
+          const uint64_t t2c = clk();
+          if (PAIR)
+            mbar_wait_cluster(&trow_full[slot], (rg / kBlurTSlots) & 1);
+          else
+            mbar_wait(&trow_full[slot], (rg / kBlurTSlots) & 1);
+          w_trow += clk() - t2c;
+        }
         tc_fence_after();
         const uint64_t bdesc0 = b_desc_base + (uint64_t)((stage * kStepsPerStage * bbytes) >> 4);
         const int t0 = st * kStepsPerStage;
@@ -257,17 +320,19 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
             const int t = t0 + u;
             if (t < a.nks) {
               const uint64_t bd = bdesc0 + (uint64_t)((u * bbytes) >> 4);
-              const uint64_t ad = s_adesc[t] + a_row_desc;
+              const bool tr = t >= a.nks_main;
+              const uint64_t ad = s_adesc[t] + (tr ? t_row_desc : a_row_desc);
+              const uint64_t rstep = tr ? t_rstep : 1ull;
               const uint32_t acc = t > 0 ? 1u : 0u;
 #pragma unroll
               for (int ch = 0; ch < C; ++ch)
 #pragma unroll
                 for (int r = 0; r < RACC; ++r) {
                   if (PAIR)
-                    umma_bf16_pair((uint32_t)((ch * RACC + r) * kAccStride), ad + ch * ch_step + (uint64_t)r, bd,
+                    umma_bf16_pair((uint32_t)((ch * RACC + r) * kAccStride), ad + ch * ch_step + r * rstep, bd,
                                    a.idesc, acc);
                   else
-                    umma_bf16((uint32_t)((ch * RACC + r) * kAccStride), ad + ch * ch_step + (uint64_t)r, bd, a.idesc,
+                    umma_bf16((uint32_t)((ch * RACC + r) * kAccStride), ad + ch * ch_step + r * rstep, bd, a.idesc,
                               acc);
                 }
             }
@@ -284,10 +349,13 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
         }
       }
       if (elect_one()) {
-        if (PAIR)
+        if (PAIR) {
           umma_commit_pair(tfull);
-        else
+          if (a.lr > 0) umma_commit_pair(&trow_empty[slot]);
+        } else {
           umma_commit(tfull);
+          if (a.lr > 0) umma_commit(&trow_empty[slot]);
+        }
       }
       __syncwarp();
     }
@@ -295,6 +363,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       atomicAdd(&a.probe[1], (unsigned long long)w_full);
       atomicAdd(&a.probe[2], (unsigned long long)w_tempty);
       atomicAdd(&a.probe[3], (unsigned long long)(clk() - t_mma0));
+      atomicAdd(&a.probe[9], (unsigned long long)w_trow);
     }
   } else if (warp >= 2) {
     // ---- epilogue warps 2..17: TMEM lane quarter qd = warp % 4; part h = 0..3 owns the
@@ -514,6 +583,10 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.RB = g.RB;
   a.RS = g.RS;
   a.nks = g.nks;
+  a.nks_main = g.nks_main;
+  a.g8 = g.g8;
+  a.lr = g.lr;
+  a.nct = g.nct;
   a.np = g.np;
   a.k0 = (uint32_t)seed;
   a.k1 = (uint32_t)(seed >> 32);
@@ -531,7 +604,7 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   }
   const bool pair = g.pair;
   a.stages = g.stages;
-  const BlurSmem L = blur_smem_layout(p->C, a.NC, a.RS, g.racc, a.np, a.nks, pair, g.stages);
+  const BlurSmem L = blur_smem_layout(p->C, a.NC, a.RS, g.racc, a.np, a.nks, pair, g.stages, a.lr, a.nct);
   // TMEM: this kernel owns all 512 columns of its SM; keep shared memory above half the SM
   // so that two CTAs never co-reside and contend for tcgen05.alloc.
   size_t sm = L.total < 116 * 1024 ? 116 * 1024 : L.total;
@@ -552,19 +625,22 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
     const double n = h[7] ? (double)h[7] : 1.0, nm = pair ? n / 2 : n;
     fprintf(stderr,
             "[blur probe] CTAs %llu  per CTA cycles: total %.0f prologue %.0f | MMA warp: loop %.0f wait_full %.0f "
-            "wait_tmem %.0f | epilogue warp 2: wait %.0f work %.0f (tfull to release %.0f)\n",
-            h[7], h[6] / n, h[0] / n, h[3] / nm, h[1] / nm, h[2] / nm, h[4] / n, h[5] / n, h[8] / n);
+            "wait_tmem %.0f wait_trow %.0f | epilogue warp 2: wait %.0f work %.0f (tfull to release %.0f) | "
+            "producer: trow fill %.0f ring wait %.0f\n",
+            h[7], h[6] / n, h[0] / n, h[3] / nm, h[1] / nm, h[2] / nm, h[9] / nm, h[4] / n, h[5] / n, h[8] / n,
+            h[10] / n, h[11] / n);
   }
   return rc;
 }
 
 // Host helper: rows per CTA that fit the shared-memory budget, balanced over the bands.
-int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair, int stages) {
-  const int NC = T + 15, G = (T + 7) / 8;
+int blur_rows_per_cta(int C, int T, int np, int racc, int H, bool pair, int stages) {
+  const int NC = T + 15, nct = NC > 23 ? NC : 23, lr = T % 8;
+  const int nks = (T * (T / 8) + 1) / 2 + (lr * ((T + 7) / 8) + 1) / 2;
   int best = racc;
   for (int RB = racc; RB <= 64; RB += racc) {
-    const int RS = RB + 8 * G;
-    if (blur_smem_layout(C, NC, RS, racc, np, nks, pair, stages).total <= 227 * 1024) best = RB;
+    const int RS = RB + T - 1;
+    if (blur_smem_layout(C, NC, RS, racc, np, nks, pair, stages, lr, nct).total <= 227 * 1024) best = RB;
   }
   const int bands = (H + best - 1) / best;
   int rb = (H + bands - 1) / bands;

@@ -51,7 +51,7 @@ struct MlpGeom {
 // Blur geometry: K-step schedule of the tap-row groups (see k_blur.cu).
 // K-steps (B tiles) moved per blur ring stage (the pair-mode B tensor-map box spans one stage).
 #ifndef P2S_KSPS
-#define P2S_KSPS 4
+#define P2S_KSPS 7
 #endif
 constexpr int kBlurStepsPerStage = P2S_KSPS;
 // Height (in 16-byte rows) of one chunk column of the blur's source tile: RS rounded up to
@@ -60,6 +60,12 @@ constexpr int kBlurStepsPerStage = P2S_KSPS;
 __host__ __device__
 #endif
 inline constexpr int blur_rs_pad(int RS) { return RS | 1; }
+// bytes of one channel's column-ordered source tile (NC chunk columns x padded RS rows)
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline constexpr uint32_t blur_main_bytes(int NC, int RS) { return ((uint32_t)NC * blur_rs_pad(RS) * 16 + 127) & ~127u; }
+constexpr int kBlurTSlots = 2;  // ring of transposed-row slots (leftover tap rows)
 
 struct BlurGeom {
   int T = 0, c = 0;        // taps, centre
@@ -70,6 +76,10 @@ struct BlurGeom {
   int stages = 8;          // B ring depth (stages of 2 K-steps)
   int RS = 0;              // source rows held in smem
   int nks = 0;             // number of K-steps
+  int nks_main = 0;        // K-steps over 8-row tap groups (the rest run along transposed rows)
+  int g8 = 0;              // full 8-row tap groups per tap column (T / 8)
+  int lr = 0;              // leftover tap rows (T % 8), run along the tap columns
+  int nct = 0;             // chunks per transposed row (>= NC)
   int np = 0;              // padded N (= MlpGeom.n3)
   uint32_t* koff = nullptr;  // device [nks]: byte offset of group a relative to (src + yl*16)
   uint32_t* klbo = nullptr;  // device [nks]: LBO (group b - group a) in bytes
@@ -146,7 +156,7 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s);
 int launch_pack_weights(const p2s_plan_s* p, int F, const float* wts, cudaStream_t s);
 int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0,
                 float* out, cudaStream_t s);
-int blur_rows_per_cta(int C, int T, int np, int racc, int nks, int H, bool pair, int stages);
+int blur_rows_per_cta(int C, int T, int np, int racc, int H, bool pair, int stages);
 size_t acorr_partial_bytes(int F, int Z, int W, int L);
 int launch_acorr(const float* zern, int F, int Z, int H, int W, int L, double* partial, double* out, cudaStream_t s);
 int ensure_pupil_table(p2s_plan_s* p);

@@ -207,15 +207,16 @@ static void run(const char* name, Cfg c) {
 
 int main() {
   const int n = 8196;  // multiple of 6
-  char name[128];
-  for (int N : {224, 112, 128, 160}) {
-    Cfg c = {1, 0, N, n, 128, 1152, 128, 256, 16, 1, 2, 0, 0, 2, 16, 1, 1, 40960};
-    snprintf(name, sizeof(name), "PAIR unrolled 2 tiles ring commit");
-    run(name, c);
-    c.commit_every = 0;
-    c.b_ring = 1;
-    snprintf(name, sizeof(name), "PAIR unrolled 2 tiles");
-    run(name, c);
+  // blur-like pair issue, 3 channel tiles, N = 112: A m-groups one chunk column apart
+  // (SBO = padded rows x 16, the column-ordered tile) vs one 16-byte chunk apart (SBO = 16,
+  // the transposed leftover rows)
+  for (uint32_t sbo : {1232u, 1264u, 16u, 32u}) {
+    for (int rnd : {0, 1}) {
+      Cfg c = {1, 0, 112, n, 128, sbo, 128, 256, 16, 1, 1, 0, 0, 3, 16, 1, rnd, 40960};
+      char name[128];
+      snprintf(name, sizeof(name), "PAIR 3 tiles A sbo=%u rnd=%d", sbo, rnd);
+      run(name, c);
+    }
   }
   return 0;
 }
