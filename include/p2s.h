@@ -246,6 +246,23 @@ p2s_status p2s_fit_basis(const float* psfs, int n, int T, int M, float* basis, d
 p2s_status p2s_fit_readout(const float* mlp_in, int n_in, int h1, int h2, int K, const float* a,
                            const float* beta, int n, double lambda, float* mlp_out, double* rel_residual);
 
+/* P2S network training ("train a small neural network to convert
+ * the Zernike coefficients ... to the PSF coefficients"), host fp64.  Reading Q26: loss
+ * L = 1/(B K) sum_i sum_k (y_ik - beta_ik)^2 over each mini-batch, Adam (beta1 = 0.9,
+ * beta2 = 0.999, eps = 1e-8, bias-corrected), one update per mini-batch; relu'(0) = 0.
+ *   mlp_in  : host float packed [W1 (h1 x n_in), b1, W2 (h2 x h1), b2, W3 (K x h2), b3]
+ *             (the initial weights, e.g. after p2s_fit_readout).
+ *   a, beta : host float [n][n_in] inputs, [n][K] targets.
+ *   order   : host int32 [epochs][n] sample order of each epoch; mini-batches are its
+ *             consecutive chunks of `batch` samples (the last may be shorter).
+ *   mlp_out : host float, same layout (may alias nothing; caller-owned).
+ *   loss_curve: host double [epochs] (nullable): per epoch, the sample-weighted mean of the
+ *             batch losses evaluated before each update.
+ * Errors: P2S_ERR_INVALID_ARGUMENT for sizes < 1, lr <= 0, NULL or out-of-range order. */
+p2s_status p2s_train_mlp(const float* mlp_in, int n_in, int h1, int h2, int K, const float* a,
+                         const float* beta, int n, const int32_t* order, int epochs, int batch, double lr,
+                         float* mlp_out, double* loss_curve);
+
 /* Validation battery: approximation energies of P:369-397, host fp64.
  * A_ij(s, phi) = E[a_i(x) a_j(x+s)] of the single-screen model (Hankel form of P:234-238
  * generalised to i != j), A~ = L diag(c_k) L^T the block-diagonal model of Eq.10 with

@@ -4,5 +4,5 @@ The product path is libp2s.so (include/p2s.h): hand-written sm_100a kernels for 
 five per-frame steps.  This package only binds it (p2s.py).
 """
 from . import runner  # noqa: F401
-from .p2s import (EXPORTS, LIB_PATH, Options, P2SError, Plan, PlanConfig, correlation_energies, fit_basis, fit_readout,  # noqa: F401
+from .p2s import (EXPORTS, LIB_PATH, Options, P2SError, Plan, PlanConfig, correlation_energies, fit_basis, fit_readout, train_mlp,  # noqa: F401
                   grid_size, host_tables, lib, philox_fill)

@@ -23,7 +23,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NUMERIC", 3: "CUDA", 4: "OUT_OF_M
 # every entry point declared in include/p2s.h
 EXPORTS = ("p2s_plan_create", "p2s_plan_destroy", "p2s_sample_zernike", "p2s_warp", "p2s_blur",
            "p2s_simulate_frames", "p2s_simulate_frames_host", "p2s_last_error", "p2s_plan_info",
-           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_exact_psf", "p2s_render_exact", "p2s_fit_basis", "p2s_fit_readout", "p2s_blur_weights", "p2s_correlation_energies", "p2s_aperture_stats",
+           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_exact_psf", "p2s_render_exact", "p2s_fit_basis", "p2s_fit_readout", "p2s_blur_weights", "p2s_correlation_energies", "p2s_aperture_stats", "p2s_train_mlp",
            "p2s_philox_fill",
            "p2s_host_tables", "p2s_grid_size")
 
@@ -69,6 +69,7 @@ def _load():
     lib.p2s_aperture_stats.argtypes = [vp, vp, i32, vp, i32, vp, vp]
     lib.p2s_fit_basis.argtypes = [vp, i32, i32, i32, vp, vp]
     lib.p2s_fit_readout.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, ctypes.c_double, vp, vp]
+    lib.p2s_train_mlp.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, vp, i32, i32, ctypes.c_double, vp, vp]
     lib.p2s_correlation_energies.argtypes = [i32, ctypes.c_double, ctypes.c_double, i32, i32, i32, vp, vp, vp, vp]
     lib.p2s_blur_weights.argtypes = [vp, vp, vp, u64, i64, vp, i32, vp]
     lib.p2s_render_exact.argtypes = [vp, vp, vp, i32, vp, vp]
@@ -153,6 +154,22 @@ def correlation_energies(s_max, n_per_unit=24, Z=36, d_over_r0=1.0, angle_mean=T
     _check(lib.p2s_correlation_energies(Z, float(d_over_r0), float(s_max), n_per_unit, int(bool(angle_mean)),
                                         mode_lo, *[o.ctypes.data for o in out]))
     return tuple(out)
+
+
+def train_mlp(mlp, a, beta, order, batch=256, lr=1e-3, hidden=(100, 100)):
+    """Adam/MSE training of all MLP layers (reading Q26): mlp (packed float32), a [n][n_in],
+    beta [n][K], order int32 [epochs][n] -> (trained packed float32, per-epoch loss)."""
+    mlp = np.ascontiguousarray(mlp, dtype=np.float32)
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    beta = np.ascontiguousarray(beta, dtype=np.float32)
+    order = np.ascontiguousarray(order, dtype=np.int32)
+    epochs = order.shape[0]
+    out = np.empty_like(mlp)
+    curve = np.empty(epochs)
+    _check(lib.p2s_train_mlp(mlp.ctypes.data, a.shape[1], hidden[0], hidden[1], beta.shape[1], a.ctypes.data,
+                             beta.ctypes.data, a.shape[0], order.ctypes.data, epochs, batch, float(lr),
+                             out.ctypes.data, curve.ctypes.data))
+    return out, curve
 
 
 def philox_fill(c1, c2, c3, k0, k1, n, out, stream=None):

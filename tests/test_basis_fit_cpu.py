@@ -73,3 +73,36 @@ def test_readout_fit_recovers_an_exact_linear_readout():
     l2 = synth.unpack_mlp(out, K)
     assert np.allclose(l2[2][0], W3o, atol=2e-4) and np.allclose(l2[2][1], b3o, atol=2e-4)
     assert abs(res - res_o) < 1e-6
+
+
+def test_train_mlp_matches_oracle_training():
+    """p2s_train_mlp (host fp64) follows the oracle's training loop (oracle/train.py,
+    reading Q26) step by step: same sample order, batches, Adam updates -> same weights and
+    loss curve up to summation order."""
+    import synth
+    from oracle import train
+    from paper_2210_06713_b200 import train_mlp
+    K = 5
+    mlp = synth.mlp_weights(K, hidden=(16, 12), seed=6)
+    layers = synth.unpack_mlp(mlp, K, hidden=(16, 12))
+    rng = np.random.default_rng(9)
+    a = (0.5 * rng.standard_normal((300, 33))).astype(np.float32)
+    beta = rng.standard_normal((300, K)).astype(np.float32)
+    order = np.stack([rng.permutation(300) for _ in range(4)]).astype(np.int32)
+    out, curve = train_mlp(mlp, a, beta, order, batch=32, lr=2e-3, hidden=(16, 12))
+    ref, ref_curve = train.train(layers, a.astype(np.float64), beta.astype(np.float64), order, 4, 32, 2e-3)
+    got = synth.unpack_mlp(out, K, hidden=(16, 12))
+    for (Wg, bg), (Wr, br) in zip(got, ref):
+        assert np.allclose(Wg, Wr, rtol=0, atol=1e-6) and np.allclose(bg, br, rtol=0, atol=1e-6)
+    assert np.allclose(curve, ref_curve, rtol=1e-9)
+    assert curve[-1] < curve[0]
+
+
+def test_train_mlp_rejects_bad_order():
+    import synth
+    from paper_2210_06713_b200 import P2SError, train_mlp
+    mlp = synth.mlp_weights(3, seed=1)
+    a = np.zeros((4, 33), np.float32)
+    beta = np.zeros((4, 3), np.float32)
+    with pytest.raises(P2SError):
+        train_mlp(mlp, a, beta, np.array([[0, 1, 2, 4]], np.int32))

@@ -131,7 +131,7 @@ def test_pca_basis_projection_render_fidelity(tmp_path):
     assert psnr >= 40.0, report
 
 
-def test_trained_readout_p2s_simulator_vs_exact(tmp_path):
+def test_trained_p2s_simulator_vs_exact(tmp_path):
     """NEXT-1 end to end: the P2S network's output layer is fitted (ridge) so that
     MLP(a_4..a_36) reproduces the PCA projections of exact PSFs; a plan with the PCA basis and
     the fitted network then runs the full five-step simulator, which is compared with the
@@ -139,7 +139,9 @@ def test_trained_readout_p2s_simulator_vs_exact(tmp_path):
     and with the exact tilt-free render of the warped image (isolates the network + basis)."""
     import json
     import os
-    from paper_2210_06713_b200 import Plan, PlanConfig, fit_basis, fit_readout
+    import time
+    from oracle import pipeline
+    from paper_2210_06713_b200 import Plan, PlanConfig, fit_basis, fit_readout, train_mlp
     H = W = 128
     T, M, dr0 = 33, 32, 2.0
     plan = _plan(H, W, 1, T, dr0)
@@ -160,35 +162,57 @@ def test_trained_readout_p2s_simulator_vs_exact(tmp_path):
     beta = np.concatenate([np.ones((psfs.shape[0], 1)), (psfs.reshape(len(psfs), -1) - mu) @ Phi.T], axis=1)
     mlp0 = synth.mlp_weights(M + 1, seed=2)
     mlp, fit_res = fit_readout(mlp0, avec, beta, lam=1e-4)
-    pb = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=dr0, K=M + 1, taps=T), np.ascontiguousarray(basis, np.float32), mlp)
-    sq, _ = correlation.sqrt_psd_tables(pb.P, pb.Q, optics.geometry()[0], 36)
-    pb.import_sqrtS(sq)
+    # then all layers by Adam/MSE (reading Q26), starting from the readout fit
+    epochs = 150
+    order = np.stack([rng.permutation(len(avec)) for _ in range(epochs)]).astype(np.int32)
+    t0 = time.time()
+    mlp_tr, curve = train_mlp(mlp, avec, beta, order, batch=256, lr=5e-4)
+    train_s = time.time() - t0
+    lt = synth.unpack_mlp(mlp_tr, M + 1)
+    pred = pipeline.mlp(avec.T.astype(np.float64), lt).T
+    tr_res = float(np.linalg.norm(pred - beta) / np.linalg.norm(beta))
     img = torch.from_numpy(synth.image(H, W, 1, seed=6)).cuda()
     f = F - 1  # held out
-    sim = torch.empty((1, 1, H, W), device="cuda")
-    pb.simulate_frames(img, 0, SEED, f, 1, sim)
     exact = torch.empty((1, H, W), device="cuda")
     plan.render_exact(img, z[f], True, exact)
-    warped = torch.empty((1, 1, H, W), device="cuda")
-    pb.warp(img, 0, z[f:f + 1], warped, 1)
-    blurred = torch.empty((1, 1, H, W), device="cuda")
-    pb.blur(warped, z[f:f + 1], SEED, f, blurred, 1)
-    exact_nt = torch.empty((1, H, W), device="cuda")
-    plan.render_exact(warped[0], z[f], False, exact_nt)
-    torch.cuda.synchronize()
 
     def psnr(a, b):
         return float(10 * np.log10(1.0 / np.mean((a - b) ** 2)))
-    s, e = sim.cpu().numpy()[0, 0], exact.cpu().numpy()[0]
+
+    def run(weights):
+        pb = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=dr0, K=M + 1, taps=T), np.ascontiguousarray(basis, np.float32),
+                  weights)
+        sq, _ = correlation.sqrt_psd_tables(pb.P, pb.Q, optics.geometry()[0], 36)
+        pb.import_sqrtS(sq)
+        sim = torch.empty((1, 1, H, W), device="cuda")
+        pb.simulate_frames(img, 0, SEED, f, 1, sim)
+        warped = torch.empty((1, 1, H, W), device="cuda")
+        pb.warp(img, 0, z[f:f + 1], warped, 1)
+        blurred = torch.empty((1, 1, H, W), device="cuda")
+        pb.blur(warped, z[f:f + 1], SEED, f, blurred, 1)
+        exact_nt = torch.empty((1, H, W), device="cuda")
+        plan.render_exact(warped[0], z[f], False, exact_nt)
+        torch.cuda.synchronize()
+        e = exact.cpu().numpy()[0]
+        return psnr(sim.cpu().numpy()[0, 0], e), psnr(blurred.cpu().numpy()[0, 0], exact_nt.cpu().numpy()[0])
+
+    sim_ro, blur_ro = run(mlp)
+    sim_tr, blur_tr = run(mlp_tr)
     report = {"H": H, "W": W, "T": T, "M": M, "d_over_r0": dr0, "train_psfs": int(psfs.shape[0]),
               "pca_residual_energy": residual, "readout_rel_residual": fit_res,
-              "psnr_simulator_vs_exact_eq1_db": psnr(s, e),
-              "psnr_p2s_blur_vs_exact_tiltfree_on_warped_db": psnr(blurred.cpu().numpy()[0, 0],
-                                                                    exact_nt.cpu().numpy()[0]),
-              "psnr_unblurred_input_vs_exact_db": psnr(img.cpu().numpy()[0], e)}
+              "psnr_simulator_vs_exact_eq1_db": sim_ro,
+              "psnr_p2s_blur_vs_exact_tiltfree_on_warped_db": blur_ro,
+              "psnr_unblurred_input_vs_exact_db": psnr(img.cpu().numpy()[0], exact.cpu().numpy()[0]),
+              "trained": {"epochs": epochs, "batch": 256, "lr": 5e-4, "seconds_host": train_s,
+                          "loss_first_last": [float(curve[0]), float(curve[-1])], "rel_residual": tr_res,
+                          "psnr_simulator_vs_exact_eq1_db": sim_tr,
+                          "psnr_p2s_blur_vs_exact_tiltfree_on_warped_db": blur_tr}}
     dst = os.environ.get("P2S_NEXT1_TRAINED_REPORT")
     if dst:
         with open(dst, "w") as fh:
             json.dump(report, fh, indent=1)
     assert report["psnr_p2s_blur_vs_exact_tiltfree_on_warped_db"] >= 35.0, report
     assert report["psnr_simulator_vs_exact_eq1_db"] > report["psnr_unblurred_input_vs_exact_db"], report
+    # training all layers improves on the readout fit (training data and the held-out frame)
+    assert tr_res < fit_res and curve[-1] < curve[0], report
+    assert blur_tr >= blur_ro - 0.2, report
