@@ -167,7 +167,15 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   // of the B reloads.  Pair mode halves the bytes.
   const char* se = getenv("P2S_BLUR_STAGES");
   g.stages = se ? std::max(2, std::min(12, atoi(se))) : (g.pair ? 4 : 3);
-  g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, p->H, g.pair, g.stages);
+  {
+    int nsm = 148;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) nsm = 148;
+    p->nsm = nsm;
+  }
+  p->ntx = (p->W + 127) / 128;
+  const char* rbe = getenv("P2S_BLUR_RB");
+  g.RB = rbe ? std::max(g.racc, atoi(rbe) / g.racc * g.racc)
+             : blur_rows_per_cta(p->C, T, g.np, g.racc, p->H, p->W, g.pair, g.stages, p->max_batch, p->nsm);
   g.RS = g.RB + T - 1;
   const uint32_t sbo = (uint32_t)blur_rs_pad(g.RS) * 16;
   const uint32_t main_bytes = blur_main_bytes(g.NC, g.RS);
@@ -571,15 +579,15 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
       }
     P2S_TRY(build_mlp_blob(W1f, nf, h1, b1, W2, h2, b2, W3, K, b3, p->mg_fold, &p->d_mlp_fold));
   }
-  // ---- basis (step 4)
-  p->basis_host.assign(basis, basis + (size_t)K * T * T);
-  P2S_TRY(build_blur(p, basis));
-  // ---- workspace
+  // ---- workspace size (frames per launch; the blur's band choice depends on it)
   {
     size_t fb = frame_bytes(p);
     int mb = o.max_batch > 0 ? o.max_batch : (int)std::min<size_t>(64, std::max<size_t>(1, ((size_t)12 << 30) / fb));
     p->max_batch = mb;
   }
+  // ---- basis (step 4)
+  p->basis_host.assign(basis, basis + (size_t)K * T * T);
+  P2S_TRY(build_blur(p, basis));
   P2S_TRY(alloc_workspace(p));
   if (p->ar_alpha != 0.f) {
     cudaError_t e = cudaMalloc(&p->d_ar, sizeof(float4) * (size_t)p->npairs * p->P * p->Q);
@@ -713,6 +721,65 @@ extern "C" p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t 
   return P2S_OK;
 }
 
+// Sub-batch sizes for the host entry point.  Modelled compute time of a sub-batch of s frames:
+//   blur_waves(s) x wave time (a partly empty last wave costs a full one)
+//   + ceil(s / 4) x the 512-point row kernel's 4-frame step + s x the linear rest + launches;
+// each sub-batch's device->host copy runs under the next sub-batch's compute (constraint:
+// compute(next) >= copy(previous)), the last copy is the exposed tail.  Minimum over
+// non-increasing size sequences by dynamic programming over (remaining, previous size).
+static std::vector<int> host_schedule(const p2s_plan_s* p, int F) {
+  const char* fix = getenv("P2S_HOST_SUB");
+  if (fix) {
+    const int s = std::max(1, atoi(fix));
+    std::vector<int> v;
+    for (int r = F; r > 0; r -= s) v.push_back(std::min(s, r));
+    return v;
+  }
+  const BlurGeom& g = p->bg;
+  const double px = (double)p->H * p->W / 262144.0;
+  const double row_ms = 8.1e-3 * (double)p->C * g.racc * g.nks / (3.0 * 69.0);
+  const double wave_ms = (g.RB + 2.5) * row_ms;
+  const bool r512 = p->Q == 512 && p->ar_alpha == 0.f;
+  const double r4_ms = r512 ? 0.09 * ((double)p->P * p->Q / 262144.0) * (p->npairs / 18.0) : 0.0;
+  const double lin_ms = 0.04 * px;  // columns + MLP per frame (512^2: ~2.6 ms / 64)
+  const double c_ms = (double)p->C * p->H * p->W * 4.0 / 50e9 * 1e3;
+  auto comp = [&](int s) { return blur_waves(p, s) * wave_ms + ((s + 3) / 4) * r4_ms + s * lin_ms + 0.03; };
+  // best[r][q]: minimal time of r remaining frames after a sub-batch of q frames (q = 0: none)
+  const size_t W1 = (size_t)F + 1;
+  std::vector<double> best(W1 * W1, -1.0);
+  std::vector<int> choice(W1 * W1, 0);
+  for (int r = 1; r <= F; ++r)
+    for (int q = 0; q <= F; ++q) {
+      double bv = 1e300;
+      int bs = 0;
+      const int smax = q ? std::min(r, q) : r;
+      for (int s = 1; s <= smax; ++s) {
+        const double cs = comp(s);
+        if (q && cs < c_ms * q) continue;  // the previous copy would not hide
+        const double rest = s == r ? c_ms * s : best[(size_t)(r - s) * W1 + s];
+        if (rest < 0) continue;
+        if (cs + rest < bv - 1e-12) {
+          bv = cs + rest;
+          bs = s;
+        }
+      }
+      if (bs) {
+        best[(size_t)r * W1 + q] = bv;
+        choice[(size_t)r * W1 + q] = bs;
+      }
+    }
+  std::vector<int> out;
+  int r = F, q = 0;
+  while (r > 0) {
+    int s = choice[(size_t)r * W1 + q];
+    if (s <= 0) s = r;  // no feasible taper (copies slower than compute): one launch
+    out.push_back(s);
+    r -= s;
+    q = s;
+  }
+  return out;
+}
+
 extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host, int64_t img_frame_stride,
                                                uint64_t seed, int64_t frame0, int nframes, float* out_host,
                                                void* stream) {
@@ -729,11 +796,12 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
     P2S_CUDA(cudaEventCreateWithFlags(&p->ev_copied, cudaEventDisableTiming), "cudaEventCreate");
   }
   // The device->host copy of each sub-batch runs on a second stream while the next
-  // sub-batch computes, so the PCIe transfer of the outputs hides behind the kernels.
-  const int sub = std::max(1, std::min(p->max_batch, 8));
+  // sub-batch computes, so the PCIe transfer of the outputs hides behind the kernels; the
+  // sub-batch sizes come from host_schedule (wave-aligned blur launches, short copy tail).
   bool pending = false;
   for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
     const int F = std::min(p->max_batch, nframes - i0);
+    const std::vector<int> subs = host_schedule(p, F);
     if (pending) P2S_CUDA(cudaStreamWaitEvent(s, p->ev_copied, 0), "wait copies");  // d_out / d_img reuse
     if (img_frame_stride == 0) {
       P2S_CUDA(cudaMemcpyAsync(p->d_img, img_host, img_floats * 4, cudaMemcpyHostToDevice, s), "H2D img");
@@ -743,8 +811,8 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
                                  img_floats * 4, cudaMemcpyHostToDevice, s),
                  "H2D img");
     }
-    for (int j0 = 0; j0 < F; j0 += sub) {
-      const int Fs = std::min(sub, F - j0);
+    int j0 = 0;
+    for (const int Fs : subs) {
       p2s_status st = p2s_simulate_frames(p, p->d_img + (img_frame_stride ? (size_t)j0 * img_floats : 0),
                                           img_frame_stride ? (int64_t)img_floats : 0, seed, frame0 + i0 + j0, Fs,
                                           p->d_out + (size_t)j0 * img_floats, stream);
@@ -754,6 +822,7 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
       P2S_CUDA(cudaMemcpyAsync(out_host + (size_t)(i0 + j0) * img_floats, p->d_out + (size_t)j0 * img_floats,
                                (size_t)Fs * img_floats * 4, cudaMemcpyDeviceToHost, p->copy_stream),
                "D2H out");
+      j0 += Fs;
     }
     P2S_CUDA(cudaEventRecord(p->ev_copied, p->copy_stream), "event record");
     pending = true;

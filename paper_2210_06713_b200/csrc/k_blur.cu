@@ -30,6 +30,7 @@
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -634,7 +635,13 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
 }
 
 // Host helper: rows per CTA that fit the shared-memory budget, balanced over the bands.
-int blur_rows_per_cta(int C, int T, int np, int racc, int H, bool pair, int stages) {
+// Output rows per CTA: the largest that fits shared memory is the cheapest per row (the
+// tile's halo and prologue are amortised), but the band count also sets how many CTA
+// (pairs) a launch of F frames has, and a last wave that is mostly empty costs a full wave.
+// Cost model in output-row units: waves(bands) x (RB + 2.5), the 2.5 rows being the
+// per-CTA fixed cost (measured at 512^2 RGB: prologue ~28k cycles = 1.8 rows of 15.4k,
+// plus the last row's epilogue that no MMA overlaps); the cheapest band count wins.
+int blur_rows_per_cta(int C, int T, int np, int racc, int H, int W, bool pair, int stages, int F, int nsm) {
   const int NC = T + 15, nct = NC > 23 ? NC : 23, lr = T % 8;
   const int nks = (T * (T / 8) + 1) / 2 + (lr * ((T + 7) / 8) + 1) / 2;
   int best = racc;
@@ -642,10 +649,35 @@ int blur_rows_per_cta(int C, int T, int np, int racc, int H, bool pair, int stag
     const int RS = RB + T - 1;
     if (blur_smem_layout(C, NC, RS, racc, np, nks, pair, stages, lr, nct).total <= 227 * 1024) best = RB;
   }
-  const int bands = (H + best - 1) / best;
-  int rb = (H + bands - 1) / bands;
-  rb = (rb + racc - 1) / racc * racc;
-  return rb < best ? rb : best;
+  const int ntx = (W + 127) / 128;
+  const int ux = pair ? (ntx + 1) / 2 : ntx;
+  const int slots = std::max(1, pair ? nsm / 2 : nsm);
+  const int b0 = (H + best - 1) / best;
+  int pick = -1;
+  double pick_cost = 0.0;
+  for (int bands = b0; bands <= std::min(H, 3 * b0); ++bands) {
+    int rb = (H + bands - 1) / bands;
+    rb = (rb + racc - 1) / racc * racc;
+    if (rb > best) continue;
+    const int be = (H + rb - 1) / rb;
+    const long long units = (long long)ux * be * std::max(1, F);
+    const long long waves = (units + slots - 1) / slots;
+    const double cost = (double)waves * (rb + 2.5);
+    if (pick < 0 || cost < pick_cost - 1e-9) {
+      pick = rb;
+      pick_cost = cost;
+    }
+  }
+  return pick > 0 ? pick : best;
+}
+
+// Blur waves of a launch of F frames (CTA pairs or CTAs over the SM slots).
+int blur_waves(const p2s_plan_s* p, int F) {
+  const BlurGeom& g = p->bg;
+  const int bands = (p->H + g.RB - 1) / g.RB;
+  const int ux = g.pair ? (p->ntx + 1) / 2 : p->ntx;
+  const int slots = std::max(1, g.pair ? p->nsm / 2 : p->nsm);
+  return (int)(((long long)ux * bands * F + slots - 1) / slots);
 }
 
 }  // namespace p2s

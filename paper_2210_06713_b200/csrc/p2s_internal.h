@@ -125,6 +125,7 @@ struct p2s_plan_s {
   uint16_t* d_Iw = nullptr;     // bf16 [mb][C][H][W]
   uint16_t* d_w = nullptr;      // bf16 [mb][H][ntx][n3/8][128 px][8]: per 128-pixel row tile, 8-basis chunks
   int ntx = 0;                  // 128-pixel tiles per image row
+  int nsm = 148;                // SMs of the plan's device (blur wave accounting)
   CUtensorMap tmap_b;           // 2-D TMA view of bg.bimg2: rows of 256 B, box 2 K-steps of one half
   float* d_img = nullptr;       // staging for the host entry point [mb][C][H][W]
   float* d_out = nullptr;       // staging for the host entry point [mb][C][H][W]
@@ -156,7 +157,8 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s);
 int launch_pack_weights(const p2s_plan_s* p, int F, const float* wts, cudaStream_t s);
 int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0,
                 float* out, cudaStream_t s);
-int blur_rows_per_cta(int C, int T, int np, int racc, int H, bool pair, int stages);
+int blur_rows_per_cta(int C, int T, int np, int racc, int H, int W, bool pair, int stages, int F, int nsm);
+int blur_waves(const p2s_plan_s* p, int F);
 size_t acorr_partial_bytes(int F, int Z, int W, int L);
 int launch_acorr(const float* zern, int F, int Z, int H, int W, int L, double* partial, double* out, cudaStream_t s);
 int ensure_pupil_table(p2s_plan_s* p);

@@ -276,6 +276,24 @@ def test_simulate_host_entry_matches_device_entry():
     assert np.array_equal(dev.cpu().numpy(), host)
 
 
+@pytest.mark.parametrize("F,per_frame_img", [(29, False), (11, True)])
+def test_simulate_host_entry_tapered_sub_batches(F, per_frame_img):
+    """The host entry point splits a batch into tapered sub-batches (wave-aligned blur
+    launches, copies overlapped): results are bit-identical to one device launch, with a
+    broadcast image and with one image per frame."""
+    H, W, C, K, T = 128, 256, 3, 16, 17
+    plan, *_ = make_plan(H, W, C, 2.0, K, T)
+    nimg = F if per_frame_img else 1
+    img = np.stack([synth.image(H, W, C, seed=20 + i) for i in range(nimg)])
+    stride = C * H * W if per_frame_img else 0
+    dev = torch.empty((F, C, H, W), device="cuda")
+    plan.simulate_frames(cuda(img), stride, SEED, 5, F, dev)
+    host = np.empty((F, C, H, W), dtype=np.float32)
+    plan.simulate_frames_host(np.ascontiguousarray(img), stride, SEED, 5, F, host)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.cpu().numpy(), host)
+
+
 def test_non_contiguous_tensor_is_rejected():
     plan, *_ = make_plan(32, 32, 1, 2.0, 16, 17)
     z = torch.empty((1, 36, 32, 64), device="cuda")[..., ::2]  # strided view
