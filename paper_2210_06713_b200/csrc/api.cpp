@@ -154,8 +154,7 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   g.T = T;
   g.c = T / 2;
   g.NC = T + 15;
-  g.g8 = T / 8;
-  g.lr = T % 8;
+  blur_tap_split(T, &g.g8, &g.lr);
   g.nct = std::max(g.NC, 23);  // the partial column group reaches chunk 22 when T < 8
   g.np = round16(K);
   g.racc = std::max(1, 4 / p->C);
@@ -176,7 +175,7 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   const char* rbe = getenv("P2S_BLUR_RB");
   g.RB = rbe ? std::max(g.racc, atoi(rbe) / g.racc * g.racc)
              : blur_rows_per_cta(p->C, T, g.np, g.racc, p->H, p->W, g.pair, g.stages, p->max_batch, p->nsm);
-  g.RS = g.RB + T - 1;
+  g.RS = blur_tile_rows(g.RB, T, g.g8, g.lr);
   const uint32_t sbo = (uint32_t)blur_rs_pad(g.RS) * 16;
   const uint32_t main_bytes = blur_main_bytes(g.NC, g.RS);
   struct Grp {

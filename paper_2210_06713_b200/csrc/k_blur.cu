@@ -642,11 +642,13 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
 // per-CTA fixed cost (measured at 512^2 RGB: prologue ~28k cycles = 1.8 rows of 15.4k,
 // plus the last row's epilogue that no MMA overlaps); the cheapest band count wins.
 int blur_rows_per_cta(int C, int T, int np, int racc, int H, int W, bool pair, int stages, int F, int nsm) {
-  const int NC = T + 15, nct = NC > 23 ? NC : 23, lr = T % 8;
-  const int nks = (T * (T / 8) + 1) / 2 + (lr * ((T + 7) / 8) + 1) / 2;
+  const int NC = T + 15, nct = NC > 23 ? NC : 23;
+  int g8, lr;
+  blur_tap_split(T, &g8, &lr);
+  const int nks = (T * g8 + 1) / 2 + (lr * ((T + 7) / 8) + 1) / 2;
   int best = racc;
   for (int RB = racc; RB <= 64; RB += racc) {
-    const int RS = RB + T - 1;
+    const int RS = blur_tile_rows(RB, T, g8, lr);
     if (blur_smem_layout(C, NC, RS, racc, np, nks, pair, stages, lr, nct).total <= 227 * 1024) best = RB;
   }
   const int ntx = (W + 127) / 128;

@@ -66,6 +66,21 @@ __host__ __device__
 #endif
 inline constexpr uint32_t blur_main_bytes(int NC, int RS) { return ((uint32_t)NC * blur_rs_pad(RS) * 16 + 127) & ~127u; }
 constexpr int kBlurTSlots = 2;  // ring of transposed-row slots (leftover tap rows)
+// Tap-row grouping of the blur: g8 groups of 8 tap rows per tap column and lr leftover tap
+// rows run along the tap columns on transposed source rows (lr = T % 8 when it is at most
+// 3; with more leftover rows the transposed copies cost more shared memory than the
+// padded 8-row group they replace, so the last group is padded instead: lr = 0).
+inline void blur_tap_split(int T, int* g8, int* lr) {
+  if (T % 8 <= 3) {
+    *g8 = T / 8;
+    *lr = T % 8;
+  } else {
+    *g8 = (T + 7) / 8;
+    *lr = 0;
+  }
+}
+// Source rows a tile needs for RB output rows.
+inline int blur_tile_rows(int RB, int T, int g8, int lr) { return lr ? RB + T - 1 : RB + 8 * g8; }
 
 struct BlurGeom {
   int T = 0, c = 0;        // taps, centre

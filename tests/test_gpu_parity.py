@@ -219,6 +219,25 @@ def test_blur_api_vs_oracle(H, W, C, K, T):
         assert rel_l2(got[c], ref[c]) <= 2e-2
 
 
+@pytest.mark.parametrize("C,T", [(1, 5), (2, 7), (3, 9), (1, 15), (3, 25), (2, 63)])
+def test_blur_tap_sizes_vs_oracle(C, T):
+    """Every tap-group shape of the blur's K-step schedule: T < 8 (transposed rows only),
+    T % 8 = 1 (one leftover row), T % 8 = 7 (seven leftover rows), up to T = 63."""
+    H = W = 64
+    K = 16
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T)
+    a = pipeline.sample_zernike(SEED, 0, 1, sq, L, H, W).astype(np.float32)
+    Iw = synth.image(H, W, C, seed=8)[None]
+    out = torch.empty((1, C, H, W), device="cuda")
+    plan.blur(cuda(Iw), cuda(a), SEED, 0, out, 1)
+    torch.cuda.synchronize()
+    w = pipeline.mlp(a[0, 3:].astype(np.float64), synth.unpack_mlp(mlp, K))
+    ref = pipeline.blur(Iw[0].astype(np.float64), w, basis)
+    got = out.cpu().numpy()[0]
+    for c in range(C):
+        assert rel_l2(got[c], ref[c]) <= 2e-2, (C, T, c)
+
+
 # ------------------------------------------------------------------ steps 1-5 fused
 @pytest.mark.parametrize("H,W,C,K,T,dr0,F", [(64, 64, 1, 16, 17, 2.0, 1), (96, 160, 3, 100, 33, 3.0, 2)])
 def test_simulate_vs_oracle(H, W, C, K, T, dr0, F):
