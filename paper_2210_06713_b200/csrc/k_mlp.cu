@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
   }
   const int wmax = na2;  // widest accumulator (n1, n2 or n3)
   const uint32_t cols_wg = wmax <= 32 ? 32 : wmax <= 64 ? 64 : wmax <= 128 ? 128 : 256;
-  const uint32_t ncols = nwg * cols_wg;  // <= 512 (the launcher picks nwg)
+  uint32_t ncols = 32;  // tcgen05.alloc takes a power of two >= 32: round nwg * cols_wg up
+  while (ncols < nwg * cols_wg) ncols <<= 1;  // <= 512 (the launcher picks nwg)
   if (warp == 0) tmem_alloc(tslot, ncols);
   tc_fence_before();
   __syncthreads();

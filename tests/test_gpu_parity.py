@@ -238,6 +238,26 @@ def test_blur_tap_sizes_vs_oracle(C, T):
         assert rel_l2(got[c], ref[c]) <= 2e-2, (C, T, c)
 
 
+@pytest.mark.parametrize("C,K,T", [(4, 128, 33), (1, 1, 3), (2, 100, 17), (4, 100, 33), (3, 128, 33), (4, 64, 17)])
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_blur_extreme_shapes_vs_oracle(C, K, T, pair, monkeypatch):
+    """Edges of the accepted shapes (C = 4, K = 128 = the widest accumulator, K = 1) in both
+    blur modes: CTA pairs (cta_group::2, M = 256) and single CTAs (P2S_BLUR_PAIR=0)."""
+    monkeypatch.setenv("P2S_BLUR_PAIR", pair)
+    H, W = 72, 136
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T)
+    a = pipeline.sample_zernike(SEED, 0, 1, sq, L, H, W).astype(np.float32)
+    Iw = synth.image(H, W, C, seed=9)[None]
+    out = torch.empty((1, C, H, W), device="cuda")
+    plan.blur(cuda(Iw), cuda(a), SEED, 0, out, 1)
+    torch.cuda.synchronize()
+    w = pipeline.mlp(a[0, 3:].astype(np.float64), synth.unpack_mlp(mlp, K))
+    ref = pipeline.blur(Iw[0].astype(np.float64), w, basis)
+    got = out.cpu().numpy()[0]
+    for c in range(C):
+        assert rel_l2(got[c], ref[c]) <= 2e-2, (C, K, T, pair, c)
+
+
 # ------------------------------------------------------------------ steps 1-5 fused
 @pytest.mark.parametrize("H,W,C,K,T,dr0,F", [(64, 64, 1, 16, 17, 2.0, 1), (96, 160, 3, 100, 33, 3.0, 2)])
 def test_simulate_vs_oracle(H, W, C, K, T, dr0, F):
