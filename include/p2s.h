@@ -70,7 +70,9 @@ typedef struct {
   double s_per_px;          /* lag per pixel in units of D; >0 overrides L*lambda/(2 D^2) (Q5) */
   double tilt_px_per_rad;   /* kappa_t pixels per unit a_2; >0 overrides 4/pi (Q12)  */
   int    pad;               /* FFT grid P x Q = next 5-smooth >= pad*(H,W); default 1 (Q6) */
-  int    mlp_hidden[2];     /* hidden widths, default {100, 100}; each <= 256        */
+  int    mlp_hidden[2];     /* hidden widths, default {100, 100}; each <= 256, and the
+                               bf16 weight images must fit shared memory next to one
+                               128-pixel tile (UNSUPPORTED otherwise; <= 128 always fits) */
   int    max_batch;         /* frames per internal chunk (workspace sizing); 0 = auto */
   float  ar_alpha;          /* AR(1) coefficient on the spectral noise in [0,1), default 0 (Q18) */
   float  noise_sigma;       /* step 5 additive Gaussian noise sigma, default 0       */

@@ -577,6 +577,17 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
         W1f[(size_t)h * nf + s] = acc;
       }
     P2S_TRY(build_mlp_blob(W1f, nf, h1, b1, W2, h2, b2, W3, K, b3, p->mg_fold, &p->d_mlp_fold));
+    // k_mlp keeps all three weight images resident in shared memory next to at least one
+    // tile pipeline (A1 + A2 images): wide hidden layers with many modes may not fit.
+    for (const MlpGeom* g : {&p->mg_plain, &p->mg_fold}) {
+      const size_t need = ((g->blob_bytes + 127) & ~(size_t)127) + 128 * (size_t)g->k1 * 2 +
+                          128 * (size_t)std::max(std::max(g->n1, g->n2), g->n3) * 2 + 96;
+      if (need > 227 * 1024) {
+        free_plan(p);
+        return set_error(P2S_ERR_UNSUPPORTED, "MLP weights + one tile pipeline exceed 227 KB of shared memory "
+                                              "(reduce mlp_hidden or Z)");
+      }
+    }
   }
   // ---- workspace size (frames per launch; the blur's band choice depends on it)
   {

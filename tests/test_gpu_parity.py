@@ -274,6 +274,34 @@ def test_simulate_vs_oracle(H, W, C, K, T, dr0, F):
             assert rel_l2(got[f, c], ref[f, c]) <= 2e-2, (f, c, rel_l2(got[f, c], ref[f, c]))
 
 
+@pytest.mark.parametrize("H,W,C,K,T,Z,hidden,max_batch,F", [
+    (37, 41, 4, 128, 33, 66, (128, 128), 0, 1),   # maxima; odd, non-5-smooth image sizes
+    (40, 48, 1, 1, 3, 4, (8, 8), 0, 2),           # minima
+    (64, 64, 2, 16, 17, 36, (100, 100), 3, 7),    # more frames than the workspace holds
+])
+def test_simulate_shape_limits_vs_oracle(H, W, C, K, T, Z, hidden, max_batch, F):
+    mlp = synth.mlp_weights(K, hidden=hidden, n_in=Z - 3, seed=3)
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 2.5, K, T, Z=Z, mlp=mlp, mlp_hidden=hidden, max_batch=max_batch)
+    img = synth.image(H, W, C, seed=12)
+    out = torch.empty((F, C, H, W), device="cuda")
+    plan.simulate_frames(cuda(img), 0, SEED, 2, F, out)
+    torch.cuda.synchronize()
+    ref = pipeline.simulate(img[None], True, SEED, 2, F, sq, L, basis,
+                            synth.unpack_mlp(mlp, K, hidden=hidden, n_in=Z - 3), optics.geometry()[1])
+    got = out.cpu().numpy()
+    for f in range(F):
+        for c in range(C):
+            assert rel_l2(got[f, c], ref[f, c]) <= 2e-2, (f, c, rel_l2(got[f, c], ref[f, c]))
+
+
+def test_oversized_mlp_is_unsupported():
+    from paper_2210_06713_b200 import P2SError, Plan, PlanConfig
+    with pytest.raises(P2SError) as e:
+        Plan(PlanConfig(H=64, W=64, C=1, d_over_r0=1.0, Z=66, K=128, taps=17, mlp_hidden=(256, 256)),
+             synth.basis(128, 17), synth.mlp_weights(128, hidden=(256, 256), n_in=63))
+    assert e.value.status == 5  # P2S_ERR_UNSUPPORTED
+
+
 def test_simulate_step5_vs_oracle():
     H, W, C, K, T = 64, 96, 2, 16, 17
     plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T, noise_sigma=0.05, clamp01=True)
