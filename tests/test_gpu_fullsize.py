@@ -66,6 +66,41 @@ def test_512_rgb_bench_config_vs_oracle_sampled():
             assert rel_l2(got[f, c, ys, xs], ref[c]) <= 2e-2
 
 
+def test_1080p_rgb_vs_oracle_sampled():
+    """cfg4's geometry (1080 x 1920 RGB, D/r0 = 4, K = 100, T = 33: generic mixed-radix FFTs,
+    separate warp kernel, 15 x-tiles with a ragged last one): step-1 fields on every pixel
+    of two modes, the final output on sampled pixels, one frame."""
+    import bench
+    H, W, C, K, T, dr0, F = 1080, 1920, 3, 100, 33, 4.0, 1
+    st5 = bench.STEP5
+    plan, basis, mlp = _plan(H, W, C, dr0, K, T, max_batch=8, **st5)
+    s_px, kappa = optics.geometry()
+    sq, _ = correlation.sqrt_psd_tables(plan.P, plan.Q, s_px, 36)
+    plan.import_sqrtS(sq)
+    img = synth.image(H, W, C, seed=3)
+    out = torch.empty((F, C, H, W), device="cuda")
+    plan.simulate_frames(torch.from_numpy(img).cuda(), 0, SEED, 11, F, out)
+    z = torch.empty((F, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 11, F, z)
+    torch.cuda.synchronize()
+    got, zg = out.cpu().numpy(), z.cpu().numpy()
+    L = optics.noll_cholesky(optics.noll_covariance(36, dr0))
+    layers = synth.unpack_mlp(mlp, K)
+    rng = np.random.default_rng(1)
+    ys = np.concatenate([rng.integers(0, H, 400), [0, H - 1, 0, H - 1, 540]])
+    xs = np.concatenate([rng.integers(0, W, 400), [0, W - 1, W - 1, 0, 1919]])
+    eta = next(iter(pipeline.spectral_noise_sequence(SEED, 11, 1, plan.P, plan.Q, 0.0, 36)))
+    a = pipeline.mix(pipeline.fields_from_noise(eta, sq, H, W), L)
+    for j in (1, 2, 7, 35):
+        assert rel_l2(zg[0, j], a[j]) <= 1e-4, j
+    Iw = pipeline.warp(img, a[1], a[2], kappa)
+    w_at = pipeline.mlp(a[3:, ys, xs][:, :, None], layers)[:, :, 0].T
+    ref = pipeline.step5_at(pipeline.blur_at(Iw, w_at, basis, ys, xs), w_at, basis, SEED, 11, ys, xs, W,
+                            sigma=st5["noise_sigma"], normalize=st5["normalize_psf_sum"], clamp01=st5["clamp01"])
+    for c in range(C):
+        assert rel_l2(got[0, c, ys, xs], ref[c]) <= 2e-2
+
+
 @pytest.mark.parametrize("H,W,dr0,F", [(1080, 1920, 4.0, 8), (2160, 3840, 5.0, 2)])
 def test_fullsize_field_statistics(H, W, dr0, F):
     plan, *_ = _plan(H, W, 3, dr0, 100, 33, max_batch=F)
