@@ -118,6 +118,16 @@ p2s_status p2s_plan_destroy(p2s_plan p);
 p2s_status p2s_sample_zernike(p2s_plan p, uint64_t seed, int64_t frame0, int nframes,
                               float* zern, void* stream);
 
+/* Step 1 from caller-supplied spectral noise (parity entry: identical host-generated noise
+ * on both sides, BASELINE north_star).  eta: device complex64 (float2) [nframes][Z-1][P][Q]
+ * (P x Q = the plan's FFT grid, p2s_plan_info), mode slot m <-> Noll j = m + 2: the
+ * Hermitian spectral noise of reading Q8 (canonical bin sqrt(PQ/2)(g1 + i g2), mirror bin
+ * its conjugate, self-conjugate bins sqrt(PQ) g1).  Runs Y = sqrt(S_a) eta_a + i sqrt(S_b)
+ * eta_b, the 2-D inverse DFT, the crop and the mixing a = L f exactly like
+ * p2s_sample_zernike (each bin read as stored; no AR state, no frozen flow) into
+ * zern (device float [nframes][Z][H][W]). */
+p2s_status p2s_sample_zernike_from_noise(p2s_plan p, const float* eta, int nframes, float* zern, void* stream);
+
 /* Step 2: warped (dev float [nframes][C][H][W]) <- bilinear(img, x + kappa (a_2, a_3)).
  *   img              dev float [..][C][H][W]; frame i uses img + i*img_frame_stride
  *                    (in floats; 0 = one image broadcast to all frames)

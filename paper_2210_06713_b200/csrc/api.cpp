@@ -646,6 +646,26 @@ extern "C" p2s_status p2s_sample_zernike(p2s_plan p, uint64_t seed, int64_t fram
   return P2S_OK;
 }
 
+extern "C" p2s_status p2s_sample_zernike_from_noise(p2s_plan p, const float* eta, int nframes, float* zern,
+                                                    void* stream) {
+  const int64_t frame0 = 0;
+  CHECK_PLAN();
+  if (nframes == 0) return P2S_OK;
+  if (!eta || !zern) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t per = (size_t)p->Z * p->H * p->W;
+  const size_t eper = (size_t)p->nslots * p->P * p->Q;  // complex values per frame
+  for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
+    const int F = std::min(p->max_batch, nframes - i0);
+    P2S_LAUNCH(launch_rows(p, 0, 0, F, false, 0, 0, s, reinterpret_cast<const float2*>(eta) + eper * i0),
+               "k_rows (given noise)");
+    P2S_LAUNCH(launch_cols(p, F, 0, zern + per * i0, s), "k_cols");
+    P2S_LAUNCH(launch_mix(p, F, zern + per * i0, s), "k_mix");
+  }
+  return P2S_OK;
+}
+
 extern "C" p2s_status p2s_warp(p2s_plan p, const float* img, int64_t img_frame_stride, const float* zern,
                                float* warped, int nframes, void* stream) {
   const int64_t frame0 = 0;

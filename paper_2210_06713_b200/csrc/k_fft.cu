@@ -257,6 +257,8 @@ struct RowArgs {
   int F;
   float alpha, calpha;
   int64_t t_start;      // first frame evolved (AR replay starts at 0)
+  const float2* eta;    // caller-supplied spectral noise [F][nslots][P][Q] (from_noise entry), or null
+  int nslots;
   int load_state;       // AR: state holds eta_{frame0-1}
   int flow;             // frozen flow: frame-0 noise translated by (vx, vy) * frame pixels
   double vx, vy;
@@ -325,10 +327,23 @@ __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
     const int64_t fr_noise = a.flow ? 0 : fr;  // frozen flow: one realisation, translated
     const float2 phy = a.flow ? flow_phase(ky, a.P, a.vy * (double)fr) : make_float2(1.f, 0.f);
     for (int kx = threadIdx.x; kx < Q; kx += NT) {
-      const float4 z = spectral_noise(ky, kx, a.P, Q, p, fr_noise, a.k0, a.k1);
       const int km = kx ? Q - kx : 0;
+      float4 z, zm;
+      if (a.eta) {  // given eta (reading Q8 scaling): zeta = eta / sqrt(PQ/2), each bin read as stored
+        const float inv = rsqrtf(0.5f * (float)a.P * (float)Q);
+        const size_t PQ = (size_t)a.P * Q;
+        const float2* ea = a.eta + ((size_t)t * a.nslots + 2 * p) * PQ;
+        const bool hb = 2 * p + 1 < a.nslots;
+        const float2 a0 = ea[(size_t)ky * Q + kx], b0 = hb ? ea[PQ + (size_t)ky * Q + kx] : make_float2(0.f, 0.f);
+        const float2 a1 = ea[(size_t)k1 * Q + km], b1 = hb ? ea[PQ + (size_t)k1 * Q + km] : make_float2(0.f, 0.f);
+        z = make_float4(a0.x * inv, a0.y * inv, b0.x * inv, b0.y * inv);
+        zm = make_float4(a1.x * inv, a1.y * inv, b1.x * inv, b1.y * inv);
+      } else {
+        z = spectral_noise(ky, kx, a.P, Q, p, fr_noise, a.k0, a.k1);
+        zm = make_float4(z.x, -z.y, z.z, -z.w);  // mirror: conjugate noise
+      }
       float2 y0 = spectrum(sS[kx], z);
-      float2 y1 = spectrum(sS[Q + km], make_float4(z.x, -z.y, z.z, -z.w));  // mirror: conjugate noise
+      float2 y1 = spectrum(sS[Q + km], zm);
       if (a.flow) {  // the mirror bin's factor is the conjugate (Hermitian shift factors)
         const float2 ph = cmul(phy, flow_phase(kx, Q, a.vx * (double)fr));
         y0 = cmul(y0, ph);
@@ -493,7 +508,7 @@ static int getenv_flag(const char* name) {
 }
 
 int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool ar, int ar_mode,
-                int64_t replay_from, cudaStream_t s) {
+                int64_t replay_from, cudaStream_t s, const float2* eta) {
   RowArgs a;
   fill_fft_args(a.fq, pl->fq);
   a.sqrtS = pl->d_sqrtS;
@@ -513,6 +528,16 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
   a.flow = (pl->flow_vx != 0.0 || pl->flow_vy != 0.0) ? 1 : 0;
   a.vx = pl->flow_vx;
   a.vy = pl->flow_vy;
+  a.eta = eta;
+  a.nslots = pl->nslots;
+  if (eta) {  // caller-supplied noise: generic row kernel, no AR state, no flow
+    a.flow = 0;
+    dim3 grid(pl->P / 2 + 1, pl->npairs);
+    size_t sm = ((size_t)3 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
+    cudaFuncSetAttribute(k_rows_pair<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_rows_pair<256><<<grid, 256, sm, s>>>(a);
+    return (int)cudaGetLastError();
+  }
   if (ar) {
     dim3 grid(pl->P, pl->npairs);
     size_t sm = ((size_t)2 * pl->Q + 2 * padded_len(pl->Q)) * sizeof(float2) + (size_t)pl->Q * sizeof(float4) + 16;

@@ -160,7 +160,7 @@ struct p2s_plan_s {
 namespace p2s {
 // ---- kernel launchers (k_*.cu); all return cudaGetLastError() as int ----
 int launch_rows(const p2s_plan_s* p, uint64_t seed, int64_t frame0, int F, bool ar, int ar_mode,
-                int64_t replay_from, cudaStream_t s);
+                int64_t replay_from, cudaStream_t s, const float2* eta = nullptr);
 int launch_cols(const p2s_plan_s* p, int F, int mode, float* zern, cudaStream_t s, const float* img = nullptr,
                 int64_t img_stride = 0, bool* warp_fused = nullptr);
 int launch_mix(const p2s_plan_s* p, int F, float* zern, cudaStream_t s);

@@ -23,7 +23,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NUMERIC", 3: "CUDA", 4: "OUT_OF_M
 # every entry point declared in include/p2s.h
 EXPORTS = ("p2s_plan_create", "p2s_plan_destroy", "p2s_sample_zernike", "p2s_warp", "p2s_blur",
            "p2s_simulate_frames", "p2s_simulate_frames_host", "p2s_last_error", "p2s_plan_info",
-           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_exact_psf", "p2s_render_exact", "p2s_fit_basis", "p2s_fit_readout", "p2s_blur_weights", "p2s_correlation_energies", "p2s_aperture_stats", "p2s_train_mlp",
+           "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_exact_psf", "p2s_render_exact", "p2s_fit_basis", "p2s_fit_readout", "p2s_blur_weights", "p2s_correlation_energies", "p2s_aperture_stats", "p2s_train_mlp", "p2s_sample_zernike_from_noise",
            "p2s_philox_fill",
            "p2s_host_tables", "p2s_grid_size")
 
@@ -69,6 +69,7 @@ def _load():
     lib.p2s_aperture_stats.argtypes = [vp, vp, i32, vp, i32, vp, vp]
     lib.p2s_fit_basis.argtypes = [vp, i32, i32, i32, vp, vp]
     lib.p2s_fit_readout.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, ctypes.c_double, vp, vp]
+    lib.p2s_sample_zernike_from_noise.argtypes = [vp, vp, i32, vp, vp]
     lib.p2s_train_mlp.argtypes = [vp, i32, i32, i32, i32, vp, vp, i32, vp, i32, i32, ctypes.c_double, vp, vp]
     lib.p2s_correlation_energies.argtypes = [i32, ctypes.c_double, ctypes.c_double, i32, i32, i32, vp, vp, vp, vp]
     lib.p2s_blur_weights.argtypes = [vp, vp, vp, u64, i64, vp, i32, vp]
@@ -251,6 +252,10 @@ class Plan:
     def field_autocorr(self, zern, nframes, max_lag, out, stream=None):
         """out (device float64 [Z][2][max_lag]) <- periodic auto-correlation of zern along x, y."""
         _check(lib.p2s_field_autocorr(self._h, _ptr(zern), nframes, max_lag, _ptr(out), _stream(stream)))
+
+    def sample_zernike_from_noise(self, eta, nframes, zern, stream=None):
+        """Step 1 from given spectral noise: eta device complex64 [F][Z-1][P][Q] -> zern."""
+        _check(lib.p2s_sample_zernike_from_noise(self._h, _ptr(eta), nframes, _ptr(zern), _stream(stream)))
 
     def aperture_stats(self, zern, nframes, pixels, out, stream=None):
         """out (device float64 [3][32][63]) <- structure function, LE and SE OTF of the pupil

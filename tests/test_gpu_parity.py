@@ -81,6 +81,27 @@ def test_sample_zernike_vs_oracle(H, W, dr0, frame0, F):
     assert worst <= 1e-4, worst
 
 
+@pytest.mark.parametrize("H,W,dr0,F", [(64, 64, 2.0, 2), (60, 90, 3.0, 1), (512, 96, 1.0, 1)])
+def test_sample_zernike_from_host_noise_vs_oracle(H, W, dr0, F):
+    """North_star parity on identical host-generated noise: the oracle's spectral noise
+    (reading Q8, its own Philox) is handed to p2s_sample_zernike_from_noise; the fields match
+    the oracle's IDFT + mixing of the same noise, and the library's own Philox path."""
+    plan, _, _, sq, L = make_plan(H, W, 1, dr0, 16, 17)
+    etas = list(pipeline.spectral_noise_sequence(SEED, 4, F, plan.P, plan.Q, 0.0, 36))
+    eta = torch.from_numpy(np.stack(etas).astype(np.complex64)).cuda()
+    z = torch.empty((F, 36, H, W), device="cuda")
+    plan.sample_zernike_from_noise(eta, F, z)
+    z2 = torch.empty_like(z)
+    plan.sample_zernike(SEED, 4, F, z2)
+    torch.cuda.synchronize()
+    got, own = z.cpu().numpy(), z2.cpu().numpy()
+    for f in range(F):
+        ref = pipeline.mix(pipeline.fields_from_noise(etas[f], sq, H, W), L)
+        assert np.all(got[f, 0] == 0)
+        assert max(rel_l2(got[f, j], ref[j]) for j in range(1, 36)) <= 1e-4
+        assert max(rel_l2(got[f, j], own[f, j]) for j in range(1, 36)) <= 1e-5
+
+
 @pytest.mark.parametrize("H,W,F", [(512, 96, 2), (96, 512, 3), (512, 512, 1)])
 def test_sample_zernike_register_fft_path_vs_oracle(H, W, F):
     """512-point axes take the register-resident radix-8 kernels (rows: Q = 512, columns:
