@@ -323,6 +323,46 @@ def test_oversized_mlp_is_unsupported():
     assert e.value.status == 5  # P2S_ERR_UNSUPPORTED
 
 
+def test_simulate_ar_sequence_vs_oracle():
+    """Steps 1-5 on an AR(1) sequence (reading Q18): a fresh start and the stored-state
+    continuation both follow the oracle's replayed sequence."""
+    H, W, C, K, T, alpha = 64, 96, 2, 16, 17, 0.9
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 3.0, K, T, ar_alpha=alpha)
+    img = synth.image(H, W, C, seed=13)
+    out = torch.empty((5, C, H, W), device="cuda")
+    plan.simulate_frames(cuda(img), 0, SEED, 0, 3, out[:3])
+    plan.simulate_frames(cuda(img), 0, SEED, 3, 2, out[3:])  # continues from the stored state
+    torch.cuda.synchronize()
+    ref = pipeline.simulate(img[None], True, SEED, 0, 5, sq, L, basis, synth.unpack_mlp(mlp, K),
+                            optics.geometry()[1], alpha=alpha)
+    got = out.cpu().numpy()
+    for f in range(5):
+        for c in range(C):
+            assert rel_l2(got[f, c], ref[f, c]) <= 2e-2, (f, c)
+
+
+def test_simulate_psf_sum_normalisation_vs_oracle():
+    """Step 5 normalisation (reading Q16): out / sum_k w_k sum_u h_k(u), with a network whose
+    weights are positive everywhere (W3 >= 0, b3 > 0 after ReLU features) so the divisor is
+    well conditioned."""
+    H, W, C, K, T = 64, 64, 3, 16, 17
+    layers = synth.unpack_mlp(synth.mlp_weights(K, seed=5), K)
+    rng = np.random.default_rng(3)
+    (W1, b1), (W2, b2), (W3, b3) = layers
+    W3 = 0.1 * np.abs(W3)
+    b3 = rng.uniform(0.5, 1.5, K) / K
+    mlp = np.concatenate([W1.ravel(), b1, W2.ravel(), b2, W3.ravel(), b3]).astype(np.float32)
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T, mlp=mlp, normalize_psf_sum=True, clamp01=True)
+    img = synth.image(H, W, C, seed=14)
+    out = torch.empty((1, C, H, W), device="cuda")
+    plan.simulate_frames(cuda(img), 0, SEED, 1, 1, out)
+    torch.cuda.synchronize()
+    ref = pipeline.simulate(img[None], True, SEED, 1, 1, sq, L, basis, synth.unpack_mlp(mlp, K),
+                            optics.geometry()[1], normalize=True, clamp01=True)
+    for c in range(C):
+        assert rel_l2(out.cpu().numpy()[0, c], ref[0, c]) <= 2e-2, c
+
+
 def test_simulate_step5_vs_oracle():
     H, W, C, K, T = 64, 96, 2, 16, 17
     plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T, noise_sigma=0.05, clamp01=True)
