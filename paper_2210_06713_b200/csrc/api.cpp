@@ -757,7 +757,7 @@ extern "C" p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t 
 // each sub-batch's device->host copy runs under the next sub-batch's compute (constraint:
 // compute(next) >= copy(previous)), the last copy is the exposed tail.  Minimum over
 // non-increasing size sequences by dynamic programming over (remaining, previous size).
-static std::vector<int> host_schedule(const p2s_plan_s* p, int F) {
+static std::vector<int> host_schedule_uncached(const p2s_plan_s* p, int F) {
   const char* fix = getenv("P2S_HOST_SUB");
   if (fix) {
     const int s = std::max(1, atoi(fix));
@@ -773,7 +773,9 @@ static std::vector<int> host_schedule(const p2s_plan_s* p, int F) {
   const double r4_ms = r512 ? 0.09 * ((double)p->P * p->Q / 262144.0) * (p->npairs / 18.0) : 0.0;
   const double lin_ms = 0.04 * px;  // columns + MLP per frame (512^2: ~2.6 ms / 64)
   const double c_ms = (double)p->C * p->H * p->W * 4.0 / 50e9 * 1e3;
-  auto comp = [&](int s) { return blur_waves(p, s) * wave_ms + ((s + 3) / 4) * r4_ms + s * lin_ms + 0.03; };
+  std::vector<double> compv(F + 1, 0.0);
+  for (int s = 1; s <= F; ++s) compv[s] = blur_waves(p, s) * wave_ms + ((s + 3) / 4) * r4_ms + s * lin_ms + 0.03;
+  auto comp = [&](int s) { return compv[s]; };
   // best[r][q]: minimal time of r remaining frames after a sub-batch of q frames (q = 0: none)
   const size_t W1 = (size_t)F + 1;
   std::vector<double> best(W1 * W1, -1.0);
@@ -810,6 +812,12 @@ static std::vector<int> host_schedule(const p2s_plan_s* p, int F) {
   return out;
 }
 
+static const std::vector<int>& host_schedule(p2s_plan_s* p, int F) {
+  auto it = p->host_sched.find(F);
+  if (it == p->host_sched.end()) it = p->host_sched.emplace(F, host_schedule_uncached(p, F)).first;
+  return it->second;
+}
+
 extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host, int64_t img_frame_stride,
                                                uint64_t seed, int64_t frame0, int nframes, float* out_host,
                                                void* stream) {
@@ -831,7 +839,7 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
   bool pending = false;
   for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
     const int F = std::min(p->max_batch, nframes - i0);
-    const std::vector<int> subs = host_schedule(p, F);
+    const std::vector<int>& subs = host_schedule(p, F);
     if (pending) P2S_CUDA(cudaStreamWaitEvent(s, p->ev_copied, 0), "wait copies");  // d_out / d_img reuse
     if (img_frame_stride == 0) {
       P2S_CUDA(cudaMemcpyAsync(p->d_img, img_host, img_floats * 4, cudaMemcpyHostToDevice, s), "H2D img");

@@ -3,6 +3,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -141,6 +142,7 @@ struct p2s_plan_s {
   uint16_t* d_w = nullptr;      // bf16 [mb][H][ntx][n3/8][128 px][8]: per 128-pixel row tile, 8-basis chunks
   int ntx = 0;                  // 128-pixel tiles per image row
   int nsm = 148;                // SMs of the plan's device (blur wave accounting)
+  std::map<int, std::vector<int>> host_sched;  // p2s_simulate_frames_host sub-batch plan per batch size
   CUtensorMap tmap_b;           // 2-D TMA view of bg.bimg2: rows of 256 B, box 2 K-steps of one half
   float* d_img = nullptr;       // staging for the host entry point [mb][C][H][W]
   float* d_out = nullptr;       // staging for the host entry point [mb][C][H][W]
