@@ -1,7 +1,7 @@
 """Validation-battery statistics -- TEST INFRASTRUCTURE ONLY.
 
-Only tests/, __graft_entry__.smoke(), bench.py's reference legs and tools/validate.py
-may use this module; the product path (libp2s) never does.
+Only tests/, __graft_entry__.smoke() and bench.py's reference legs may use this module;
+the product path (libp2s) never does.
 
 The paper builds the sampler so that the Zernike coefficient fields reproduce the spatial
 auto-correlation of the coefficients between pixels: homogeneous kernels A_jj(s)
