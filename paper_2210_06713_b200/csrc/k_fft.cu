@@ -304,7 +304,9 @@ __device__ __forceinline__ float2 spectrum(float2 s, float4 z) {
 // White-noise path: one CTA per Hermitian row pair {ky, P-ky}: each Philox draw serves the
 // bin and its mirror (the mirror's noise is the conjugate), the two rows are transformed
 // as two interleaved sequences, and the CTA loops over the frame batch.
-template <int NT>
+// ETA: caller-supplied noise (p2s_sample_zernike_from_noise) instead of the Philox draw; a
+// separate instantiation so the generated-noise kernel keeps its register budget.
+template <int NT, bool ETA = false>
 __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int Q = a.Q;
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
     for (int kx = threadIdx.x; kx < Q; kx += NT) {
       const int km = kx ? Q - kx : 0;
       float4 z, zm;
-      if (a.eta) {  // given eta (reading Q8 scaling): zeta = eta / sqrt(PQ/2), each bin read as stored
+      if (ETA) {  // given eta (reading Q8 scaling): zeta = eta / sqrt(PQ/2), each bin read as stored
         const float inv = rsqrtf(0.5f * (float)a.P * (float)Q);
         const size_t PQ = (size_t)a.P * Q;
         const float2* ea = a.eta + ((size_t)t * a.nslots + 2 * p) * PQ;
@@ -534,8 +536,8 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
     a.flow = 0;
     dim3 grid(pl->P / 2 + 1, pl->npairs);
     size_t sm = ((size_t)3 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
-    cudaFuncSetAttribute(k_rows_pair<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_rows_pair<256><<<grid, 256, sm, s>>>(a);
+    cudaFuncSetAttribute(k_rows_pair<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_rows_pair<256, true><<<grid, 256, sm, s>>>(a);
     return (int)cudaGetLastError();
   }
   if (ar) {
@@ -820,10 +822,27 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
     }
     return (int)cudaGetLastError();
   }
+  // Long columns (P > 1152: the 4K grid): 1024 threads and up to 8640 elements per CTA
+  // double the columns per CTA (TC = 4 at P = 2160; 5.53 -> 4.67 ms per 2 4K frames); at
+  // 1080p the 256-thread kernel with TC = 4 is as fast.
+  const int wide = pl->P * 4 > kColElems;
+  if (wide) {
+    tcl = 4;
+    while (tcl > 0 && pl->P * (1 << tcl) > 8640) --tcl;
+    a.tc_log2 = tcl;
+  }
   const int TC = 1 << tcl;
   dim3 grid((pl->W + TC - 1) / TC, pl->npairs, F);
   size_t sm = ((size_t)pl->P + 2 * padded_len((size_t)pl->P * TC)) * sizeof(float2);
-  if (mode == 0) {
+  if (wide) {
+    if (mode == 0) {
+      cudaFuncSetAttribute(k_cols<0, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_cols<0, 1024><<<grid, 1024, sm, s>>>(a);
+    } else {
+      cudaFuncSetAttribute(k_cols<1, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_cols<1, 1024><<<grid, 1024, sm, s>>>(a);
+    }
+  } else if (mode == 0) {
     cudaFuncSetAttribute(k_cols<0, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_cols<0, 256><<<grid, 256, sm, s>>>(a);
   } else {
