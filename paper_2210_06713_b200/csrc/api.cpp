@@ -369,6 +369,7 @@ static void free_plan(p2s_plan_s* p) {
     cudaStreamDestroy(p->copy_stream);
     cudaEventDestroy(p->ev_sub);
     cudaEventDestroy(p->ev_copied);
+    cudaEventDestroy(p->ev_img);
   }
   cudaFree(p->d_ztab);
   cudaFree(p->bg.koff);
@@ -716,19 +717,16 @@ extern "C" p2s_status p2s_blur_weights(p2s_plan p, const float* warped, const fl
   return P2S_OK;
 }
 
-extern "C" p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t img_frame_stride, uint64_t seed,
-                                          int64_t frame0, int nframes, float* out, void* stream) {
-  CHECK_PLAN();
-  if (nframes == 0) return P2S_OK;
-  if (!img || !out) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
-  if (img_frame_stride < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "img_frame_stride < 0");
-  DeviceGuard guard(p->device);
-  cudaStream_t s = (cudaStream_t)stream;
+// Steps 1-5; img_ready (nullable): an event the image upload records -- step 1's row pass
+// does not read the image, so the upload overlaps it and only the column/warp stage waits.
+static p2s_status simulate_impl(p2s_plan_s* p, const float* img, int64_t img_frame_stride, uint64_t seed,
+                                int64_t frame0, int nframes, float* out, cudaStream_t s, cudaEvent_t img_ready) {
   const size_t HW = (size_t)p->H * p->W;
   for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
     const int F = std::min(p->max_batch, nframes - i0);
     p2s_status st = run_step1(p, seed, frame0 + i0, F, s);
     if (st != P2S_OK) return st;
+    if (img_ready) P2S_CUDA(cudaStreamWaitEvent(s, img_ready, 0), "wait image upload");
     bool warp_fused = false;  // 512-point columns: step 2 runs inside the column kernel
     {
       StageScope sc(p, 1, s);
@@ -749,6 +747,16 @@ extern "C" p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t 
     }
   }
   return P2S_OK;
+}
+
+extern "C" p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t img_frame_stride, uint64_t seed,
+                                          int64_t frame0, int nframes, float* out, void* stream) {
+  CHECK_PLAN();
+  if (nframes == 0) return P2S_OK;
+  if (!img || !out) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (img_frame_stride < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "img_frame_stride < 0");
+  DeviceGuard guard(p->device);
+  return simulate_impl(p, img, img_frame_stride, seed, frame0, nframes, out, (cudaStream_t)stream, nullptr);
 }
 
 // Sub-batch sizes for the host entry point.  Modelled compute time of a sub-batch of s frames:
@@ -832,6 +840,7 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
     P2S_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     P2S_CUDA(cudaEventCreateWithFlags(&p->ev_sub, cudaEventDisableTiming), "cudaEventCreate");
     P2S_CUDA(cudaEventCreateWithFlags(&p->ev_copied, cudaEventDisableTiming), "cudaEventCreate");
+    P2S_CUDA(cudaEventCreateWithFlags(&p->ev_img, cudaEventDisableTiming), "cudaEventCreate");
   }
   // The device->host copy of each sub-batch runs on a second stream while the next
   // sub-batch computes, so the PCIe transfer of the outputs hides behind the kernels; the
@@ -840,20 +849,25 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
   for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
     const int F = std::min(p->max_batch, nframes - i0);
     const std::vector<int>& subs = host_schedule(p, F);
-    if (pending) P2S_CUDA(cudaStreamWaitEvent(s, p->ev_copied, 0), "wait copies");  // d_out / d_img reuse
+    if (pending) P2S_CUDA(cudaStreamWaitEvent(s, p->ev_copied, 0), "wait copies");  // d_out reuse
+    // image upload on the copy stream (after the previous chunk's compute has read d_img);
+    // the compute stream waits for it only before the column/warp stage
+    if (pending) P2S_CUDA(cudaStreamWaitEvent(p->copy_stream, p->ev_sub, 0), "wait compute");
     if (img_frame_stride == 0) {
-      P2S_CUDA(cudaMemcpyAsync(p->d_img, img_host, img_floats * 4, cudaMemcpyHostToDevice, s), "H2D img");
+      P2S_CUDA(cudaMemcpyAsync(p->d_img, img_host, img_floats * 4, cudaMemcpyHostToDevice, p->copy_stream),
+               "H2D img");
     } else {
       for (int i = 0; i < F; ++i)
         P2S_CUDA(cudaMemcpyAsync(p->d_img + i * img_floats, img_host + (size_t)(i0 + i) * img_frame_stride,
-                                 img_floats * 4, cudaMemcpyHostToDevice, s),
+                                 img_floats * 4, cudaMemcpyHostToDevice, p->copy_stream),
                  "H2D img");
     }
+    P2S_CUDA(cudaEventRecord(p->ev_img, p->copy_stream), "event record");
     int j0 = 0;
     for (const int Fs : subs) {
-      p2s_status st = p2s_simulate_frames(p, p->d_img + (img_frame_stride ? (size_t)j0 * img_floats : 0),
-                                          img_frame_stride ? (int64_t)img_floats : 0, seed, frame0 + i0 + j0, Fs,
-                                          p->d_out + (size_t)j0 * img_floats, stream);
+      p2s_status st = simulate_impl(p, p->d_img + (img_frame_stride ? (size_t)j0 * img_floats : 0),
+                                    img_frame_stride ? (int64_t)img_floats : 0, seed, frame0 + i0 + j0, Fs,
+                                    p->d_out + (size_t)j0 * img_floats, s, p->ev_img);
       if (st != P2S_OK) return st;
       P2S_CUDA(cudaEventRecord(p->ev_sub, s), "event record");
       P2S_CUDA(cudaStreamWaitEvent(p->copy_stream, p->ev_sub, 0), "wait sub-batch");

@@ -151,7 +151,7 @@ struct p2s_plan_s {
   std::vector<int> t_stage;
   std::vector<cudaEvent_t> t_ev;  // pairs
   cudaStream_t copy_stream = nullptr;  // host entry: device->host copies overlapped with compute
-  cudaEvent_t ev_sub = nullptr, ev_copied = nullptr;
+  cudaEvent_t ev_sub = nullptr, ev_copied = nullptr, ev_img = nullptr;
   // AR bookkeeping
   bool ar_valid = false;
   uint64_t ar_seed = 0;
