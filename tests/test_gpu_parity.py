@@ -404,13 +404,13 @@ def test_simulate_host_entry_matches_device_entry():
     assert np.array_equal(dev.cpu().numpy(), host)
 
 
-@pytest.mark.parametrize("F,per_frame_img", [(29, False), (11, True)])
-def test_simulate_host_entry_tapered_sub_batches(F, per_frame_img):
+@pytest.mark.parametrize("F,per_frame_img,max_batch", [(29, False, 0), (11, True, 0), (11, True, 4)])
+def test_simulate_host_entry_tapered_sub_batches(F, per_frame_img, max_batch):
     """The host entry point splits a batch into tapered sub-batches (wave-aligned blur
     launches, copies overlapped): results are bit-identical to one device launch, with a
     broadcast image and with one image per frame."""
     H, W, C, K, T = 128, 256, 3, 16, 17
-    plan, *_ = make_plan(H, W, C, 2.0, K, T)
+    plan, *_ = make_plan(H, W, C, 2.0, K, T, max_batch=max_batch)  # max_batch 4: chunked uploads
     nimg = F if per_frame_img else 1
     img = np.stack([synth.image(H, W, C, seed=20 + i) for i in range(nimg)])
     stride = C * H * W if per_frame_img else 0
