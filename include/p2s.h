@@ -156,7 +156,10 @@ p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t img_frame_s
                                int64_t frame0, int nframes, float* out, void* stream);
 
 /* Same as p2s_simulate_frames with HOST buffers: img_host [..][C][H][W] (stride as above),
- * out_host [nframes][C][H][W].  Copies in, runs, copies out, synchronises. */
+ * out_host [nframes][C][H][W].  Copies in, runs, copies out, synchronises.  Internally the
+ * frames run as tapered sub-batches on `stream` while a second (plan-owned) stream uploads
+ * the images and downloads each finished sub-batch; pinned host memory gives full PCIe
+ * overlap.  Results are bit-identical to p2s_simulate_frames. */
 p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host, int64_t img_frame_stride,
                                     uint64_t seed, int64_t frame0, int nframes, float* out_host,
                                     void* stream);
@@ -222,7 +225,7 @@ p2s_status p2s_field_autocorr(p2s_plan p, const float* zern, int nframes, int ma
 p2s_status p2s_aperture_stats(p2s_plan p, const float* zern, int nframes, const int32_t* pixels, int npix,
                               double* out, void* stream);
 
-/* Exact-PSF path (partial): the slow per-pixel reference that P2S
+/* Exact-PSF path: the slow per-pixel reference that P2S
  * replaces.  Eq.2: h_x(u) = |F{P e^{-j phi_x}}|^2 with phi_x = sum_j a_j(x) Z_j on
  * a 32-sample pupil zero-padded to a 64-point FFT (PSF pixel = lambda/(2D): a pure tilt moves
  * the PSF by 4 a_2/pi px, reading Q24), T x T window (the plan's taps), unit sum.
