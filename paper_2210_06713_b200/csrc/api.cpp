@@ -52,6 +52,22 @@ static void radix_plan(int N, AxisFFT& a) {
   a.N = N;
   a.nrad = 0;
   int m = N;
+  // sizes with factors 3 or 5 (1080, 1920, 2160, 3840, ...): composite radices up to 16 done
+  // in registers, three shared-memory passes instead of five or six; powers of two keep the
+  // radix-8 plan (the 512-point register kernels match on it)
+  const char* small = getenv("P2S_FFT_SMALL_RADIX");
+  if ((N % 3 == 0 || N % 5 == 0) && !(small && atoi(small))) {
+    static const int big[] = {16, 15, 12, 10, 9, 8, 6, 5, 4, 3, 2};
+    while (m > 1) {
+      for (int r : big)
+        if (m % r == 0) {
+          a.rad[a.nrad++] = r;
+          m /= r;
+          break;
+        }
+    }
+    return;
+  }
   while (m % 8 == 0) { a.rad[a.nrad++] = 8; m /= 8; }
   while (m % 4 == 0) { a.rad[a.nrad++] = 4; m /= 4; }
   while (m % 2 == 0) { a.rad[a.nrad++] = 2; m /= 2; }

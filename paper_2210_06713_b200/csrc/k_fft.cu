@@ -91,6 +91,81 @@ __device__ __forceinline__ void dft_inv<5>(float2* v) {
   v[3] = make_float2(a2.x + b2.y, a2.y - b2.x);
 }
 
+// Twiddles e^{+2 pi i j / R} of the composite radices: local constant tables, indexed
+// with compile-time j after unrolling (folded into immediates).
+template <int R>
+__device__ __forceinline__ float2 twr(int j);
+template <>
+__device__ __forceinline__ float2 twr<6>(int j) {
+  const float2 t[6] = {{1.0f, 0.0f}, {0.50000000000000011f, 0.8660254037844386f}, {-0.49999999999999978f, 0.86602540378443871f}, {-1.0f, 1.2246467991473532e-16f}, {-0.50000000000000044f, -0.86602540378443837f}, {0.50000000000000011f, -0.8660254037844386f}};
+  return t[j];
+}
+template <>
+__device__ __forceinline__ float2 twr<9>(int j) {
+  const float2 t[9] = {{1.0f, 0.0f}, {0.76604444311897801f, 0.64278760968653925f}, {0.17364817766693041f, 0.98480775301220802f}, {-0.49999999999999978f, 0.86602540378443871f}, {-0.93969262078590832f, 0.34202014332566888f}, {-0.93969262078590843f, -0.34202014332566866f}, {-0.50000000000000044f, -0.86602540378443837f}, {0.17364817766692997f, -0.98480775301220813f}, {0.76604444311897779f, -0.64278760968653958f}};
+  return t[j];
+}
+template <>
+__device__ __forceinline__ float2 twr<10>(int j) {
+  const float2 t[10] = {{1.0f, 0.0f}, {0.80901699437494745f, 0.58778525229247314f}, {0.30901699437494745f, 0.95105651629515353f}, {-0.30901699437494734f, 0.95105651629515364f}, {-0.80901699437494734f, 0.58778525229247325f}, {-1.0f, 1.2246467991473532e-16f}, {-0.80901699437494756f, -0.58778525229247303f}, {-0.30901699437494756f, -0.95105651629515353f}, {0.30901699437494723f, -0.95105651629515364f}, {0.80901699437494734f, -0.58778525229247336f}};
+  return t[j];
+}
+template <>
+__device__ __forceinline__ float2 twr<12>(int j) {
+  const float2 t[12] = {{1.0f, 0.0f}, {0.86602540378443871f, 0.49999999999999994f}, {0.50000000000000011f, 0.8660254037844386f}, {6.123233995736766e-17f, 1.0f}, {-0.49999999999999978f, 0.86602540378443871f}, {-0.86602540378443871f, 0.49999999999999994f}, {-1.0f, 1.2246467991473532e-16f}, {-0.86602540378443882f, -0.49999999999999972f}, {-0.50000000000000044f, -0.86602540378443837f}, {-1.8369701987210297e-16f, -1.0f}, {0.50000000000000011f, -0.8660254037844386f}, {0.86602540378443837f, -0.50000000000000044f}};
+  return t[j];
+}
+template <>
+__device__ __forceinline__ float2 twr<15>(int j) {
+  const float2 t[15] = {{1.0f, 0.0f}, {0.91354545764260087f, 0.40673664307580015f}, {0.66913060635885824f, 0.74314482547739413f}, {0.30901699437494745f, 0.95105651629515353f}, {-0.10452846326765333f, 0.9945218953682734f}, {-0.49999999999999978f, 0.86602540378443871f}, {-0.80901699437494734f, 0.58778525229247325f}, {-0.97814760073380569f, 0.20791169081775931f}, {-0.97814760073380569f, -0.20791169081775907f}, {-0.80901699437494756f, -0.58778525229247303f}, {-0.50000000000000044f, -0.86602540378443837f}, {-0.10452846326765423f, -0.99452189536827329f}, {0.30901699437494723f, -0.95105651629515364f}, {0.66913060635885846f, -0.74314482547739402f}, {0.91354545764260098f, -0.40673664307580015f}};
+  return t[j];
+}
+template <>
+__device__ __forceinline__ float2 twr<16>(int j) {
+  const float2 t[16] = {{1.0f, 0.0f}, {0.92387953251128674f, 0.38268343236508978f}, {0.70710678118654757f, 0.70710678118654746f}, {0.38268343236508984f, 0.92387953251128674f}, {6.123233995736766e-17f, 1.0f}, {-0.38268343236508973f, 0.92387953251128674f}, {-0.70710678118654746f, 0.70710678118654757f}, {-0.92387953251128674f, 0.38268343236508989f}, {-1.0f, 1.2246467991473532e-16f}, {-0.92387953251128685f, -0.38268343236508967f}, {-0.70710678118654768f, -0.70710678118654746f}, {-0.38268343236509034f, -0.92387953251128652f}, {-1.8369701987210297e-16f, -1.0f}, {0.38268343236509f, -0.92387953251128663f}, {0.70710678118654735f, -0.70710678118654768f}, {0.92387953251128652f, -0.38268343236509039f}};
+  return t[j];
+}
+// Composite radix R = A * B in registers (Cooley-Tukey): n = a + A b, k = kb + B ka;
+// DFT_B over b for each a, twiddle e^{+2 pi i a kb / R}, DFT_A over a for each kb.
+template <int A, int B>
+__device__ __forceinline__ void dft_inv_ct(float2* v) {
+  constexpr int R = A * B;
+  float2 y[A][B];
+#pragma unroll
+  for (int a = 0; a < A; ++a) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) y[a][b] = v[a + A * b];
+    dft_inv<B>(y[a]);
+#pragma unroll
+    for (int kb = 1; kb < B; ++kb) {
+      const int j = (a * kb) % R;
+      if (j) y[a][kb] = cmul(y[a][kb], twr<R>(j));
+    }
+  }
+#pragma unroll
+  for (int kb = 0; kb < B; ++kb) {
+    float2 t[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) t[a] = y[a][kb];
+    dft_inv<A>(t);
+#pragma unroll
+    for (int ka = 0; ka < A; ++ka) v[kb + B * ka] = t[ka];
+  }
+}
+template <>
+__device__ __forceinline__ void dft_inv<6>(float2* v) { dft_inv_ct<2, 3>(v); }
+template <>
+__device__ __forceinline__ void dft_inv<9>(float2* v) { dft_inv_ct<3, 3>(v); }
+template <>
+__device__ __forceinline__ void dft_inv<10>(float2* v) { dft_inv_ct<2, 5>(v); }
+template <>
+__device__ __forceinline__ void dft_inv<12>(float2* v) { dft_inv_ct<4, 3>(v); }
+template <>
+__device__ __forceinline__ void dft_inv<15>(float2* v) { dft_inv_ct<3, 5>(v); }
+template <>
+__device__ __forceinline__ void dft_inv<16>(float2* v) { dft_inv_ct<4, 4>(v); }
+
+
 // ------------------------------------------------------------------ shared-memory Stockham IDFT
 // TC interleaved sequences of length N live in shared memory, element i of sequence c at
 // x[i*TC + c] (TC = 2^tc_log2).  Out-of-place (ping-pong) passes of radix 8/4/2/3/5; the
@@ -168,6 +243,12 @@ __device__ __forceinline__ float2* smem_ifft(float2* a, float2* b, const FFTPlan
     const int R = f->rad[ip];
     const uint32_t mg = f->magic[ip];
     switch (R) {
+      case 16: ifft_pass<16, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 15: ifft_pass<15, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 12: ifft_pass<12, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 10: ifft_pass<10, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 9: ifft_pass<9, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 6: ifft_pass<6, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
       case 8: ifft_pass<8, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
       case 4: ifft_pass<4, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
       case 2: ifft_pass<2, NT>(a, b, f->N, Ns, mg, tc_log2, f->tw); break;
