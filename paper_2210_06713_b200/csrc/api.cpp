@@ -48,15 +48,18 @@ static uint16_t host_bf16(float f) {
   return u;
 }
 
-static void radix_plan(int N, AxisFFT& a) {
+static void radix_plan(int N, AxisFFT& a, bool columns) {
   a.N = N;
   a.nrad = 0;
   int m = N;
-  // sizes with factors 3 or 5 (1080, 1920, 2160, 3840, ...): composite radices up to 16 done
-  // in registers, three shared-memory passes instead of five or six; powers of two keep the
-  // radix-8 plan (the 512-point register kernels match on it)
+  // composite radices up to 16 done in registers: 1080, 1920, 2160, 3840 take three
+  // shared-memory passes instead of five or six, 256 two instead of three; 512 keeps the
+  // radix-8 plan the 512-point register kernels match on
   const char* small = getenv("P2S_FFT_SMALL_RADIX");
-  if ((N % 3 == 0 || N % 5 == 0) && !(small && atoi(small))) {
+  // (powers of two: columns only -- the row kernels run one or two sequences per CTA and
+  // a radix-16 pass of a 256-point row leaves most of their threads idle)
+  const bool pow2 = (N & (N - 1)) == 0;
+  if (N != 512 && (!pow2 || columns) && !(small && atoi(small))) {
     static const int big[] = {16, 15, 12, 10, 9, 8, 6, 5, 4, 3, 2};
     while (m > 1) {
       for (int r : big)
@@ -556,8 +559,8 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
     p->clamped_max = *std::max_element(cl.begin(), cl.end());
   }
   P2S_TRY(upload_sqrtS(p));
-  radix_plan(p->Q, p->fq);
-  radix_plan(p->P, p->fp);
+  radix_plan(p->Q, p->fq, false);
+  radix_plan(p->P, p->fp, true);
   P2S_TRY(upload_twiddles(p->fq));
   P2S_TRY(upload_twiddles(p->fp));
   {
