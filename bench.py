@@ -126,6 +126,11 @@ WORKLOADS = {
                     desc="3840x2160 RGB, 2 frames/GPU per step, D/r0=5, Z=36, K=100 bases 33x33"),
     "cfg2_256": dict(H=256, W=256, C=1, F=100, d_over_r0=3.0, K=100, T=33, ar_alpha=0.95,
                      desc="256x256 gray, 100-frame AR(0.95) sequence, D/r0=3, K=100 bases 33x33"),
+    # configs 4 and 5 as AR(1) sequences (the BASELINE descriptions' "100-frame sequences")
+    "cfg4_1080p_ar": dict(H=1080, W=1920, C=3, F=8, d_over_r0=4.0, K=100, T=33, ar_alpha=0.95,
+                          desc="1920x1080 RGB, AR(0.95) sequence, 8 frames/GPU per step, D/r0=4, K=100 bases 33x33"),
+    "cfg5_4k_ar": dict(H=2160, W=3840, C=3, F=2, d_over_r0=5.0, K=100, T=33, ar_alpha=0.95,
+                       desc="3840x2160 RGB, AR(0.95) sequence, 2 frames/GPU per step, D/r0=5, K=100 bases 33x33"),
     # NEXT-3: the frozen-flow temporal model on the headline geometry
     "cfg3_512_flow": dict(H=512, W=512, C=3, F=64, d_over_r0=3.0, K=100, T=33, ar_alpha=0.0, flow=(0.5, 0.25),
                           desc="512x512 RGB, 64-frame frozen-flow sequence (0.5, 0.25) px/frame, D/r0=3, K=100"),
