@@ -903,13 +903,14 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
     }
     return (int)cudaGetLastError();
   }
-  // Long columns (P > 1152: the 4K grid): 1024 threads and up to 8640 elements per CTA
-  // double the columns per CTA (TC = 4 at P = 2160; 5.53 -> 4.67 ms per 2 4K frames); at
-  // 1080p the 256-thread kernel with TC = 4 is as fast.
-  const int wide = pl->P * 4 > kColElems;
+  // Long columns: 1024 threads and up to 8640 elements per CTA double the columns per CTA
+  // where that is still below 16 (1080 points: 8 columns, 64-byte row segments, 3.26 ->
+  // 3.10 ms per 8 frames; 2160: 4 columns, 5.53 -> 4.67 ms per 2 frames).
+  int tw = 4;
+  while (tw > 0 && pl->P * (1 << tw) > 8640) --tw;
+  const int wide = tw > tcl;
   if (wide) {
-    tcl = 4;
-    while (tcl > 0 && pl->P * (1 << tcl) > 8640) --tcl;
+    tcl = tw;
     a.tc_log2 = tcl;
   }
   const int TC = 1 << tcl;
