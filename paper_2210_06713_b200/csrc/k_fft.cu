@@ -581,6 +581,92 @@ __global__ void __launch_bounds__(NT) k_rows_ar(RowArgs a) {
   for (int kx = threadIdx.x; kx < Q; kx += NT) a.ar[row + kx] = st[kx];
 }
 
+// AR(1) path, Hermitian row pairs: one CTA per row pair {ky, P-ky} as in k_rows_pair.  The
+// state of a mirror bin is the conjugate of its canonical bin's (the draws are conjugate and
+// the recursion has real coefficients, so this holds exactly, negation being exact), so the
+// CTA keeps only row ky's state, in registers (bins kx = tid + NT i, MB per thread), draws
+// Philox once per bin pair and feeds the mirror row with the conjugate.  Half the draws and
+// half the state traffic of k_rows_ar; the same values up to the FFT's rounding order.
+// It pays where the rows are long (Q > 1024: 4K AR rows 5.48 -> 3.84 ms, 1080p 3.89 -> 3.56
+// per launch); at Q = 256 (cfg2) the one-CTA-per-row kernel's twice-as-large grid wins
+// (1.57 vs 1.83 ms: 100 sequential frames per CTA), so short rows keep k_rows_ar.
+// 128 registers, no spills (an 80-register cap spills and is slower at 1080p).
+template <int NT, int MB>
+__global__ void __launch_bounds__(NT) k_rows_ar_pair(RowArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int Q = a.Q;
+  float2* twq = reinterpret_cast<float2*>(smem);  // [Q] twiddles
+  float2* sS = twq + Q;                            // [2][Q]
+  float2* X = sS + 2 * Q;                          // [Q][2] interleaved rows (padded)
+  float2* Xb = X + padded_len(2 * Q);
+  __shared__ FFTPlanSmem fpl;
+  stage_fft_plan(&fpl, a.fq, twq);
+  const int ky = blockIdx.x, p = blockIdx.y;
+  const int k1 = ky ? a.P - ky : 0;
+  const size_t plane = (size_t)p * a.P * Q;
+  const size_t row = plane + (size_t)ky * Q, rowm = plane + (size_t)k1 * Q;
+  for (int kx = threadIdx.x; kx < Q; kx += NT) {
+    sS[kx] = a.sqrtS[row + kx];
+    sS[Q + kx] = a.sqrtS[rowm + kx];
+  }
+  float4 st[MB];
+#pragma unroll
+  for (int i = 0; i < MB; ++i) {
+    const int kx = threadIdx.x + NT * i;
+    st[i] = (a.load_state && kx < Q) ? a.ar[row + kx] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  const int64_t t_end = a.frame0 + a.F;
+  for (int64_t t = a.t_start; t < t_end; ++t) {
+    const bool out = t >= a.frame0;
+#pragma unroll
+    for (int i = 0; i < MB; ++i) {
+      const int kx = threadIdx.x + NT * i;
+      if (kx < Q) {
+        float4 z = spectral_noise(ky, kx, a.P, Q, p, t, a.k0, a.k1);
+        if (t > 0) {
+          const float4 o = st[i];
+          z = make_float4(a.alpha * o.x + a.calpha * z.x, a.alpha * o.y + a.calpha * z.y,
+                          a.alpha * o.z + a.calpha * z.z, a.alpha * o.w + a.calpha * z.w);
+        }
+        st[i] = z;
+        if (out) {
+          const int km = kx ? Q - kx : 0;
+          X[pidx(2 * kx)] = spectrum(sS[kx], z);
+          X[pidx(2 * km + 1)] = spectrum(sS[Q + km], make_float4(z.x, -z.y, z.z, -z.w));
+        }
+      }
+    }
+    if (!out) continue;  // replay: state only
+    __syncthreads();
+    const float2* R = smem_ifft<NT>(X, Xb, &fpl, 1);
+    float2* dst = a.Zout + (size_t)(t - a.frame0) * a.npairs * a.P * Q + plane;
+    for (int x = threadIdx.x; x < Q; x += NT) {
+      dst[(size_t)ky * Q + x] = R[pidx(2 * x)];
+      if (k1 != ky) dst[(size_t)k1 * Q + x] = R[pidx(2 * x + 1)];
+    }
+    __syncthreads();
+  }
+  // Write back both rows (the mirror row as the conjugate) so the stored state is complete.
+#pragma unroll
+  for (int i = 0; i < MB; ++i) {
+    const int kx = threadIdx.x + NT * i;
+    if (kx < Q) {
+      const float4 z = st[i];
+      a.ar[row + kx] = z;
+      a.ar[rowm + (kx ? Q - kx : 0)] = make_float4(z.x, -z.y, z.z, -z.w);
+    }
+  }
+}
+
+template <int NT, int MB>
+static void launch_rows_ar_pair(const RowArgs& a, int P, int npairs, int Q, cudaStream_t s) {
+  dim3 grid(P / 2 + 1, npairs);
+  size_t sm = ((size_t)3 * Q + 2 * padded_len(2 * Q)) * sizeof(float2);
+  cudaFuncSetAttribute(k_rows_ar_pair<NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_rows_ar_pair<NT, MB><<<grid, NT, sm, s>>>(a);
+}
+
 // The register fast path needs a 512-point axis planned as radix 8 x 8 x 8.
 static bool reg512(const AxisFFT& ax) {
   return ax.N == kRegN && ax.nrad == 3 && ax.rad[0] == 8 && ax.rad[1] == 8 && ax.rad[2] == 8;
@@ -621,7 +707,18 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
     k_rows_pair<256, true><<<grid, 256, sm, s>>>(a);
     return (int)cudaGetLastError();
   }
-  if (ar) {
+  const int Q = pl->Q, NTp = Q > 1024 ? 512 : 256, mb = (Q + NTp - 1) / NTp;
+  const int ar_rows = getenv_flag("P2S_AR_ROWS");  // 1: always k_rows_ar, 2: always the pair kernel
+  if (ar && mb <= 8 && ar_rows != 1 && (Q > 1024 || ar_rows == 2)) {
+    if (NTp == 512) {
+      if (mb <= 4) launch_rows_ar_pair<512, 4>(a, pl->P, pl->npairs, Q, s);
+      else launch_rows_ar_pair<512, 8>(a, pl->P, pl->npairs, Q, s);
+    } else {
+      if (mb <= 1) launch_rows_ar_pair<256, 1>(a, pl->P, pl->npairs, Q, s);
+      else if (mb <= 2) launch_rows_ar_pair<256, 2>(a, pl->P, pl->npairs, Q, s);
+      else launch_rows_ar_pair<256, 4>(a, pl->P, pl->npairs, Q, s);
+    }
+  } else if (ar) {
     dim3 grid(pl->P, pl->npairs);
     size_t sm = ((size_t)2 * pl->Q + 2 * padded_len(pl->Q)) * sizeof(float2) + (size_t)pl->Q * sizeof(float4) + 16;
     if (pl->Q > 1024) {

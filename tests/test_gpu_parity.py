@@ -146,7 +146,9 @@ def test_sample_zernike_own_tables_vs_oracle():
     assert worst <= 1e-3, worst
 
 
-def test_sample_zernike_ar_sequence_and_replay():
+@pytest.mark.parametrize("ar_rows", ["0", "2"])  # 2: force the row-pair kernel (k_rows_ar_pair)
+def test_sample_zernike_ar_sequence_and_replay(ar_rows, monkeypatch):
+    monkeypatch.setenv("P2S_AR_ROWS", ar_rows)
     H = W = 64
     alpha = 0.95
     plan, _, _, sq, L = make_plan(H, W, 1, 3.0, 16, 17, ar_alpha=alpha)
@@ -162,6 +164,30 @@ def test_sample_zernike_ar_sequence_and_replay():
     plan.sample_zernike(SEED, 2, 2, z2)         # replay frames 0..1 on the device
     torch.cuda.synchronize()
     assert torch.equal(z2, z[2:4])              # bit-identical to the sequential run
+
+
+@pytest.mark.parametrize("H,W", [(45, 75), (64, 96), (1080, 1920)])
+def test_ar_row_pair_kernel_matches_row_kernel(H, W, monkeypatch):
+    """The AR(1) row-pair kernel (k_rows_ar_pair: mirror state = conjugate, one draw per bin
+    pair, forced with P2S_AR_ROWS=2) against the one-CTA-per-row kernel (P2S_AR_ROWS=1): the
+    same draws and state, so the fields agree to the FFT's fp32 rounding, for a fresh start, a
+    stored-state continuation and a replayed start; odd P and Q included."""
+    from paper_2210_06713_b200 import Plan, PlanConfig
+    plan = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=3.0, Z=36, K=16, taps=17, ar_alpha=0.95),
+                synth.basis(16, 17, seed=1), synth.mlp_weights(16, n_in=33, seed=1))
+    F = 2 if H > 512 else 3
+    outs = []
+    for mode in ("2", "1"):
+        monkeypatch.setenv("P2S_AR_ROWS", mode)
+        z = torch.empty((2 * F + 1, 36, H, W), device="cuda")
+        plan.sample_zernike(SEED, 0, F, z[:F])
+        plan.sample_zernike(SEED, F, F, z[F:2 * F])
+        plan.sample_zernike(SEED, 2 * F + 2, 1, z[2 * F:])   # replays frames 0..2F+1
+        torch.cuda.synchronize()
+        outs.append(z.cpu().numpy())
+    a, b = outs
+    worst = max(rel_l2(a[f, j], b[f, j]) for f in range(2 * F + 1) for j in range(1, 36))
+    assert worst <= 1e-6, worst
 
 
 # ------------------------------------------------------------------ step 2
