@@ -264,6 +264,62 @@ __device__ __forceinline__ float2* smem_ifft(float2* a, float2* b, const FFTPlan
   return a;
 }
 
+// In-place variant for plans where every pass has at most one butterfly per thread
+// ((N / R) * TC <= NT): each thread loads its butterfly into registers, the CTA
+// synchronises, and the results overwrite the same buffer, so one buffer serves (the
+// persistent column kernel spends the second one on prefetching the next block).
+template <int R, int NT>
+__device__ __forceinline__ void ifft_pass_inplace(float2* __restrict__ x, int N, int Ns, uint32_t mag, int tc_log2,
+                                                  const float2* __restrict__ tw) {
+  const int NR = N / R;
+  const int total = NR << tc_log2;
+  const int ts = N / (Ns * R);
+  const int w = threadIdx.x;
+  const bool act = w < total;
+  const int c = w & ((1 << tc_log2) - 1), j = act ? w >> tc_log2 : 0;
+  float2 v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = x[pidx(((j + r * NR) << tc_log2) + c)];
+  __syncthreads();
+  const int q = Ns == 1 ? j : (int)__umulhi((uint32_t)j, mag);
+  const int k = j - q * Ns;
+  if (Ns > 1) {
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[r * k * ts]);
+  }
+  dft_inv<R>(v);
+  const int base = q * Ns * R + k;
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[pidx(((base + r * Ns) << tc_log2) + c)] = v[r];
+  }
+  __syncthreads();
+}
+
+template <int NT>
+__device__ __forceinline__ void smem_ifft_inplace(float2* x, const FFTPlanSmem* f, int tc_log2) {
+  int Ns = 1;
+  const int nrad = f->nrad;
+  for (int ip = 0; ip < nrad; ++ip) {
+    const int R = f->rad[ip];
+    const uint32_t mg = f->magic[ip];
+    switch (R) {
+      case 16: ifft_pass_inplace<16, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 15: ifft_pass_inplace<15, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 12: ifft_pass_inplace<12, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 10: ifft_pass_inplace<10, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 9: ifft_pass_inplace<9, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 6: ifft_pass_inplace<6, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 8: ifft_pass_inplace<8, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 4: ifft_pass_inplace<4, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 2: ifft_pass_inplace<2, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+      case 3: ifft_pass_inplace<3, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+      default: ifft_pass_inplace<5, NT>(x, f->N, Ns, mg, tc_log2, f->tw); break;
+    }
+    Ns *= R;
+  }
+}
+
 static void fill_fft_args(FFTArgs& a, const AxisFFT& ax) {
   a.N = ax.N;
   a.nrad = ax.nrad;
@@ -753,6 +809,7 @@ struct ColArgs {
   FFTArgs fp;
   const float2* Zin;  // [F][npairs][P][Q]
   int P, Q, H, W, npairs, nslots, Z;
+  int F;  // frames (the persistent column kernel's tile count)
   int tc_log2;
   float* zern;        // mode 0: [F][Z][H][W]
   uint16_t* X;        // mode 1: bf16 [F][nslots][H*W]
@@ -844,6 +901,80 @@ __global__ void __launch_bounds__(NT) k_cols(ColArgs a) {
         t[HW + pix] = v.y;
       }
     }
+  }
+}
+
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Long columns (1080p / 4K), persistent: one CTA per SM walks the column blocks; the next
+// block's loads (cp.async, zero-filled past Q) land in the second buffer while the current
+// block is transformed in place (smem_ifft_inplace) and written out.  k_cols runs one
+// 164 KB CTA per SM whose load, transform and store phases serialise (ncu at 4K: DRAM 11%
+// of peak, stalls on the load scoreboard and on barriers).
+template <int MODE, int NT>
+__global__ void __launch_bounds__(NT) k_cols_p(ColArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int TC = 1 << a.tc_log2;
+  float2* twp = reinterpret_cast<float2*>(smem);
+  float2* Xw = twp + a.P;
+  float2* Xn = Xw + padded_len((size_t)a.P << a.tc_log2);
+  __shared__ FFTPlanSmem fpl;
+  stage_fft_plan(&fpl, a.fp, twp);
+  const int nxb = (a.W + TC - 1) / TC;
+  const int ntiles = nxb * a.npairs * a.F;
+  const int n = a.P << a.tc_log2;
+  auto prefetch = [&](int tile, float2* dst) {
+    const int xk = tile % nxb, r = tile / nxb;
+    const int p = r % a.npairs, f = r / a.npairs;
+    const float2* src = a.Zin + ((size_t)f * a.npairs + p) * a.P * a.Q;
+    for (int w = threadIdx.x; w < n; w += NT) {
+      const int c = w & (TC - 1), ky = w >> a.tc_log2;
+      const int x = xk * TC + c;
+      cp_async8(dst + pidx(w), x < a.Q ? &src[(size_t)ky * a.Q + x] : src, x < a.Q ? 8u : 0u);
+    }
+    cp_async_commit();
+  };
+  if ((int)blockIdx.x < ntiles) prefetch(blockIdx.x, Xw);
+  const size_t HW = (size_t)a.H * a.W;
+  const int m = a.H << a.tc_log2;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    cp_async_wait<0>();
+    __syncthreads();  // this block landed; every thread is done with the previous one (Xn)
+    if (tile + (int)gridDim.x < ntiles) prefetch(tile + gridDim.x, Xn);
+    smem_ifft_inplace<NT>(Xw, &fpl, a.tc_log2);
+    const int xk = tile % nxb, r = tile / nxb;
+    const int p = r % a.npairs, f = r / a.npairs;
+    const int x0 = xk * TC, sa = 2 * p, sb = 2 * p + 1;
+    for (int w = threadIdx.x; w < m; w += NT) {
+      const int c = w & (TC - 1), yy = w >> a.tc_log2;
+      const int x = x0 + c;
+      if (x >= a.W) continue;
+      const float2 v = Xw[pidx(w)];
+      const size_t pix = (size_t)yy * a.W + x;
+      if (MODE == 0) {
+        float* z = a.zern + (size_t)f * a.Z * HW;
+        z[(size_t)(sa + 1) * HW + pix] = v.x;
+        if (sb < a.nslots) z[(size_t)(sb + 1) * HW + pix] = v.y;
+      } else {
+        uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
+        Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
+        if (sb < a.nslots) Xo[(size_t)sb * HW + pix] = f_to_bf16(v.y);
+        if (p == 0) {
+          float* t = a.tilt + (size_t)f * 2 * HW;
+          t[pix] = v.x;
+          t[HW + pix] = v.y;
+        }
+      }
+    }
+    float2* t = Xw;
+    Xw = Xn;
+    Xn = t;
   }
 }
 
@@ -968,6 +1099,7 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   a.npairs = pl->npairs;
   a.nslots = pl->nslots;
   a.Z = pl->Z;
+  a.F = F;
   int tcl = 4;
   while (tcl > 0 && pl->P * (1 << tcl) > kColElems) --tcl;
   a.tc_log2 = tcl;
@@ -1011,6 +1143,23 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
     a.tc_log2 = tcl;
   }
   const int TC = 1 << tcl;
+  if (wide && getenv_flag("P2S_COLS_NP") == 0) {
+    bool one = true;  // every pass at most one butterfly per thread: in-place persistent kernel
+    for (int i = 0; i < pl->fp.nrad; ++i) one = one && (pl->P / pl->fp.rad[i]) * TC <= 1024;
+    if (one) {
+      const int ntiles = (pl->W + TC - 1) / TC * pl->npairs * F;
+      const int grid = std::min(ntiles, pl->num_sms);
+      size_t sm = ((size_t)pl->P + 2 * padded_len((size_t)pl->P * TC)) * sizeof(float2);
+      if (mode == 0) {
+        cudaFuncSetAttribute(k_cols_p<0, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_cols_p<0, 1024><<<grid, 1024, sm, s>>>(a);
+      } else {
+        cudaFuncSetAttribute(k_cols_p<1, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_cols_p<1, 1024><<<grid, 1024, sm, s>>>(a);
+      }
+      return (int)cudaGetLastError();
+    }
+  }
   dim3 grid((pl->W + TC - 1) / TC, pl->npairs, F);
   size_t sm = ((size_t)pl->P + 2 * padded_len((size_t)pl->P * TC)) * sizeof(float2);
   if (wide) {

@@ -166,6 +166,50 @@ def test_sample_zernike_ar_sequence_and_replay(ar_rows, monkeypatch):
     assert torch.equal(z2, z[2:4])              # bit-identical to the sequential run
 
 
+def test_persistent_column_kernel_vs_oracle():
+    """P = 1000 (radices 10 x 10 x 10, 8 columns per block) takes the persistent in-place
+    column kernel (k_cols_p); fields against the oracle."""
+    H, W, F = 1000, 40, 1
+    plan, _, _, sq, L = make_plan(H, W, 1, 3.0, 16, 17)
+    assert plan.P == 1000
+    z = torch.empty((F, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 2, F, z)
+    torch.cuda.synchronize()
+    got = z.cpu().numpy()
+    ref = pipeline.sample_zernike(SEED, 2, F, sq, L, H, W)
+    worst = max(rel_l2(got[f, j], ref[f, j]) for f in range(F) for j in range(1, 36))
+    assert worst <= 1e-4, worst
+
+
+@pytest.mark.parametrize("H,W,F", [(1080, 1920, 2), (2160, 3840, 1)])
+def test_persistent_column_kernel_matches_per_block_kernel(H, W, F, monkeypatch):
+    """k_cols_p (persistent, cp.async prefetch, in-place passes) against k_cols
+    (P2S_COLS_NP=1) at the cfg4/cfg5 geometries: the same butterflies, so the fields agree to
+    fp32 rounding; both the fp32 field output (sample_zernike) and the fused bf16 path."""
+    from paper_2210_06713_b200 import Plan, PlanConfig
+    plan = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=3.0, Z=36, K=16, taps=17),
+                synth.basis(16, 17, seed=1), synth.mlp_weights(16, n_in=33, seed=1))
+    outs = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("P2S_COLS_NP", mode)
+        z = torch.empty((F, 36, H, W), device="cuda")
+        plan.sample_zernike(SEED, 1, F, z)
+        torch.cuda.synchronize()
+        outs.append(z.cpu().numpy())
+    a, b = outs
+    worst = max(rel_l2(a[f, j], b[f, j]) for f in range(F) for j in range(1, 36))
+    assert worst <= 1e-6, worst
+    img = torch.from_numpy(synth.image(H, W, 1, seed=4)).cuda()
+    sims = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("P2S_COLS_NP", mode)
+        out = torch.empty((F, 1, H, W), device="cuda")
+        plan.simulate_frames(img, 0, SEED, 1, F, out)
+        torch.cuda.synchronize()
+        sims.append(out.cpu().numpy())
+    assert rel_l2(sims[0], sims[1]) <= 1e-4
+
+
 @pytest.mark.parametrize("H,W", [(45, 75), (64, 96), (1080, 1920)])
 def test_ar_row_pair_kernel_matches_row_kernel(H, W, monkeypatch):
     """The AR(1) row-pair kernel (k_rows_ar_pair: mirror state = conjugate, one draw per bin
