@@ -60,6 +60,21 @@ static void radix_plan(int N, AxisFFT& a, bool columns) {
   // a radix-16 pass of a 256-point row leaves most of their threads idle)
   const bool pow2 = (N & (N - 1)) == 0;
   if (N != 512 && (!pow2 || columns) && !(small && atoi(small))) {
+    // columns: prefer three radices >= 9 (1080 = 12 x 10 x 9 rather than 15 x 12 x 6), so
+    // every pass has at most one butterfly per thread and the persistent in-place column
+    // kernel (k_cols_p) applies
+    static const int wide[] = {16, 15, 12, 10, 9};
+    if (columns && !pow2)
+      for (int r1 : wide)
+        for (int r2 : wide)
+          for (int r3 : wide)
+            if (r1 >= r2 && r2 >= r3 && r1 * r2 * r3 == N) {
+              a.rad[0] = r1;
+              a.rad[1] = r2;
+              a.rad[2] = r3;
+              a.nrad = 3;
+              return;
+            }
     static const int big[] = {16, 15, 12, 10, 9, 8, 6, 5, 4, 3, 2};
     while (m > 1) {
       for (int r : big)
