@@ -502,6 +502,66 @@ __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
   }
 }
 
+// In-place variant for long rows whose plan has at most one butterfly per thread per pass
+// ((Q/R)*2 <= NT): one exchange buffer and the sqrt(S) rows read straight from global memory
+// (once per frame and bin) halve the shared memory (4K: 222 -> 95 KB), so two CTAs share
+// an SM and one's Philox/butterfly work overlaps the other's barriers and stores.
+template <int NT, bool ETA = false>
+__global__ void __launch_bounds__(NT, 2) k_rows_pair_ip(RowArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int Q = a.Q;
+  float2* twq = reinterpret_cast<float2*>(smem);  // [Q] twiddles
+  float2* X = twq + Q;                             // [Q][2] interleaved rows (padded)
+  __shared__ FFTPlanSmem fpl;
+  stage_fft_plan(&fpl, a.fq, twq);
+  const int ky = blockIdx.x, p = blockIdx.y;
+  const int k1 = ky ? a.P - ky : 0;
+  const size_t plane = (size_t)p * a.P * Q;
+  const float2* sS0 = a.sqrtS + plane + (size_t)ky * Q;
+  const float2* sS1 = a.sqrtS + plane + (size_t)k1 * Q;
+  __syncthreads();
+  for (int t = 0; t < a.F; ++t) {
+    const int64_t fr = a.frame0 + t;
+    const int64_t fr_noise = a.flow ? 0 : fr;  // frozen flow: one realisation, translated
+    const float2 phy = a.flow ? flow_phase(ky, a.P, a.vy * (double)fr) : make_float2(1.f, 0.f);
+    for (int kx = threadIdx.x; kx < Q; kx += NT) {
+      const int km = kx ? Q - kx : 0;
+      float4 z, zm;
+      if (ETA) {  // given eta (reading Q8 scaling): zeta = eta / sqrt(PQ/2), each bin read as stored
+        const float inv = rsqrtf(0.5f * (float)a.P * (float)Q);
+        const size_t PQ = (size_t)a.P * Q;
+        const float2* ea = a.eta + ((size_t)t * a.nslots + 2 * p) * PQ;
+        const bool hb = 2 * p + 1 < a.nslots;
+        const float2 a0 = ea[(size_t)ky * Q + kx], b0 = hb ? ea[PQ + (size_t)ky * Q + kx] : make_float2(0.f, 0.f);
+        const float2 a1 = ea[(size_t)k1 * Q + km], b1 = hb ? ea[PQ + (size_t)k1 * Q + km] : make_float2(0.f, 0.f);
+        z = make_float4(a0.x * inv, a0.y * inv, b0.x * inv, b0.y * inv);
+        zm = make_float4(a1.x * inv, a1.y * inv, b1.x * inv, b1.y * inv);
+      } else {
+        z = spectral_noise(ky, kx, a.P, Q, p, fr_noise, a.k0, a.k1);
+        zm = make_float4(z.x, -z.y, z.z, -z.w);  // mirror: conjugate noise
+      }
+      float2 y0 = spectrum(__ldg(&sS0[kx]), z);
+      float2 y1 = spectrum(__ldg(&sS1[km]), zm);
+      if (a.flow) {  // the mirror bin's factor is the conjugate (Hermitian shift factors)
+        const float2 ph = cmul(phy, flow_phase(kx, Q, a.vx * (double)fr));
+        y0 = cmul(y0, ph);
+        y1 = cmul(y1, make_float2(ph.x, -ph.y));
+      }
+      X[pidx(2 * kx)] = y0;
+      X[pidx(2 * km + 1)] = y1;
+    }
+    __syncthreads();
+    smem_ifft_inplace<NT>(X, &fpl, 1);
+    const float2* R = X;
+    float2* dst = a.Zout + (size_t)t * a.npairs * a.P * Q + plane;
+    for (int x = threadIdx.x; x < Q; x += NT) {
+      dst[(size_t)ky * Q + x] = R[pidx(2 * x)];
+      if (k1 != ky) dst[(size_t)k1 * Q + x] = R[pidx(2 * x + 1)];
+    }
+    __syncthreads();
+  }
+}
+
 // White-noise rows at Q = 512: one CTA per (Hermitian row pair, mode pair); NG groups of
 // 64 threads, each group transforms one frame at a time (frames g, g + NG, ...).  Thread t
 // owns butterfly t of row ky and butterfly (64 - t) % 64 of row P - ky, which holds exactly
@@ -792,6 +852,19 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
     k_rows_pair512<NG><<<grid, 64 * NG, sm, s>>>(a);
   } else {
     dim3 grid(pl->P / 2 + 1, pl->npairs);
+    // only where the ping-pong kernel fits one CTA per SM (4K: 222 KB; at 1920 points it
+    // already fits two, and the in-place variant measured slower there: 2.94 vs 2.50 ms)
+    const size_t sm_pp = ((size_t)3 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
+    if (pl->Q > 1024 && 2 * sm_pp > 227 * 1024 && getenv_flag("P2S_ROWS_NIP") == 0) {
+      bool one = true;  // every pass at most one butterfly per thread (two interleaved rows)
+      for (int i = 0; i < pl->fq.nrad; ++i) one = one && (pl->Q / pl->fq.rad[i]) * 2 <= 512;
+      if (one) {
+        size_t sm = ((size_t)pl->Q + padded_len(2 * pl->Q)) * sizeof(float2);
+        cudaFuncSetAttribute(k_rows_pair_ip<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_rows_pair_ip<512><<<grid, 512, sm, s>>>(a);
+        return (int)cudaGetLastError();
+      }
+    }
     size_t sm = ((size_t)3 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
     if (pl->Q > 1024) {
       cudaFuncSetAttribute(k_rows_pair<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

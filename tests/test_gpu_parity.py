@@ -181,6 +181,41 @@ def test_persistent_column_kernel_vs_oracle():
     assert worst <= 1e-4, worst
 
 
+def test_inplace_row_kernel_vs_oracle():
+    """Q = 2400 (radices 16 x 15 x 10, two interleaved rows, <= 512 butterflies per pass;
+    the ping-pong kernel would need 165 KB) takes the in-place row kernel (k_rows_pair_ip,
+    sqrt(S) read from global); fields against the oracle."""
+    H, W, F = 20, 2400, 2
+    plan, _, _, sq, L = make_plan(H, W, 1, 2.0, 16, 17)
+    assert plan.Q == 2400
+    z = torch.empty((F, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 5, F, z)
+    torch.cuda.synchronize()
+    got = z.cpu().numpy()
+    ref = pipeline.sample_zernike(SEED, 5, F, sq, L, H, W)
+    worst = max(rel_l2(got[f, j], ref[f, j]) for f in range(F) for j in range(1, 36))
+    assert worst <= 1e-4, worst
+
+
+@pytest.mark.parametrize("H,W,F", [(1080, 1920, 2), (2160, 3840, 1)])
+def test_inplace_row_kernel_matches_pingpong_kernel(H, W, F, monkeypatch):
+    """k_rows_pair_ip against k_rows_pair (P2S_ROWS_NIP=1) at the cfg4/cfg5 geometries:
+    same draws and butterflies, fields equal to fp32 rounding."""
+    from paper_2210_06713_b200 import Plan, PlanConfig
+    plan = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=3.0, Z=36, K=16, taps=17),
+                synth.basis(16, 17, seed=1), synth.mlp_weights(16, n_in=33, seed=1))
+    outs = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("P2S_ROWS_NIP", mode)
+        z = torch.empty((F, 36, H, W), device="cuda")
+        plan.sample_zernike(SEED, 3, F, z)
+        torch.cuda.synchronize()
+        outs.append(z.cpu().numpy())
+    a, b = outs
+    worst = max(rel_l2(a[f, j], b[f, j]) for f in range(F) for j in range(1, 36))
+    assert worst <= 1e-6, worst
+
+
 @pytest.mark.parametrize("H,W,F", [(1080, 1920, 2), (2160, 3840, 1)])
 def test_persistent_column_kernel_matches_per_block_kernel(H, W, F, monkeypatch):
     """k_cols_p (persistent, cp.async prefetch, in-place passes) against k_cols
