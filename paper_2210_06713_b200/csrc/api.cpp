@@ -340,7 +340,7 @@ static size_t frame_bytes(const p2s_plan_s* p) {
   const size_t HW = (size_t)p->H * p->W, PQ = (size_t)p->P * p->Q;
   size_t b = 0;
   b += PQ * p->npairs * sizeof(float2);
-  b += HW * (size_t)std::max(p->nslots, p->Z - 3) * 2;
+  b += (size_t)p->H * ((p->W + 127) / 128) * 128 * (size_t)std::max(p->nslots, p->Z - 3) * 2;
   b += 2 * HW * 4;
   b += (size_t)p->C * HW * 2;
   b += (size_t)p->H * ((p->W + 127) / 128) * 128 * (size_t)p->mg_fold.n3 * 2;
@@ -359,7 +359,8 @@ static p2s_status alloc_workspace(p2s_plan_s* p) {
     return r;
   };
   p->d_Z = reinterpret_cast<float2*>(take(mb * PQ * p->npairs * sizeof(float2)));
-  p->d_X = reinterpret_cast<uint16_t*>(take(mb * HW * (size_t)std::max(p->nslots, p->Z - 3) * 2));
+  p->d_X = reinterpret_cast<uint16_t*>(
+      take(mb * (size_t)p->H * ((p->W + 127) / 128) * 128 * (size_t)std::max(p->nslots, p->Z - 3) * 2));
   p->d_tilt = reinterpret_cast<float*>(take(mb * 2 * HW * 4));
   p->d_Iw = reinterpret_cast<uint16_t*>(take(mb * (size_t)p->C * HW * 2));
   p->ntx = (p->W + 127) / 128;

@@ -791,6 +791,16 @@ static int getenv_flag(const char* name) {
   const char* v = getenv(name);
   return v ? atoi(v) : 0;
 }
+// MLP input layout shared by its producers (k_cols*, k_zern_to_x) and k_mlp.  Tile-major
+// where the planes are far apart (H W >= 4M pixels: 4K k_mlp 2.05 -> 1.36 ms, its 35
+// per-tile plane segments were 16.6 MB apart); planes elsewhere (512^2: the column kernel's
+// stores are 0.1 ms faster into planes, k_mlp unchanged; 1080p: neutral).
+// P2S_X_PLANES=1 / P2S_X_TILES=1 force either (A/B measurements, tests).
+int x_tile_layout(const p2s_plan_s* pl) {
+  if (getenv_flag("P2S_X_PLANES")) return 0;
+  if (getenv_flag("P2S_X_TILES")) return 1;
+  return (size_t)pl->H * pl->W >= ((size_t)4 << 20) ? 1 : 0;
+}
 
 int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool ar, int ar_mode,
                 int64_t replay_from, cudaStream_t s, const float2* eta) {
@@ -883,6 +893,7 @@ struct ColArgs {
   const float2* Zin;  // [F][npairs][P][Q]
   int P, Q, H, W, npairs, nslots, Z;
   int F;  // frames (the persistent column kernel's tile count)
+  int ntx, xtile;  // MLP input layout (x_index)
   int tc_log2;
   float* zern;        // mode 0: [F][Z][H][W]
   uint16_t* X;        // mode 1: bf16 [F][nslots][H*W]
@@ -965,9 +976,15 @@ __global__ void __launch_bounds__(NT) k_cols(ColArgs a) {
       z[(size_t)(sa + 1) * HW + pix] = v.x;
       if (sb < a.nslots) z[(size_t)(sb + 1) * HW + pix] = v.y;
     } else {
-      uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
-      Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
-      if (sb < a.nslots) Xo[(size_t)sb * HW + pix] = f_to_bf16(v.y);
+      if (a.xtile) {  // tile-major (x_index); the plane path below keeps its cheaper addressing
+        uint16_t* Xt = a.X + x_index(1, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x);
+        Xt[0] = f_to_bf16(v.x);
+        if (sb < a.nslots) Xt[128] = f_to_bf16(v.y);
+      } else {
+        uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
+        Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
+        if (sb < a.nslots) Xo[(size_t)sb * HW + pix] = f_to_bf16(v.y);
+      }
       if (p == 0) {
         float* t = a.tilt + (size_t)f * 2 * HW;
         t[pix] = v.x;
@@ -1035,9 +1052,15 @@ __global__ void __launch_bounds__(NT) k_cols_p(ColArgs a) {
         z[(size_t)(sa + 1) * HW + pix] = v.x;
         if (sb < a.nslots) z[(size_t)(sb + 1) * HW + pix] = v.y;
       } else {
-        uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
-        Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
-        if (sb < a.nslots) Xo[(size_t)sb * HW + pix] = f_to_bf16(v.y);
+        if (a.xtile) {  // tile-major (x_index)
+          uint16_t* Xt = a.X + x_index(1, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x);
+          Xt[0] = f_to_bf16(v.x);
+          if (sb < a.nslots) Xt[128] = f_to_bf16(v.y);
+        } else {
+          uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
+          Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
+          if (sb < a.nslots) Xo[(size_t)sb * HW + pix] = f_to_bf16(v.y);
+        }
         if (p == 0) {
           float* t = a.tilt + (size_t)f * 2 * HW;
           t[pix] = v.x;
@@ -1116,9 +1139,15 @@ __global__ void __launch_bounds__(512) k_cols512(ColArgs a) {
       z[(size_t)(sa + 1) * HW + pix] = v.x;
       if (sb < a.nslots) z[(size_t)(sb + 1) * HW + pix] = v.y;
     } else {
-      uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
-      Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
-      if (sb < a.nslots) Xo[(size_t)sb * HW + pix] = f_to_bf16(v.y);
+      if (a.xtile) {  // tile-major (x_index); the plane path below keeps its cheaper addressing
+        uint16_t* Xt = a.X + x_index(1, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x);
+        Xt[0] = f_to_bf16(v.x);
+        if (sb < a.nslots) Xt[128] = f_to_bf16(v.y);
+      } else {
+        uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
+        Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
+        if (sb < a.nslots) Xo[(size_t)sb * HW + pix] = f_to_bf16(v.y);
+      }
       if (p == 0 && !a.fuse_warp) {
         float* tl = a.tilt + (size_t)f * 2 * HW;
         tl[pix] = v.x;
@@ -1173,6 +1202,8 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   a.nslots = pl->nslots;
   a.Z = pl->Z;
   a.F = F;
+  a.ntx = pl->ntx;
+  a.xtile = x_tile_layout(pl);
   int tcl = 4;
   while (tcl > 0 && pl->P * (1 << tcl) > kColElems) --tcl;
   a.tc_log2 = tcl;
@@ -1280,19 +1311,20 @@ int launch_mix(const p2s_plan_s* pl, int F, float* zern, cudaStream_t s) {
 }
 
 // a_4..a_Z (fp32 Zernike planes) -> bf16 MLP input planes (p2s_blur API path).
-__global__ void k_zern_to_x(const float* __restrict__ zern, uint16_t* __restrict__ X, int Z, size_t HW) {
+__global__ void k_zern_to_x(const float* __restrict__ zern, uint16_t* __restrict__ X, int Z, int H, int W, int ntx,
+                            int xtile) {
+  const size_t HW = (size_t)H * W;
   const size_t pix = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (pix >= HW) return;
-  const int f = blockIdx.y;
+  const int f = blockIdx.y, y = (int)(pix / W), x = (int)(pix - (size_t)y * W);
   const float* z = zern + (size_t)f * Z * HW + pix;
-  uint16_t* x = X + (size_t)f * (Z - 3) * HW + pix;
-  for (int k = 0; k < Z - 3; ++k) x[(size_t)k * HW] = f_to_bf16(z[(size_t)(k + 3) * HW]);
+  for (int k = 0; k < Z - 3; ++k) X[x_index(xtile, f, k, Z - 3, H, W, ntx, y, x)] = f_to_bf16(z[(size_t)(k + 3) * HW]);
 }
 
 int launch_zern_to_x(const p2s_plan_s* pl, int F, const float* zern, cudaStream_t s) {
   size_t HW = (size_t)pl->H * pl->W;
   dim3 grid((unsigned)((HW + 255) / 256), F);
-  k_zern_to_x<<<grid, 256, 0, s>>>(zern, pl->d_X, pl->Z, HW);
+  k_zern_to_x<<<grid, 256, 0, s>>>(zern, pl->d_X, pl->Z, pl->H, pl->W, pl->ntx, x_tile_layout(pl));
   return (int)cudaGetLastError();
 }
 

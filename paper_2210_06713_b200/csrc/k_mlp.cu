@@ -37,6 +37,7 @@ struct MlpArgs {
   uint32_t off_w2, off_w3, off_b1, off_b2, off_b3, blob_bytes;
   int HW, H, W, ntx, F, tiles_per_frame;
   int bias_folded;  // A1 column nin is the constant 1; biases live in the weight images
+  int xtile;        // X layout (x_index): 1 = tile-major [F][H][ntx][nin][128]
 };
 
 // Epilogue of a hidden layer: TMEM columns [0, ncols) of this thread's row -> +bias -> ReLU
@@ -88,12 +89,15 @@ __device__ __forceinline__ void wg_sync(int wg) {  // named barrier of one 128-t
 
 // A1 tile (nin planes x 128 pixels, MN-major, k linear at 16 B): pixels [pix0, pix0 + n) of
 // frame f (one row segment, n <= 128; the rest of the tile is zero).
-__device__ __forceinline__ void load_a1(const MlpArgs& a, uint8_t* A1, int f, int pix0, int n, int ltid, bool async) {
+__device__ __forceinline__ void load_a1(const MlpArgs& a, uint8_t* A1, int tile, int f, int pix0, int n, int ltid,
+                                        bool async) {
   const uint16_t* Xf = a.X + (size_t)f * a.nin * a.HW;
+  const uint16_t* Xt = a.X + (size_t)tile * 128 * a.nin;  // tile-major: this tile's block
   for (int idx = ltid; idx < a.nin * 16; idx += 128) {
     const int k = idx % a.nin, g = idx / a.nin;
     const int o = 8 * g;
-    const uint16_t* src = Xf + (size_t)k * a.HW + pix0 + o;
+    // tile-major: plane k of this tile at k * 128 elements of its contiguous block
+    const uint16_t* src = a.xtile ? Xt + (size_t)k * 128 + o : Xf + (size_t)k * a.HW + pix0 + o;
     uint8_t* dst = A1 + g * (a.k1 * 16) + k * 16;
     if (async) {  // W % 8 == 0: whole 16-byte chunks, zero-filled past the row segment
       cp_async16(dst, o < n ? src : a.X, o < n ? 16u : 0u);
@@ -197,7 +201,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
   if (tile < ntiles) {
     int f, pix0, n;
     tile_pixels(a, tile, f, pix0, n);
-    load_a1(a, A1, f, pix0, n, ltid, async);
+    load_a1(a, A1, tile, f, pix0, n, ltid, async);
   }
   cp_async_commit();
   for (; tile < ntiles; tile += stride) {
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
       if (nxt < ntiles) {
         int fn, pn, nn;
         tile_pixels(a, nxt, fn, pn, nn);
-        load_a1(a, A1, fn, pn, nn, ltid, async);
+        load_a1(a, A1, nxt, fn, pn, nn, ltid, async);
       }
       cp_async_commit();
     }
@@ -350,6 +354,7 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   a.W = p->W;
   a.ntx = p->ntx;
   a.bias_folded = g.bias_folded ? 1 : 0;
+  a.xtile = x_tile_layout(p);
   a.F = F;
   a.tiles_per_frame = p->H * p->ntx;
   const int nmax = std::max(std::max(g.n1, g.n2), g.n3);

@@ -54,6 +54,16 @@ __device__ __forceinline__ float2 box_muller_fast(uint32_t a, uint32_t b) {
   return make_float2(-r * c, -r * s);
 }
 
+// MLP input X (bf16): xtile = 1 -> per 128-pixel row tile, [F][H][ntx][nin][128 px] (one
+// tile's inputs are one contiguous 256*nin-byte block, so k_mlp's 16-byte chunk loads stay
+// within a few pages; consecutive pixels stay adjacent, so the column kernels' stores keep
+// their full-sector runs); xtile = 0 -> planes [F][nin][H][W].
+__device__ __forceinline__ size_t x_index(int xtile, int f, int k, int nin, int H, int W, int ntx, int y, int x) {
+  if (!xtile) return ((size_t)f * nin + k) * (size_t)H * W + (size_t)y * W + x;
+  const int xt = x >> 7, px = x & 127;
+  return ((((size_t)f * H + y) * ntx + xt) * nin + k) * 128 + px;
+}
+
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }

@@ -171,6 +171,7 @@ int launch_warp_f32(const p2s_plan_s* p, int F, const float* img, int64_t stride
                     cudaStream_t s);
 int launch_warp_sim(const p2s_plan_s* p, int F, const float* img, int64_t stride, cudaStream_t s);
 int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s);
+int x_tile_layout(const p2s_plan_s* p);  // 1: MLP input X is tile-major (x_index in p2s_dev.cuh)
 int launch_pack_weights(const p2s_plan_s* p, int F, const float* wts, cudaStream_t s);
 int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0,
                 float* out, cudaStream_t s);

@@ -329,8 +329,10 @@ def test_blur_single_basis_vs_oracle(H, W, K, T, k0):
     assert rel_l2(out.cpu().numpy()[0, 0], ref[0]) <= 1e-2
 
 
-@pytest.mark.parametrize("H,W,C,K,T", [(64, 64, 1, 16, 17), (96, 160, 3, 100, 33)])
-def test_blur_api_vs_oracle(H, W, C, K, T):
+@pytest.mark.parametrize("x_tiles", ["0", "1"])  # 1: force the tile-major MLP input layout
+@pytest.mark.parametrize("H,W,C,K,T", [(64, 64, 1, 16, 17), (96, 160, 3, 100, 33), (40, 90, 1, 16, 17)])
+def test_blur_api_vs_oracle(H, W, C, K, T, x_tiles, monkeypatch):
+    monkeypatch.setenv("P2S_X_TILES", x_tiles)
     plan, basis, mlp, sq, L = make_plan(H, W, C, 3.0, K, T)
     a = pipeline.sample_zernike(SEED, 0, 1, sq, L, H, W).astype(np.float32)
     Iw = synth.image(H, W, C, seed=6)[None]
@@ -428,9 +430,11 @@ def test_oversized_mlp_is_unsupported():
     assert e.value.status == 5  # P2S_ERR_UNSUPPORTED
 
 
-def test_simulate_ar_sequence_vs_oracle():
+@pytest.mark.parametrize("x_tiles", ["0", "1"])  # 1: force the tile-major MLP input layout
+def test_simulate_ar_sequence_vs_oracle(x_tiles, monkeypatch):
     """Steps 1-5 on an AR(1) sequence (reading Q18): a fresh start and the stored-state
     continuation both follow the oracle's replayed sequence."""
+    monkeypatch.setenv("P2S_X_TILES", x_tiles)
     H, W, C, K, T, alpha = 64, 96, 2, 16, 17, 0.9
     plan, basis, mlp, sq, L = make_plan(H, W, C, 3.0, K, T, ar_alpha=alpha)
     img = synth.image(H, W, C, seed=13)
