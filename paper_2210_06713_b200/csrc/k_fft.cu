@@ -834,8 +834,13 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
     return (int)cudaGetLastError();
   }
   const int Q = pl->Q, NTp = Q > 1024 ? 512 : 256, mb = (Q + NTp - 1) / NTp;
-  const int ar_rows = getenv_flag("P2S_AR_ROWS");  // 1: always k_rows_ar, 2: always the pair kernel
-  if (ar && mb <= 8 && ar_rows != 1 && (Q > 1024 || ar_rows == 2)) {
+  const int ar_rows = getenv_flag("P2S_AR_ROWS");  // 1: always k_rows_ar, 2: the 256/512-thread pair kernel
+  if (ar && ar_rows == 0 && Q <= 512) {
+    // short rows: 128-thread row-pair CTAs keep the grid's CTA count up where each CTA
+    // runs a long frame sequence (cfg2, Q = 256, 100 frames: 1.57 -> 1.38 ms vs k_rows_ar;
+    // 256-thread pair CTAs 1.84 ms)
+    launch_rows_ar_pair<128, 4>(a, pl->P, pl->npairs, Q, s);
+  } else if (ar && mb <= 8 && ar_rows != 1 && (Q > 1024 || ar_rows == 2)) {
     if (NTp == 512) {
       if (mb <= 4) launch_rows_ar_pair<512, 4>(a, pl->P, pl->npairs, Q, s);
       else launch_rows_ar_pair<512, 8>(a, pl->P, pl->npairs, Q, s);
