@@ -84,7 +84,24 @@ typedef struct {
                               * frame 0 of the sequence translated by t (vx, vy) on the periodic
                               * grid (exact sub-pixel shift in the spectral domain, Q23).
                               * Exclusive with ar_alpha.  Default (0, 0). */
+  unsigned int force;       /* kernel-selection overrides, P2S_FORCE_* bits; 0 = the production
+                               dispatch.  For parity tests that pin one kernel variant against
+                               another and for A/B measurements: every variant computes the
+                               same result (up to rounding).  Read once, by p2s_plan_create; the
+                               library reads no environment variables. */
 } p2s_options;
+
+/* p2s_options.force bits */
+#define P2S_FORCE_FFT_GENERIC     0x001u /* generic shared-memory Stockham even at 512 points  */
+#define P2S_FORCE_FFT_SMALL_RADIX 0x002u /* radices <= 8 only (no composite 9..16 butterflies) */
+#define P2S_FORCE_AR_ROW_KERNEL   0x004u /* AR(1): one CTA per spectral row (k_rows_ar)        */
+#define P2S_FORCE_AR_PAIR_KERNEL  0x008u /* AR(1): Hermitian row-pair CTAs (k_rows_ar_pair)    */
+#define P2S_FORCE_ROWS_PINGPONG   0x010u /* long rows: ping-pong buffers, not in place         */
+#define P2S_FORCE_COLS_PER_BLOCK  0x020u /* long columns: one CTA per block, not persistent    */
+#define P2S_FORCE_X_PLANES        0x040u /* MLP inputs as [F][slot][H*W] planes                */
+#define P2S_FORCE_X_TILES         0x080u /* MLP inputs tile-major [F][H][ntx][slot][128]       */
+#define P2S_FORCE_NO_WARP_FUSION  0x100u /* step 2 as its own kernel, not in the column pass   */
+#define P2S_FORCE_BLUR_SINGLE     0x200u /* blur on single CTAs (cta_group::1), not CTA pairs  */
 
 /* Build a plan (P:312-330 generation setup; runs once, off the per-frame clock).
  *   H, W        image size in pixels (>= T, <= 8192)

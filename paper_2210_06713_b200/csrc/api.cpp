@@ -48,18 +48,17 @@ static uint16_t host_bf16(float f) {
   return u;
 }
 
-static void radix_plan(int N, AxisFFT& a, bool columns) {
+static void radix_plan(int N, AxisFFT& a, bool columns, bool small_only) {
   a.N = N;
   a.nrad = 0;
   int m = N;
   // composite radices up to 16 done in registers: 1080, 1920, 2160, 3840 take three
   // shared-memory passes instead of five or six, 256 two instead of three; 512 keeps the
   // radix-8 plan the 512-point register kernels match on
-  const char* small = getenv("P2S_FFT_SMALL_RADIX");
   // (powers of two: columns only -- the row kernels run one or two sequences per CTA and
   // a radix-16 pass of a 256-point row leaves most of their threads idle)
   const bool pow2 = (N & (N - 1)) == 0;
-  if (N != 512 && (!pow2 || columns) && !(small && atoi(small))) {
+  if (N != 512 && (!pow2 || columns || N == 4096) && !small_only) {
     // columns: prefer three radices >= 9 (1080 = 12 x 10 x 9 rather than 15 x 12 x 6), so
     // every pass has at most one butterfly per thread and the persistent in-place column
     // kernel (k_cols_p) applies
@@ -192,23 +191,19 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   g.nct = std::max(g.NC, 23);  // the partial column group reaches chunk 22 when T < 8
   g.np = round16(K);
   g.racc = std::max(1, 4 / p->C);
-  const char* pe = getenv("P2S_BLUR_PAIR");
-  g.pair = pe ? (atoi(pe) != 0) : true;
+  g.pair = !(p->force & P2S_FORCE_BLUR_SINGLE);
   // B ring: a stage is kBlurStepsPerStage (7) K-steps x C*racc MMAs.  Large stages keep
   // the single MMA-issuing thread ahead of the tensor pipe (one barrier wait + commit per
   // 21 MMAs; measured 4 -> 7: 8.3 -> 7.6 ms per 64 frames); 4 stages cover the L2 latency
   // of the B reloads.  Pair mode halves the bytes.
-  const char* se = getenv("P2S_BLUR_STAGES");
-  g.stages = se ? std::max(2, std::min(12, atoi(se))) : (g.pair ? 4 : 3);
+  g.stages = g.pair ? 4 : 3;
   {
     int nsm = 148;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) nsm = 148;
     p->nsm = nsm;
   }
   p->ntx = (p->W + 127) / 128;
-  const char* rbe = getenv("P2S_BLUR_RB");
-  g.RB = rbe ? std::max(g.racc, atoi(rbe) / g.racc * g.racc)
-             : blur_rows_per_cta(p->C, T, g.np, g.racc, p->H, p->W, g.pair, g.stages, p->max_batch, p->nsm);
+  g.RB = blur_rows_per_cta(p->C, T, g.np, g.racc, p->H, p->W, g.pair, g.stages, p->max_batch, p->nsm);
   g.RS = blur_tile_rows(g.RB, T, g.g8, g.lr);
   const uint32_t sbo = (uint32_t)blur_rs_pad(g.RS) * 16;
   const uint32_t main_bytes = blur_main_bytes(g.NC, g.RS);
@@ -280,8 +275,7 @@ static p2s_status build_blur(p2s_plan_s* p, const float* basis) {
   }
   // Every CTA streams the same B tiles at about the same time; brep copies (CTA picks one by
   // its index) spread those reads over more L2 slices.
-  const char* re = getenv("P2S_BLUR_BREP");
-  g.brep = re ? std::max(1, std::min(64, atoi(re))) : 8;
+  g.brep = 8;
   g.bstride = (img.size() + 4095) & ~(size_t)4095;
   P2S_CUDA(cudaMalloc(&g.bimg, g.bstride * g.brep), "cudaMalloc blur B");
   for (int r = 0; r < g.brep; ++r)
@@ -530,6 +524,12 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
   p->normalize = o.normalize_psf_sum;
   p->clamp01 = o.clamp01;
   p->device = dev;
+  p->force = o.force;
+  if ((o.force & P2S_FORCE_X_PLANES) && (o.force & P2S_FORCE_X_TILES))
+    return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "P2S_FORCE_X_PLANES and _X_TILES are exclusive");
+  if ((o.force & P2S_FORCE_AR_ROW_KERNEL) && (o.force & P2S_FORCE_AR_PAIR_KERNEL))
+    return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "P2S_FORCE_AR_ROW_KERNEL and _AR_PAIR_KERNEL are exclusive");
+  p->xtile = x_tile_layout(p);
   p->P = grid_size(pad * H);
   p->Q = grid_size(pad * W);
   if (p->P > 4096 || p->Q > 4096) {
@@ -575,8 +575,12 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
     p->clamped_max = *std::max_element(cl.begin(), cl.end());
   }
   P2S_TRY(upload_sqrtS(p));
-  radix_plan(p->Q, p->fq, false);
-  radix_plan(p->P, p->fp, true);
+  radix_plan(p->Q, p->fq, false, p->force & P2S_FORCE_FFT_SMALL_RADIX);
+  radix_plan(p->P, p->fp, true, p->force & P2S_FORCE_FFT_SMALL_RADIX);
+  if (rows_smem_bytes(p, p->ar_alpha != 0.f, false) > 227 * 1024) {
+    free_plan(p);
+    return set_error(P2S_ERR_UNSUPPORTED, "no row-pass kernel fits shared memory for this FFT row length");
+  }
   P2S_TRY(upload_twiddles(p->fq));
   P2S_TRY(upload_twiddles(p->fp));
   {
@@ -688,6 +692,8 @@ extern "C" p2s_status p2s_sample_zernike_from_noise(p2s_plan p, const float* eta
   CHECK_PLAN();
   if (nframes == 0) return P2S_OK;
   if (!eta || !zern) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (rows_smem_bytes(p, false, true) > 227 * 1024)
+    return set_error(P2S_ERR_UNSUPPORTED, "the given-noise row kernel does not fit shared memory at this row length");
   DeviceGuard guard(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t per = (size_t)p->Z * p->H * p->W;
@@ -801,13 +807,6 @@ extern "C" p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t 
 // compute(next) >= copy(previous)), the last copy is the exposed tail.  Minimum over
 // non-increasing size sequences by dynamic programming over (remaining, previous size).
 static std::vector<int> host_schedule_uncached(const p2s_plan_s* p, int F) {
-  const char* fix = getenv("P2S_HOST_SUB");
-  if (fix) {
-    const int s = std::max(1, atoi(fix));
-    std::vector<int> v;
-    for (int r = F; r > 0; r -= s) v.push_back(std::min(s, r));
-    return v;
-  }
   const BlurGeom& g = p->bg;
   const double px = (double)p->H * p->W / 262144.0;
   const double row_ms = 8.1e-3 * (double)p->C * g.racc * g.nks / (3.0 * 69.0);

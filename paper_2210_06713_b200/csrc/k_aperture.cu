@@ -236,7 +236,7 @@ int launch_aperture(const p2s_plan_s* p, const float* zern, int nframes, const i
   ApArgs a{zern, p->d_ztab, pix, partial, (int64_t)nframes * npix, npix, p->Z, (int64_t)p->H * p->W};
   const int grid = aperture_grid(a.nsamples);
   const size_t sm = aperture_smem();
-  cudaFuncSetAttribute(k_aperture, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  P2S_SMEM_OPTIN(k_aperture, sm);
   k_aperture<<<grid, kThreads, sm, s>>>(a);
   k_aperture_reduce<<<kSlots / 256, 256, 0, s>>>(partial, grid, a.nsamples, out);
   return (int)cudaGetLastError();

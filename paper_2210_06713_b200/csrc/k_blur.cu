@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
 template <bool SRC_F32, int C, int RACC, bool PAIR>
 static int launch_blur_t(const BlurArgs& a, const CUtensorMap& tb, dim3 grid, size_t sm, cudaStream_t s) {
   auto kern = k_blur<SRC_F32, C, RACC, PAIR>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  P2S_SMEM_OPTIN(kern, sm);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kBlurThreads);
@@ -596,8 +596,14 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.normalize = p->normalize;
   a.clamp01 = p->clamp01;
   a.probe = nullptr;
+  // phase cycle counters: a tuning build only (make EXTRA=-DP2S_BLUR_PROBE)
+#ifdef P2S_BLUR_PROBE
   static unsigned long long* probe = nullptr;
-  const bool want_probe = getenv("P2S_BLUR_PROBE") != nullptr;
+  const bool want_probe = true;
+#else
+  unsigned long long* probe = nullptr;
+  const bool want_probe = false;
+#endif
   if (want_probe) {
     if (!probe) cudaMalloc(&probe, 12 * sizeof(unsigned long long));
     cudaMemsetAsync(probe, 0, 12 * sizeof(unsigned long long), s);

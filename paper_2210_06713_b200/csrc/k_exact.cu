@@ -221,7 +221,7 @@ int launch_exact_psf(const p2s_plan_s* p, const float* zern, const int* pix, int
                      cudaStream_t s) {
   ExactArgs a{zern, p->d_ztab, nullptr, out, pix, n, p->Z, p->H, p->W, p->C, p->T, include_tilt};
   const size_t sm = exact_smem(p->T);
-  cudaFuncSetAttribute(k_exact_psf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  P2S_SMEM_OPTIN(k_exact_psf, sm);
   k_exact_psf<<<n, 512, sm, s>>>(a);
   return (int)cudaGetLastError();
 }
@@ -230,7 +230,7 @@ int launch_render_exact(const p2s_plan_s* p, const float* img, const float* zern
                         cudaStream_t s) {
   ExactArgs a{zern, p->d_ztab, img, out, nullptr, p->H * p->W, p->Z, p->H, p->W, p->C, p->T, include_tilt};
   const size_t sm = exact_smem(p->T);
-  cudaFuncSetAttribute(k_render_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  P2S_SMEM_OPTIN(k_render_exact, sm);
   k_render_exact<<<p->H * p->W, 512, sm, s>>>(a);
   return (int)cudaGetLastError();
 }

@@ -775,31 +775,97 @@ __global__ void __launch_bounds__(NT) k_rows_ar_pair(RowArgs a) {
   }
 }
 
-template <int NT, int MB>
-static void launch_rows_ar_pair(const RowArgs& a, int P, int npairs, int Q, cudaStream_t s) {
-  dim3 grid(P / 2 + 1, npairs);
-  size_t sm = ((size_t)3 * Q + 2 * padded_len(2 * Q)) * sizeof(float2);
-  cudaFuncSetAttribute(k_rows_ar_pair<NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_rows_ar_pair<NT, MB><<<grid, NT, sm, s>>>(a);
-}
-
-// The register fast path needs a 512-point axis planned as radix 8 x 8 x 8.
+// The 512-point register fast path needs a 512-point axis planned as radix 8 x 8 x 8.
 static bool reg512(const AxisFFT& ax) {
   return ax.N == kRegN && ax.nrad == 3 && ax.rad[0] == 8 && ax.rad[1] == 8 && ax.rad[2] == 8;
 }
-static int getenv_flag(const char* name) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : 0;
-}
-// MLP input layout shared by its producers (k_cols*, k_zern_to_x) and k_mlp.  Tile-major
-// where the planes are far apart (H W >= 4M pixels: 4K k_mlp 2.05 -> 1.36 ms, its 35
-// per-tile plane segments were 16.6 MB apart); planes elsewhere (512^2: the column kernel's
-// stores are 0.1 ms faster into planes, k_mlp unchanged; 1080p: neutral).
-// P2S_X_PLANES=1 / P2S_X_TILES=1 force either (A/B measurements, tests).
+
+// MLP input layout shared by its producers (k_cols*, k_zern_to_x) and k_mlp, decided once
+// at plan creation (p2s_plan_s::xtile).  Tile-major where the planes are far apart
+// (H W >= 4M pixels: 4K k_mlp 2.05 -> 1.36 ms, its 35 per-tile plane segments were 16.6 MB
+// apart); planes elsewhere (512^2: the column kernel's stores are 0.1 ms faster into planes,
+// k_mlp unchanged; 1080p: neutral).  P2S_FORCE_X_PLANES / _X_TILES force either.
 int x_tile_layout(const p2s_plan_s* pl) {
-  if (getenv_flag("P2S_X_PLANES")) return 0;
-  if (getenv_flag("P2S_X_TILES")) return 1;
+  if (pl->force & P2S_FORCE_X_PLANES) return 0;
+  if (pl->force & P2S_FORCE_X_TILES) return 1;
   return (size_t)pl->H * pl->W >= ((size_t)4 << 20) ? 1 : 0;
+}
+
+// Row-pass kernel variants (one per dispatch outcome of rows_variant).
+enum RowVariant {
+  RV_GIVEN_NOISE,   // k_rows_pair<256, true>: caller-supplied spectral noise
+  RV_AR_PAIR_128,   // k_rows_ar_pair<128, 4>: AR(1), Q <= 512
+  RV_AR_PAIR_256_1, RV_AR_PAIR_256_2, RV_AR_PAIR_256_4, RV_AR_PAIR_512_4, RV_AR_PAIR_512_8,
+  RV_AR_ROW_128, RV_AR_ROW_512,  // k_rows_ar<NT>: one CTA per spectral row
+  RV_REG512,        // k_rows_pair512<4>
+  RV_PAIR_IP_512,   // k_rows_pair_ip<512>: in place, long rows
+  RV_PAIR_256, RV_PAIR_512  // k_rows_pair<NT>: ping-pong
+};
+
+static size_t smem_pair(int Q) { return ((size_t)3 * Q + 2 * padded_len(2 * (size_t)Q)) * sizeof(float2); }
+static size_t smem_ar_row(int Q) {
+  return ((size_t)2 * Q + 2 * padded_len(Q)) * sizeof(float2) + (size_t)Q * sizeof(float4) + 16;
+}
+static size_t smem_pair_ip(int Q) { return ((size_t)Q + padded_len(2 * (size_t)Q)) * sizeof(float2); }
+constexpr size_t kSmemMax = 227 * 1024;
+
+// The row kernel the plan runs for white noise / AR(1) / given noise, and its dynamic shared
+// memory.  Where the preferred kernel would exceed the per-CTA limit the next one that fits
+// is taken; plan creation rejects a plan whose row pass fits none (rows_smem_bytes).
+static RowVariant rows_variant(const p2s_plan_s* pl, bool ar, bool given, size_t* sm) {
+  const int Q = pl->Q, NTp = Q > 1024 ? 512 : 256, mb = (Q + NTp - 1) / NTp;
+  if (given) {
+    *sm = smem_pair(Q);
+    return RV_GIVEN_NOISE;
+  }
+  // in place: every pass at most one butterfly per thread (two interleaved rows)
+  bool one = true;
+  for (int i = 0; i < pl->fq.nrad; ++i) one = one && (Q / pl->fq.rad[i]) * 2 <= 512;
+  if (ar) {
+    // 1: always k_rows_ar, 2: the 256/512-thread pair kernel (P2S_FORCE_AR_*)
+    const int ar_rows = (pl->force & P2S_FORCE_AR_ROW_KERNEL) ? 1 : (pl->force & P2S_FORCE_AR_PAIR_KERNEL) ? 2 : 0;
+    if (ar_rows == 0 && Q <= 512) {
+      // short rows: 128-thread row-pair CTAs keep the grid's CTA count up where each CTA
+      // runs a long frame sequence (cfg2, Q = 256, 100 frames: 1.57 -> 1.38 ms vs k_rows_ar;
+      // 256-thread pair CTAs 1.84 ms)
+      *sm = smem_pair(Q);
+      return RV_AR_PAIR_128;
+    }
+    if (mb <= 8 && ar_rows != 1 && (Q > 1024 || ar_rows == 2) && smem_pair(Q) <= kSmemMax) {
+      *sm = smem_pair(Q);
+      if (NTp == 512) return mb <= 4 ? RV_AR_PAIR_512_4 : RV_AR_PAIR_512_8;
+      return mb <= 1 ? RV_AR_PAIR_256_1 : mb <= 2 ? RV_AR_PAIR_256_2 : RV_AR_PAIR_256_4;
+    }
+    *sm = smem_ar_row(Q);
+    return Q > 1024 ? RV_AR_ROW_512 : RV_AR_ROW_128;
+  }
+  if (reg512(pl->fq) && !(pl->force & P2S_FORCE_FFT_GENERIC)) {
+    *sm = ((size_t)3 * kRegN + (size_t)4 * 2 * (kRegN + kRegN / 8)) * sizeof(float2);
+    return RV_REG512;
+  }
+  // in place only where the ping-pong kernel fits one CTA per SM (4K: 222 KB; at 1920
+  // points it already fits two, and the in-place variant measured slower there: 2.94 vs
+  // 2.50 ms), or does not fit at all (4096 = 16 x 16 x 16)
+  if (Q > 1024 && 2 * smem_pair(Q) > kSmemMax && one && !(pl->force & P2S_FORCE_ROWS_PINGPONG)) {
+    *sm = smem_pair_ip(Q);
+    return RV_PAIR_IP_512;
+  }
+  *sm = smem_pair(Q);
+  return Q > 1024 ? RV_PAIR_512 : RV_PAIR_256;
+}
+
+size_t rows_smem_bytes(const p2s_plan_s* pl, bool ar, bool given_noise) {
+  size_t sm = 0;
+  rows_variant(pl, ar, given_noise, &sm);
+  return sm;
+}
+
+template <int NT, int MB>
+static int launch_rows_ar_pair(const RowArgs& a, int P, int npairs, size_t sm, cudaStream_t s) {
+  dim3 grid(P / 2 + 1, npairs);
+  P2S_SMEM_OPTIN((k_rows_ar_pair<NT, MB>), sm);
+  k_rows_ar_pair<NT, MB><<<grid, NT, sm, s>>>(a);
+  return (int)cudaGetLastError();
 }
 
 int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool ar, int ar_mode,
@@ -825,69 +891,46 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
   a.vy = pl->flow_vy;
   a.eta = eta;
   a.nslots = pl->nslots;
-  if (eta) {  // caller-supplied noise: generic row kernel, no AR state, no flow
-    a.flow = 0;
-    dim3 grid(pl->P / 2 + 1, pl->npairs);
-    size_t sm = ((size_t)3 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
-    cudaFuncSetAttribute(k_rows_pair<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_rows_pair<256, true><<<grid, 256, sm, s>>>(a);
-    return (int)cudaGetLastError();
-  }
-  const int Q = pl->Q, NTp = Q > 1024 ? 512 : 256, mb = (Q + NTp - 1) / NTp;
-  const int ar_rows = getenv_flag("P2S_AR_ROWS");  // 1: always k_rows_ar, 2: the 256/512-thread pair kernel
-  if (ar && ar_rows == 0 && Q <= 512) {
-    // short rows: 128-thread row-pair CTAs keep the grid's CTA count up where each CTA
-    // runs a long frame sequence (cfg2, Q = 256, 100 frames: 1.57 -> 1.38 ms vs k_rows_ar;
-    // 256-thread pair CTAs 1.84 ms)
-    launch_rows_ar_pair<128, 4>(a, pl->P, pl->npairs, Q, s);
-  } else if (ar && mb <= 8 && ar_rows != 1 && (Q > 1024 || ar_rows == 2)) {
-    if (NTp == 512) {
-      if (mb <= 4) launch_rows_ar_pair<512, 4>(a, pl->P, pl->npairs, Q, s);
-      else launch_rows_ar_pair<512, 8>(a, pl->P, pl->npairs, Q, s);
-    } else {
-      if (mb <= 1) launch_rows_ar_pair<256, 1>(a, pl->P, pl->npairs, Q, s);
-      else if (mb <= 2) launch_rows_ar_pair<256, 2>(a, pl->P, pl->npairs, Q, s);
-      else launch_rows_ar_pair<256, 4>(a, pl->P, pl->npairs, Q, s);
-    }
-  } else if (ar) {
-    dim3 grid(pl->P, pl->npairs);
-    size_t sm = ((size_t)2 * pl->Q + 2 * padded_len(pl->Q)) * sizeof(float2) + (size_t)pl->Q * sizeof(float4) + 16;
-    if (pl->Q > 1024) {
-      cudaFuncSetAttribute(k_rows_ar<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_rows_ar<512><<<grid, 512, sm, s>>>(a);
-    } else {
-      cudaFuncSetAttribute(k_rows_ar<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_rows_ar<128><<<grid, 128, sm, s>>>(a);
-    }
-  } else if (reg512(pl->fq) && getenv_flag("P2S_FFT_GENERIC") == 0) {
-    constexpr int NG = 4;
-    dim3 grid(pl->P / 2 + 1, pl->npairs);
-    size_t sm = ((size_t)3 * kRegN + (size_t)NG * 2 * (kRegN + kRegN / 8)) * sizeof(float2);
-    cudaFuncSetAttribute(k_rows_pair512<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_rows_pair512<NG><<<grid, 64 * NG, sm, s>>>(a);
-  } else {
-    dim3 grid(pl->P / 2 + 1, pl->npairs);
-    // only where the ping-pong kernel fits one CTA per SM (4K: 222 KB; at 1920 points it
-    // already fits two, and the in-place variant measured slower there: 2.94 vs 2.50 ms)
-    const size_t sm_pp = ((size_t)3 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
-    if (pl->Q > 1024 && 2 * sm_pp > 227 * 1024 && getenv_flag("P2S_ROWS_NIP") == 0) {
-      bool one = true;  // every pass at most one butterfly per thread (two interleaved rows)
-      for (int i = 0; i < pl->fq.nrad; ++i) one = one && (pl->Q / pl->fq.rad[i]) * 2 <= 512;
-      if (one) {
-        size_t sm = ((size_t)pl->Q + padded_len(2 * pl->Q)) * sizeof(float2);
-        cudaFuncSetAttribute(k_rows_pair_ip<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_rows_pair_ip<512><<<grid, 512, sm, s>>>(a);
-        return (int)cudaGetLastError();
-      }
-    }
-    size_t sm = ((size_t)3 * pl->Q + 2 * padded_len(2 * pl->Q)) * sizeof(float2);
-    if (pl->Q > 1024) {
-      cudaFuncSetAttribute(k_rows_pair<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_rows_pair<512><<<grid, 512, sm, s>>>(a);
-    } else {
-      cudaFuncSetAttribute(k_rows_pair<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_rows_pair<256><<<grid, 256, sm, s>>>(a);
-    }
+  if (eta) a.flow = 0;  // caller-supplied noise: generic row kernel, no AR state, no flow
+  size_t sm = 0;
+  const RowVariant v = rows_variant(pl, ar, eta != nullptr, &sm);
+  if (sm > kSmemMax) return (int)cudaErrorInvalidConfiguration;
+  const dim3 gpair(pl->P / 2 + 1, pl->npairs), grow(pl->P, pl->npairs);
+  switch (v) {
+    case RV_GIVEN_NOISE:
+      P2S_SMEM_OPTIN((k_rows_pair<256, true>), sm);
+      k_rows_pair<256, true><<<gpair, 256, sm, s>>>(a);
+      break;
+    case RV_AR_PAIR_128: return launch_rows_ar_pair<128, 4>(a, pl->P, pl->npairs, sm, s);
+    case RV_AR_PAIR_256_1: return launch_rows_ar_pair<256, 1>(a, pl->P, pl->npairs, sm, s);
+    case RV_AR_PAIR_256_2: return launch_rows_ar_pair<256, 2>(a, pl->P, pl->npairs, sm, s);
+    case RV_AR_PAIR_256_4: return launch_rows_ar_pair<256, 4>(a, pl->P, pl->npairs, sm, s);
+    case RV_AR_PAIR_512_4: return launch_rows_ar_pair<512, 4>(a, pl->P, pl->npairs, sm, s);
+    case RV_AR_PAIR_512_8: return launch_rows_ar_pair<512, 8>(a, pl->P, pl->npairs, sm, s);
+    case RV_AR_ROW_512:
+      P2S_SMEM_OPTIN(k_rows_ar<512>, sm);
+      k_rows_ar<512><<<grow, 512, sm, s>>>(a);
+      break;
+    case RV_AR_ROW_128:
+      P2S_SMEM_OPTIN(k_rows_ar<128>, sm);
+      k_rows_ar<128><<<grow, 128, sm, s>>>(a);
+      break;
+    case RV_REG512:
+      P2S_SMEM_OPTIN(k_rows_pair512<4>, sm);
+      k_rows_pair512<4><<<gpair, 64 * 4, sm, s>>>(a);
+      break;
+    case RV_PAIR_IP_512:
+      P2S_SMEM_OPTIN(k_rows_pair_ip<512>, sm);
+      k_rows_pair_ip<512><<<gpair, 512, sm, s>>>(a);
+      break;
+    case RV_PAIR_512:
+      P2S_SMEM_OPTIN((k_rows_pair<512>), sm);
+      k_rows_pair<512><<<gpair, 512, sm, s>>>(a);
+      break;
+    case RV_PAIR_256:
+      P2S_SMEM_OPTIN((k_rows_pair<256>), sm);
+      k_rows_pair<256><<<gpair, 256, sm, s>>>(a);
+      break;
   }
   return (int)cudaGetLastError();
 }
@@ -1208,7 +1251,7 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   a.Z = pl->Z;
   a.F = F;
   a.ntx = pl->ntx;
-  a.xtile = x_tile_layout(pl);
+  a.xtile = pl->xtile;
   int tcl = 4;
   while (tcl > 0 && pl->P * (1 << tcl) > kColElems) --tcl;
   a.tc_log2 = tcl;
@@ -1217,8 +1260,8 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   a.tilt = pl->d_tilt;
   a.fuse_warp = 0;
   if (warp_fused) *warp_fused = false;
-  if (reg512(pl->fp) && getenv_flag("P2S_FFT_GENERIC") == 0) {
-    if (mode == 1 && img && warp_fused && getenv_flag("P2S_NO_WARP_FUSION") == 0) {
+  if (reg512(pl->fp) && !(pl->force & P2S_FORCE_FFT_GENERIC)) {
+    if (mode == 1 && img && warp_fused && !(pl->force & P2S_FORCE_NO_WARP_FUSION)) {
       const int Z = pl->Z;
       a.fuse_warp = 1;
       a.img = img;
@@ -1233,10 +1276,10 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
     dim3 grid((pl->W + 15) / 16, pl->npairs, F);  // only the W cropped columns are needed
     size_t sm = (size_t)kRegN * 17 * sizeof(float2);
     if (mode == 0) {
-      cudaFuncSetAttribute(k_cols512<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      P2S_SMEM_OPTIN((k_cols512<0>), sm);
       k_cols512<0><<<grid, 512, sm, s>>>(a);
     } else {
-      cudaFuncSetAttribute(k_cols512<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      P2S_SMEM_OPTIN((k_cols512<1>), sm);
       k_cols512<1><<<grid, 512, sm, s>>>(a);
     }
     return (int)cudaGetLastError();
@@ -1252,7 +1295,7 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
     a.tc_log2 = tcl;
   }
   const int TC = 1 << tcl;
-  if (wide && getenv_flag("P2S_COLS_NP") == 0) {
+  if (wide && !(pl->force & P2S_FORCE_COLS_PER_BLOCK)) {
     bool one = true;  // every pass at most one butterfly per thread: in-place persistent kernel
     for (int i = 0; i < pl->fp.nrad; ++i) one = one && (pl->P / pl->fp.rad[i]) * TC <= 1024;
     if (one) {
@@ -1260,10 +1303,10 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
       const int grid = std::min(ntiles, pl->num_sms);
       size_t sm = ((size_t)pl->P + 2 * padded_len((size_t)pl->P * TC)) * sizeof(float2);
       if (mode == 0) {
-        cudaFuncSetAttribute(k_cols_p<0, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        P2S_SMEM_OPTIN((k_cols_p<0, 1024>), sm);
         k_cols_p<0, 1024><<<grid, 1024, sm, s>>>(a);
       } else {
-        cudaFuncSetAttribute(k_cols_p<1, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        P2S_SMEM_OPTIN((k_cols_p<1, 1024>), sm);
         k_cols_p<1, 1024><<<grid, 1024, sm, s>>>(a);
       }
       return (int)cudaGetLastError();
@@ -1273,17 +1316,17 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   size_t sm = ((size_t)pl->P + 2 * padded_len((size_t)pl->P * TC)) * sizeof(float2);
   if (wide) {
     if (mode == 0) {
-      cudaFuncSetAttribute(k_cols<0, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      P2S_SMEM_OPTIN((k_cols<0, 1024>), sm);
       k_cols<0, 1024><<<grid, 1024, sm, s>>>(a);
     } else {
-      cudaFuncSetAttribute(k_cols<1, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      P2S_SMEM_OPTIN((k_cols<1, 1024>), sm);
       k_cols<1, 1024><<<grid, 1024, sm, s>>>(a);
     }
   } else if (mode == 0) {
-    cudaFuncSetAttribute(k_cols<0, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    P2S_SMEM_OPTIN((k_cols<0, 256>), sm);
     k_cols<0, 256><<<grid, 256, sm, s>>>(a);
   } else {
-    cudaFuncSetAttribute(k_cols<1, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    P2S_SMEM_OPTIN((k_cols<1, 256>), sm);
     k_cols<1, 256><<<grid, 256, sm, s>>>(a);
   }
   return (int)cudaGetLastError();
@@ -1329,7 +1372,7 @@ __global__ void k_zern_to_x(const float* __restrict__ zern, uint16_t* __restrict
 int launch_zern_to_x(const p2s_plan_s* pl, int F, const float* zern, cudaStream_t s) {
   size_t HW = (size_t)pl->H * pl->W;
   dim3 grid((unsigned)((HW + 255) / 256), F);
-  k_zern_to_x<<<grid, 256, 0, s>>>(zern, pl->d_X, pl->Z, pl->H, pl->W, pl->ntx, x_tile_layout(pl));
+  k_zern_to_x<<<grid, 256, 0, s>>>(zern, pl->d_X, pl->Z, pl->H, pl->W, pl->ntx, pl->xtile);
   return (int)cudaGetLastError();
 }
 

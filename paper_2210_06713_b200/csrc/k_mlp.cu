@@ -354,7 +354,7 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   a.W = p->W;
   a.ntx = p->ntx;
   a.bias_folded = g.bias_folded ? 1 : 0;
-  a.xtile = x_tile_layout(p);
+  a.xtile = p->xtile;
   a.F = F;
   a.tiles_per_frame = p->H * p->ntx;
   const int nmax = std::max(std::max(g.n1, g.n2), g.n3);
@@ -364,7 +364,7 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   int nwg = std::min(kMlpWG, 512 / cols_wg);
   while (nwg > 1 && blob_al + nwg * per_wg + 64 > 227 * 1024) --nwg;
   size_t sm = blob_al + nwg * per_wg + 64;
-  cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  P2S_SMEM_OPTIN(k_mlp, sm);
   const int ntiles = F * a.tiles_per_frame;
   int grid = p->num_sms;  // persistent: one CTA (nwg tile pipelines) per SM
   if (nwg * grid > ntiles) grid = (ntiles + nwg - 1) / nwg;

@@ -117,6 +117,8 @@ struct p2s_plan_s {
   float ar_alpha = 0, noise_sigma = 0;
   double flow_vx = 0, flow_vy = 0;  // frozen flow, pixels per frame (0 = off)
   int normalize = 0, clamp01 = 0, device = 0, max_batch = 0;
+  unsigned force = 0;           // p2s_options.force (P2S_FORCE_* bits), fixed at plan creation
+  int xtile = 0;                // MLP input layout, fixed at plan creation (1: tile-major, x_index)
   double clamped_max = 0;
   std::vector<double> A0, Lc;      // Z x Z
   std::vector<float> sqrtS_host;   // [nslots][P][Q]
@@ -159,6 +161,14 @@ struct p2s_plan_s {
   int num_sms = 148;
 };
 
+// Dynamic shared memory above the default 48 KB needs an opt-in per kernel; its failure
+// (a request above the 227 KB per-CTA limit) is returned, never ignored.
+#define P2S_SMEM_OPTIN(kern, bytes)                                                               \
+  do {                                                                                          \
+    cudaError_t e_ = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes)); \
+    if (e_ != cudaSuccess) return (int)e_;                                                      \
+  } while (0)
+
 namespace p2s {
 // ---- kernel launchers (k_*.cu); all return cudaGetLastError() as int ----
 int launch_rows(const p2s_plan_s* p, uint64_t seed, int64_t frame0, int F, bool ar, int ar_mode,
@@ -171,7 +181,8 @@ int launch_warp_f32(const p2s_plan_s* p, int F, const float* img, int64_t stride
                     cudaStream_t s);
 int launch_warp_sim(const p2s_plan_s* p, int F, const float* img, int64_t stride, cudaStream_t s);
 int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s);
-int x_tile_layout(const p2s_plan_s* p);  // 1: MLP input X is tile-major (x_index in p2s_dev.cuh)
+size_t rows_smem_bytes(const p2s_plan_s* p, bool ar, bool given_noise);  // row pass dynamic smem
+int x_tile_layout(const p2s_plan_s* p);  // decided at plan creation; 1: MLP input X tile-major (x_index)
 int launch_pack_weights(const p2s_plan_s* p, int F, const float* wts, cudaStream_t s);
 int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0,
                 float* out, cudaStream_t s);

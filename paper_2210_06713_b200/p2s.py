@@ -14,8 +14,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# P2S_LIB_NAME selects an alternative in-tree build (tuning experiments only).
-LIB_PATH = os.path.join(_HERE, os.environ.get("P2S_LIB_NAME", "libp2s.so"))
+LIB_PATH = os.path.join(_HERE, "libp2s.so")
 
 P2S_OK = 0
 _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "NUMERIC", 3: "CUDA", 4: "OUT_OF_MEMORY", 5: "UNSUPPORTED"}
@@ -39,7 +38,20 @@ class Options(ctypes.Structure):
                 ("s_per_px", ctypes.c_double), ("tilt_px_per_rad", ctypes.c_double), ("pad", ctypes.c_int),
                 ("mlp_hidden", ctypes.c_int * 2), ("max_batch", ctypes.c_int), ("ar_alpha", ctypes.c_float),
                 ("noise_sigma", ctypes.c_float), ("normalize_psf_sum", ctypes.c_int), ("clamp01", ctypes.c_int),
-                ("device", ctypes.c_int), ("flow_px_per_frame", ctypes.c_float * 2)]
+                ("device", ctypes.c_int), ("flow_px_per_frame", ctypes.c_float * 2), ("force", ctypes.c_uint)]
+
+
+# p2s_options.force bits (include/p2s.h): kernel-selection overrides for tests / A-B runs
+FORCE_FFT_GENERIC = 0x001
+FORCE_FFT_SMALL_RADIX = 0x002
+FORCE_AR_ROW_KERNEL = 0x004
+FORCE_AR_PAIR_KERNEL = 0x008
+FORCE_ROWS_PINGPONG = 0x010
+FORCE_COLS_PER_BLOCK = 0x020
+FORCE_X_PLANES = 0x040
+FORCE_X_TILES = 0x080
+FORCE_NO_WARP_FUSION = 0x100
+FORCE_BLUR_SINGLE = 0x200
 
 
 def _load():
@@ -200,6 +212,7 @@ class PlanConfig:
     clamp01: bool = False
     device: int = 0
     flow: tuple = (0.0, 0.0)  # frozen flow (vx, vy) pixels per frame (NEXT-3)
+    force: int = 0  # FORCE_* bits (kernel-selection overrides; 0 = production dispatch)
     extra: dict = field(default_factory=dict)
 
 
@@ -225,6 +238,7 @@ class Plan:
         o.clamp01 = int(cfg.clamp01)
         o.device = cfg.device
         o.flow_px_per_frame[0], o.flow_px_per_frame[1] = cfg.flow
+        o.force = cfg.force
         self._h = ctypes.c_void_p()
         _check(lib.p2s_plan_create(ctypes.byref(self._h), cfg.H, cfg.W, cfg.C, float(cfg.d_over_r0),
                                    float(cfg.L_m), cfg.Z, cfg.K, basis.ctypes.data, mlp.ctypes.data, ctypes.byref(o)))

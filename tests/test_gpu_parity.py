@@ -117,16 +117,17 @@ def test_sample_zernike_register_fft_path_vs_oracle(H, W, F):
     assert worst <= 1e-4, worst
 
 
-def test_register_fft_matches_generic_fft(monkeypatch):
+def test_register_fft_matches_generic_fft():
     """The 512-point register kernels and the generic shared-memory Stockham kernels run
     the same radix-8 passes: their fields agree to fp32 rounding."""
+    from paper_2210_06713_b200 import FORCE_FFT_GENERIC
     H = W = 512
     plan, _, _, _, _ = make_plan(H, W, 1, 3.0, 16, 17)
     zf = torch.empty((2, 36, H, W), device="cuda")
     plan.sample_zernike(SEED, 0, 2, zf)
-    monkeypatch.setenv("P2S_FFT_GENERIC", "1")
+    plan_g, _, _, _, _ = make_plan(H, W, 1, 3.0, 16, 17, force=FORCE_FFT_GENERIC)
     zg = torch.empty_like(zf)
-    plan.sample_zernike(SEED, 0, 2, zg)
+    plan_g.sample_zernike(SEED, 0, 2, zg)
     torch.cuda.synchronize()
     a, b = zf.cpu().numpy(), zg.cpu().numpy()
     worst = max(rel_l2(a[f, j], b[f, j]) for f in range(2) for j in range(1, 36))
@@ -146,12 +147,11 @@ def test_sample_zernike_own_tables_vs_oracle():
     assert worst <= 1e-3, worst
 
 
-@pytest.mark.parametrize("ar_rows", ["0", "2"])  # 2: force the row-pair kernel (k_rows_ar_pair)
-def test_sample_zernike_ar_sequence_and_replay(ar_rows, monkeypatch):
-    monkeypatch.setenv("P2S_AR_ROWS", ar_rows)
+@pytest.mark.parametrize("force", [0, 0x008, 0x004])  # default, row-pair (k_rows_ar_pair), row kernel (k_rows_ar)
+def test_sample_zernike_ar_sequence_and_replay(force):
     H = W = 64
     alpha = 0.95
-    plan, _, _, sq, L = make_plan(H, W, 1, 3.0, 16, 17, ar_alpha=alpha)
+    plan, _, _, sq, L = make_plan(H, W, 1, 3.0, 16, 17, ar_alpha=alpha, force=force)
     ref = pipeline.sample_zernike(SEED, 0, 6, sq, L, H, W, alpha=alpha)
     z = torch.empty((6, 36, H, W), device="cuda")
     plan.sample_zernike(SEED, 0, 4, z[:4])      # fresh sequence
@@ -198,15 +198,14 @@ def test_inplace_row_kernel_vs_oracle():
 
 
 @pytest.mark.parametrize("H,W,F", [(1080, 1920, 2), (2160, 3840, 1)])
-def test_inplace_row_kernel_matches_pingpong_kernel(H, W, F, monkeypatch):
-    """k_rows_pair_ip against k_rows_pair (P2S_ROWS_NIP=1) at the cfg4/cfg5 geometries:
-    same draws and butterflies, fields equal to fp32 rounding."""
-    from paper_2210_06713_b200 import Plan, PlanConfig
-    plan = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=3.0, Z=36, K=16, taps=17),
-                synth.basis(16, 17, seed=1), synth.mlp_weights(16, n_in=33, seed=1))
+def test_inplace_row_kernel_matches_pingpong_kernel(H, W, F):
+    """k_rows_pair_ip against k_rows_pair (P2S_FORCE_ROWS_PINGPONG) at the cfg4/cfg5
+    geometries: same draws and butterflies, fields equal to fp32 rounding."""
+    from paper_2210_06713_b200 import FORCE_ROWS_PINGPONG, Plan, PlanConfig
     outs = []
-    for mode in ("0", "1"):
-        monkeypatch.setenv("P2S_ROWS_NIP", mode)
+    for force in (0, FORCE_ROWS_PINGPONG):
+        plan = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=3.0, Z=36, K=16, taps=17, force=force),
+                    synth.basis(16, 17, seed=1), synth.mlp_weights(16, n_in=33, seed=1))
         z = torch.empty((F, 36, H, W), device="cuda")
         plan.sample_zernike(SEED, 3, F, z)
         torch.cuda.synchronize()
@@ -217,16 +216,16 @@ def test_inplace_row_kernel_matches_pingpong_kernel(H, W, F, monkeypatch):
 
 
 @pytest.mark.parametrize("H,W,F", [(1080, 1920, 2), (2160, 3840, 1)])
-def test_persistent_column_kernel_matches_per_block_kernel(H, W, F, monkeypatch):
+def test_persistent_column_kernel_matches_per_block_kernel(H, W, F):
     """k_cols_p (persistent, cp.async prefetch, in-place passes) against k_cols
-    (P2S_COLS_NP=1) at the cfg4/cfg5 geometries: the same butterflies, so the fields agree to
-    fp32 rounding; both the fp32 field output (sample_zernike) and the fused bf16 path."""
-    from paper_2210_06713_b200 import Plan, PlanConfig
-    plan = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=3.0, Z=36, K=16, taps=17),
-                synth.basis(16, 17, seed=1), synth.mlp_weights(16, n_in=33, seed=1))
+    (P2S_FORCE_COLS_PER_BLOCK) at the cfg4/cfg5 geometries: the same butterflies, so the fields
+    agree to fp32 rounding; both the fp32 field output (sample_zernike) and the fused bf16 path."""
+    from paper_2210_06713_b200 import FORCE_COLS_PER_BLOCK, Plan, PlanConfig
+    plans = [Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=3.0, Z=36, K=16, taps=17, force=force),
+                  synth.basis(16, 17, seed=1), synth.mlp_weights(16, n_in=33, seed=1))
+             for force in (0, FORCE_COLS_PER_BLOCK)]
     outs = []
-    for mode in ("0", "1"):
-        monkeypatch.setenv("P2S_COLS_NP", mode)
+    for plan in plans:
         z = torch.empty((F, 36, H, W), device="cuda")
         plan.sample_zernike(SEED, 1, F, z)
         torch.cuda.synchronize()
@@ -236,8 +235,7 @@ def test_persistent_column_kernel_matches_per_block_kernel(H, W, F, monkeypatch)
     assert worst <= 1e-6, worst
     img = torch.from_numpy(synth.image(H, W, 1, seed=4)).cuda()
     sims = []
-    for mode in ("0", "1"):
-        monkeypatch.setenv("P2S_COLS_NP", mode)
+    for plan in plans:
         out = torch.empty((F, 1, H, W), device="cuda")
         plan.simulate_frames(img, 0, SEED, 1, F, out)
         torch.cuda.synchronize()
@@ -246,18 +244,18 @@ def test_persistent_column_kernel_matches_per_block_kernel(H, W, F, monkeypatch)
 
 
 @pytest.mark.parametrize("H,W", [(45, 75), (64, 96), (256, 256), (1080, 1920)])
-def test_ar_row_pair_kernel_matches_row_kernel(H, W, monkeypatch):
+def test_ar_row_pair_kernel_matches_row_kernel(H, W):
     """The AR(1) row-pair kernel (k_rows_ar_pair: mirror state = conjugate, one draw per bin
-    pair, forced with P2S_AR_ROWS=2) against the one-CTA-per-row kernel (P2S_AR_ROWS=1): the
-    same draws and state, so the fields agree to the FFT's fp32 rounding, for a fresh start, a
-    stored-state continuation and a replayed start; odd P and Q included."""
-    from paper_2210_06713_b200 import Plan, PlanConfig
-    plan = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=3.0, Z=36, K=16, taps=17, ar_alpha=0.95),
-                synth.basis(16, 17, seed=1), synth.mlp_weights(16, n_in=33, seed=1))
+    pair, P2S_FORCE_AR_PAIR_KERNEL) against the one-CTA-per-row kernel (P2S_FORCE_AR_ROW_KERNEL):
+    the same draws and state, so the fields agree to the FFT's fp32 rounding, for a fresh start,
+    a stored-state continuation and a replayed start; odd P and Q included."""
+    from paper_2210_06713_b200 import FORCE_AR_PAIR_KERNEL, FORCE_AR_ROW_KERNEL, Plan, PlanConfig
     F = 2 if H > 512 else 3
     outs = []
-    for mode in ("0", "2", "1"):  # default dispatch (128-thread pair CTAs for Q <= 512), forced pair, row kernel
-        monkeypatch.setenv("P2S_AR_ROWS", mode)
+    # default dispatch (128-thread pair CTAs for Q <= 512), forced pair, row kernel
+    for force in (0, FORCE_AR_PAIR_KERNEL, FORCE_AR_ROW_KERNEL):
+        plan = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=3.0, Z=36, K=16, taps=17, ar_alpha=0.95, force=force),
+                    synth.basis(16, 17, seed=1), synth.mlp_weights(16, n_in=33, seed=1))
         z = torch.empty((2 * F + 1, 36, H, W), device="cuda")
         plan.sample_zernike(SEED, 0, F, z[:F])
         plan.sample_zernike(SEED, F, F, z[F:2 * F])
@@ -330,11 +328,10 @@ def test_blur_single_basis_vs_oracle(H, W, K, T, k0):
     assert rel_l2(out.cpu().numpy()[0, 0], ref[0]) <= 1e-2
 
 
-@pytest.mark.parametrize("x_tiles", ["0", "1"])  # 1: force the tile-major MLP input layout
+@pytest.mark.parametrize("force", [0, 0x080])  # 0x080: force the tile-major MLP input layout
 @pytest.mark.parametrize("H,W,C,K,T", [(64, 64, 1, 16, 17), (96, 160, 3, 100, 33), (40, 90, 1, 16, 17)])
-def test_blur_api_vs_oracle(H, W, C, K, T, x_tiles, monkeypatch):
-    monkeypatch.setenv("P2S_X_TILES", x_tiles)
-    plan, basis, mlp, sq, L = make_plan(H, W, C, 3.0, K, T)
+def test_blur_api_vs_oracle(H, W, C, K, T, force):
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 3.0, K, T, force=force)
     a = pipeline.sample_zernike(SEED, 0, 1, sq, L, H, W).astype(np.float32)
     Iw = synth.image(H, W, C, seed=6)[None]
     out = torch.empty((1, C, H, W), device="cuda")
@@ -368,13 +365,13 @@ def test_blur_tap_sizes_vs_oracle(C, T):
 
 
 @pytest.mark.parametrize("C,K,T", [(4, 128, 33), (1, 1, 3), (2, 100, 17), (4, 100, 33), (3, 128, 33), (4, 64, 17)])
-@pytest.mark.parametrize("pair", ["1", "0"])
-def test_blur_extreme_shapes_vs_oracle(C, K, T, pair, monkeypatch):
+@pytest.mark.parametrize("pair", [True, False])
+def test_blur_extreme_shapes_vs_oracle(C, K, T, pair):
     """Edges of the accepted shapes (C = 4, K = 128 = the widest accumulator, K = 1) in both
-    blur modes: CTA pairs (cta_group::2, M = 256) and single CTAs (P2S_BLUR_PAIR=0)."""
-    monkeypatch.setenv("P2S_BLUR_PAIR", pair)
+    blur modes: CTA pairs (cta_group::2, M = 256) and single CTAs (P2S_FORCE_BLUR_SINGLE)."""
+    from paper_2210_06713_b200 import FORCE_BLUR_SINGLE
     H, W = 72, 136
-    plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T)
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T, force=0 if pair else FORCE_BLUR_SINGLE)
     a = pipeline.sample_zernike(SEED, 0, 1, sq, L, H, W).astype(np.float32)
     Iw = synth.image(H, W, C, seed=9)[None]
     out = torch.empty((1, C, H, W), device="cuda")
@@ -431,13 +428,12 @@ def test_oversized_mlp_is_unsupported():
     assert e.value.status == 5  # P2S_ERR_UNSUPPORTED
 
 
-@pytest.mark.parametrize("x_tiles", ["0", "1"])  # 1: force the tile-major MLP input layout
-def test_simulate_ar_sequence_vs_oracle(x_tiles, monkeypatch):
+@pytest.mark.parametrize("force", [0, 0x080])  # 0x080: force the tile-major MLP input layout
+def test_simulate_ar_sequence_vs_oracle(force):
     """Steps 1-5 on an AR(1) sequence (reading Q18): a fresh start and the stored-state
     continuation both follow the oracle's replayed sequence."""
-    monkeypatch.setenv("P2S_X_TILES", x_tiles)
     H, W, C, K, T, alpha = 64, 96, 2, 16, 17, 0.9
-    plan, basis, mlp, sq, L = make_plan(H, W, C, 3.0, K, T, ar_alpha=alpha)
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 3.0, K, T, ar_alpha=alpha, force=force)
     img = synth.image(H, W, C, seed=13)
     out = torch.empty((5, C, H, W), device="cuda")
     plan.simulate_frames(cuda(img), 0, SEED, 0, 3, out[:3])
