@@ -1,27 +1,36 @@
 #!/usr/bin/env python
 """Benchmark of the DF-P2S dense-field simulator (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg3_512]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg3_512] [--extra cfg5_4k] [--dry-run]
 
 One step = one p2s_simulate_frames call over a batch of F frames (all five steps of
 the hot path) on synthetic seeded inputs already resident in HBM.  The
 default workload is BASELINE config 3, the paper's real-time headline: 512x512 RGB,
 F = 64 frames per GPU, D/r0 = 3, Z = 36, K = 100 bases of 33x33 taps, MLP 33-100-100-100.
-Multi-GPU (torchrun, one rank per GPU, NCCL process group for the barrier and the
-max-over-ranks time only): every rank simulates its own disjoint frame range
-(weak scaling, no data-path collective -- frames are independent).
+The metric also names 3840x2160 RGB: the same run measures cfg5_4k (2 frames per GPU
+per step) afterwards and reports it under "workloads" (--extra none skips it).
 
-Prints ONE JSON line on rank 0.  `value` is whole-job frames/s from CUDA events
-(max over ranks); `e2e` is the same metric through p2s_simulate_frames_host with
-pinned host buffers (H2D of the image and D2H of every output frame inside the
-timed region); `stages` and `roofline` come from per-launch CUDA event pairs
-recorded by the library on the launching stream (p2s_plan_stage_timing).
-`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample of the
-same workload on the host cores.
+Multi-GPU: one process per GPU.  Under torchrun the world comes from the environment
+and must equal --gpus; `python bench.py --gpus N` without torchrun re-launches itself
+under torch.distributed.run with N ranks.  The NCCL process group carries only the
+barriers, a communicator check (all_reduce) and the max-over-ranks time: every rank
+simulates its own frames (white noise: a contiguous block of the one sequence per rank;
+AR(1): a whole sequence per rank, so no rank replays), no data-path collective --
+frames are independent ("scaling": "weak").
+
+Prints ONE JSON line on rank 0.  `value` is whole-job frames/s from CUDA events (max
+over ranks); `e2e` is the same metric through p2s_simulate_frames_host with pinned host
+buffers (H2D of the image and D2H of every output frame inside the timed region);
+`stages` and `roofline` come from per-launch CUDA event pairs recorded by the library
+on the launching stream (p2s_plan_stage_timing).
+`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample of the same
+workload on the host cores (rank 0 only).
 """
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -52,9 +61,9 @@ def load_peaks():
 def tensor_peak(peaks, clocks):
     """bf16 dense peak for the roofline.  MEASURED_PEAKS.json has a burst figure (best of 10
     8192^3 matmuls) and a sustained one (4 s back to back, SM clock fell to its under-load
-    median, 1282 MHz on this pool).  A bench step is ~12 ms and the timed region short, so
-    when the SM clock sampled during it is well above that median the burst figure is the
-    comparable one; otherwise the sustained one."""
+    median).  A bench step is ~12 ms and the timed region short, so when the SM clock
+    sampled during it is well above that median the burst figure is the comparable one;
+    otherwise the sustained one."""
     burst = peaks["bf16_tflops"]
     sus = peaks.get("bf16_tflops_sustained")
     if sus is None:
@@ -67,7 +76,7 @@ def tensor_peak(peaks, clocks):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -81,19 +90,21 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.1)
         except Exception:
             self.proc = None
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.1)
         self.proc.terminate()
         self.proc.wait()
         self.f.flush()
         rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        os.unlink(self.f.name)
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
@@ -122,15 +133,21 @@ WORKLOADS = {
                      desc="512x512 RGB, batch of 64 frames/GPU, D/r0=3, Z=36, K=100 bases 33x33, MLP 33-100-100-100"),
     "cfg4_1080p": dict(H=1080, W=1920, C=3, F=8, d_over_r0=4.0, K=100, T=33, ar_alpha=0.0,
                        desc="1920x1080 RGB, 8 frames/GPU per step, D/r0=4, Z=36, K=100 bases 33x33"),
+    # BASELINE.json configs[4]: the metric's 3840x2160 RGB half (the paper's ~60 s/frame case)
     "cfg5_4k": dict(H=2160, W=3840, C=3, F=2, d_over_r0=5.0, K=100, T=33, ar_alpha=0.0,
                     desc="3840x2160 RGB, 2 frames/GPU per step, D/r0=5, Z=36, K=100 bases 33x33"),
     "cfg2_256": dict(H=256, W=256, C=1, F=100, d_over_r0=3.0, K=100, T=33, ar_alpha=0.95,
                      desc="256x256 gray, 100-frame AR(0.95) sequence, D/r0=3, K=100 bases 33x33"),
     # configs 4 and 5 as AR(1) sequences (the BASELINE descriptions' "100-frame sequences")
     "cfg4_1080p_ar": dict(H=1080, W=1920, C=3, F=8, d_over_r0=4.0, K=100, T=33, ar_alpha=0.95,
-                          desc="1920x1080 RGB, AR(0.95) sequence, 8 frames/GPU per step, D/r0=4, K=100 bases 33x33"),
+                          desc="1920x1080 RGB, AR(0.95) sequence per GPU, 8 frames/GPU per step, D/r0=4, K=100 "
+                               "bases 33x33"),
     "cfg5_4k_ar": dict(H=2160, W=3840, C=3, F=2, d_over_r0=5.0, K=100, T=33, ar_alpha=0.95,
-                       desc="3840x2160 RGB, AR(0.95) sequence, 2 frames/GPU per step, D/r0=5, K=100 bases 33x33"),
+                       desc="3840x2160 RGB, AR(0.95) sequence per GPU, 2 frames/GPU per step, D/r0=5, K=100 "
+                            "bases 33x33"),
+    # single-frame 4K latency (SURVEY 8(e) NEXT-4 decision input)
+    "cfg5_4k_f1": dict(H=2160, W=3840, C=3, F=1, d_over_r0=5.0, K=100, T=33, ar_alpha=0.0,
+                       desc="3840x2160 RGB, one frame per call (latency), D/r0=5, K=100 bases 33x33"),
     # NEXT-3: the frozen-flow temporal model on the headline geometry
     "cfg3_512_flow": dict(H=512, W=512, C=3, F=64, d_over_r0=3.0, K=100, T=33, ar_alpha=0.0, flow=(0.5, 0.25),
                           desc="512x512 RGB, 64-frame frozen-flow sequence (0.5, 0.25) px/frame, D/r0=3, K=100"),
@@ -144,7 +161,6 @@ def algorithmic_work(w, Z=36, hidden=(100, 100)):
     PQ = HW  # pad = 1 and every config size is 5-smooth
     npairs = (Z - 1 + 1) // 2
     nslots = Z - 1
-    n3 = (K + 15) // 16 * 16
     nin = Z - 3
     return {
         # sqrt(S) read once per batch + complex row-transformed spectrum written per frame
@@ -160,9 +176,31 @@ def algorithmic_work(w, Z=36, hidden=(100, 100)):
     }
 
 
+# ---------------------------------------------------------------- reference arm (CPU oracle)
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [d.get("num_threads", 1) for d in threadpool_info()]
+        return max(n) if n else 1
+    except Exception:
+        return 1
+
+
 def oracle_sample(w, n_blur_px=2048, seed=SEED, frame=0):
     """Bounded oracle sample: steps 1-3 and 5 on one full frame, step 4 (Eq.9) on
-    n_blur_px pixels scaled to the frame.  Returns (frame seconds, description)."""
+    n_blur_px pixels.  Returns (measured seconds, extrapolated seconds per frame, description)."""
     import synth
     from oracle import optics, pipeline
     H, W, C, K, T, Z = w["H"], w["W"], w["C"], w["K"], w["T"], 36
@@ -174,7 +212,7 @@ def oracle_sample(w, n_blur_px=2048, seed=SEED, frame=0):
     sq = np.ones((Z - 1, H, W))  # timing only: plan tables are off the clock in both arms
     kappa = optics.geometry()[1]
     t0 = time.perf_counter()
-    eta = pipeline.white_spectral_noise(seed, frame, H, W, Z)
+    eta = pipeline.white_spectral_noise(seed, frame, H, W)
     a = pipeline.mix(pipeline.fields_from_noise(eta, sq, H, W), L)
     Iw = pipeline.warp(img, a[1], a[2], kappa)
     wts = pipeline.mlp(a[3:], layers)
@@ -189,77 +227,58 @@ def oracle_sample(w, n_blur_px=2048, seed=SEED, frame=0):
     t3 = time.perf_counter()
     frame_s = (t1 - t0) + (t2 - t1) * (H * W / n_blur_px) + (t3 - t2)
     desc = (f"oracle (fp64 numpy) steps 1-3+5 on one full {H}x{W}x{C} frame, Eq.9 blur on {n_blur_px} "
-            f"random pixels x{H * W // n_blur_px} scaled; sqrt(S) tables not timed")
-    return frame_s, desc
-
-
-def oracle_threads():
-    try:
-        from threadpoolctl import threadpool_info
-        n = [d.get("num_threads", 1) for d in threadpool_info()]
-        return max(n) if n else 1
-    except Exception:
-        return 1
+            f"random pixels, scaled x{H * W / n_blur_px:.0f} to the frame; sqrt(S) tables not timed")
+    return t3 - t0, frame_s, desc
 
 
 def run_reference(args, w, rank, world):
+    """Rank 0 times the oracle; the other ranks exit without work."""
     if rank != 0:
         return
-    times = []
+    measured, per_frame = [], []
     desc = ""
     for i in range(args.warmup + args.steps):
-        s, desc = oracle_sample(w, frame=i)
+        m, s, desc = oracle_sample(w, frame=i)
         if i >= args.warmup:
-            times.append(s)
-    fps = 1.0 / statistics.mean(times)
+            measured.append(m)
+            per_frame.append(s)
+    fps = 1.0 / statistics.mean(per_frame)
+    info = cpu_info()
     cores = oracle_threads()
     line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(measured),
+            "s_per_frame_extrapolated": statistics.mean(per_frame),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_dict(w, args, world),
-            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "data": "synthetic", "config": config_dict(w, args.workload, world),
+            "step_definition": "one bounded oracle sample (ms_per_step is its measured wall time); value = "
+                               "1 / extrapolated seconds per full frame",
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": desc,
+                             **info},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def config_dict(w, args, world):
-    return {"workload": f"{args.workload}: {w['desc']}", "H": w["H"], "W": w["W"], "C": w["C"],
+def config_dict(w, name, world):
+    return {"workload": f"{name}: {w['desc']}", "H": w["H"], "W": w["W"], "C": w["C"],
             "frames_per_gpu_per_step": w["F"], "global_batch": w["F"] * world, "d_over_r0": w["d_over_r0"],
             "Z": 36, "K": w["K"], "T": w["T"], "mlp": f"33-100-100-{w['K']}", "ar_alpha": w["ar_alpha"],
             "step5": "noise sigma={noise_sigma} + clamp01 (normalisation off: random-init weights)".format(**STEP5),
-            "parallelism": f"frames dp{world}", "l2": "no flush: per-step working set "
-            "(spectrum + fields + weights, GBs) far exceeds the 126 MB L2"}
+            "parallelism": f"frames dp{world}",
+            "frames_per_rank": "AR(1): a whole sequence per rank (seed + rank)" if w["ar_alpha"] else
+                               "contiguous block of one sequence per rank",
+            "l2": "no flush: per-step working set (spectrum + fields + weights, GBs) far exceeds the 126 MB L2"}
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg3_512", choices=sorted(WORKLOADS))
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    args = ap.parse_args()
-    w = dict(WORKLOADS[args.workload])
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-
-    if args.impl == "reference":
-        run_reference(args, w, rank, world)
-        return
-
+# ---------------------------------------------------------------- our arm
+def measure(name, args, rank, world, local, peaks):
+    """Device-timed steps, stage times and the e2e leg of one workload; a dict on rank 0."""
     import torch
-    import torch.distributed as dist
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
     import synth
     from paper_2210_06713_b200 import Plan, PlanConfig, runner
 
+    w = dict(WORKLOADS[name])
     H, W, C, F, K, T = w["H"], w["W"], w["C"], w["F"], w["K"], w["T"]
+    ar = w["ar_alpha"] != 0.0
     basis = synth.basis(K, T, seed=0)
     mlp = synth.mlp_weights(K, seed=0)
     img_np = synth.image(H, W, C, seed=0)
@@ -269,16 +288,20 @@ def main():
     img = torch.from_numpy(img_np).to(dev)
     out = torch.empty((F, C, H, W), device=dev)
     stream = torch.cuda.current_stream()
+    # step indices: device warmup [0, W), device timed [W, W+K), e2e warmup W+K, e2e timed after
+    total = args.warmup + 2 * args.steps + 1
 
-    def frame0(step):
-        return runner.step_frame0(step, rank, world, F)
+    def frames(step):
+        soff, f0 = runner.bench_frames(step, rank, F, total, ar)
+        return SEED + soff, f0
 
     def barrier():
         if world > 1:
+            import torch.distributed as dist
             dist.barrier()
 
     for s in range(args.warmup):
-        plan.simulate_frames(img, 0, SEED, frame0(s), F, out)
+        plan.simulate_frames(img, 0, *frames(s), F, out)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -289,7 +312,7 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for s in range(args.steps):
-        plan.simulate_frames(img, 0, SEED, frame0(args.warmup + s), F, out)
+        plan.simulate_frames(img, 0, *frames(args.warmup + s), F, out)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -306,62 +329,177 @@ def main():
     if not args.no_e2e:
         img_h = torch.from_numpy(img_np).pin_memory().numpy()
         out_h = torch.empty((F, C, H, W), dtype=torch.float32).pin_memory().numpy()
-        plan.simulate_frames_host(img_h, 0, SEED, frame0(0), F, out_h)
+        s0 = args.warmup + args.steps
+        plan.simulate_frames_host(img_h, 0, *frames(s0), F, out_h)
         barrier()
         te0 = time.perf_counter()
         for s in range(args.steps):
-            plan.simulate_frames_host(img_h, 0, SEED, frame0(args.warmup + s), F, out_h)
+            plan.simulate_frames_host(img_h, 0, *frames(s0 + 1 + s), F, out_h)
         te = time.perf_counter() - te0
         e2e = {"value": world * F * args.steps / runner.max_over_ranks(te), "unit": "frames/s",
                "h2d_bytes_per_step": int(img_np.nbytes), "d2h_bytes_per_step": int(out_h.nbytes),
                "api": "p2s_simulate_frames_host (pinned host buffers, wall clock, max over ranks)"}
+    del plan, out, img
+    torch.cuda.empty_cache()
+    if rank != 0:
+        return None
+
+    work = algorithmic_work(w)
+    if stages.get("k_warp", (0.0, 0))[1] == 0:
+        # step 2 fused into the 512-point column kernel: its bytes move there (Iw written
+        # and the image read instead of the fp32 tilt planes)
+        kind, amount = work["k_cols"]
+        HW = H * W
+        work["k_cols"] = (kind, amount - F * 2 * HW * 4 + F * C * HW * 2 + C * HW * 4)
+        del work["k_warp"]
+    if stages.get("k_mlp", (0.0, 0))[1] == 0:
+        del work["k_mlp"]  # step 3 fused into the blur kernel: its flops are counted there
+    st = {}
+    for kname, (kind, amount) in work.items():
+        tot_ms, n = stages[kname]
+        per = tot_ms / max(n, 1)
+        if kind == "hbm":
+            ach = amount / (per / 1e3) / 1e9
+            peak = peaks["hbm_gbs"]
+            st[kname] = {"ms_per_launch": per, "launches": n, "bound": "hbm", "bytes_per_launch": amount,
+                         "achieved": ach, "unit": "GB/s", "peak": peak, "frac": ach / peak}
+        else:
+            ach = amount / (per / 1e3) / 1e12
+            peak, _ = tensor_peak(peaks, clocks)
+            st[kname] = {"ms_per_launch": per, "launches": n, "bound": "tensor", "flops_per_launch": amount,
+                         "achieved": ach, "unit": "TFLOP/s", "peak": peak, "frac": ach / peak}
+        st[kname]["share_of_step"] = tot_ms / ms if ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(name, {}).get("k_blur")
+    b = st["k_blur"]
+    roofline = {"kernel": "k_blur (Eq.9 implicit GEMM, tcgen05)", "bound": "tensor", "achieved": b["achieved"],
+                "peak": b["peak"], "unit": "TFLOP/s", "frac": b["frac"], "traffic": traffic,
+                "work": "2*H*W*C*K*T^2 flop/frame (direct Eq.9)",
+                "peak_source": peaks["source"] + " " + tensor_peak(peaks, clocks)[1]}
+    return {"w": w, "value": value, "ms_per_step": ms_max / args.steps, "clocks": clocks, "e2e": e2e,
+            "gpu_launches": int(sum(n for _, n in stages.values())), "roofline": roofline, "stages": st}
+
+
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) without torchrun: run N ranks via torch.distributed.run."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def init_comm(world, local, dry_run):
+    """Process group + a communicator check: all_reduce of ones must give the world size."""
+    import torch
+    import torch.distributed as dist
+    if dry_run:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        t = torch.ones(1, device=torch.device("cuda", local))
+    dist.all_reduce(t)
+    got = int(t.item())
+    backend = dist.get_backend()
+    info = {"backend": backend, "world_size": dist.get_world_size(), "allreduce_ranks": got}
+    if backend == "nccl":
+        info["nccl_version"] = ".".join(str(v) for v in torch.cuda.nccl.version())
+    print(f"[bench] rank {dist.get_rank()}/{world}: {backend} communicator up, all_reduce over {got} ranks",
+          file=sys.stderr, flush=True)
+    if got != world:
+        raise RuntimeError(f"communicator check: all_reduce saw {got} ranks, expected {world}")
+    return info
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3_512", choices=sorted(WORKLOADS))
+    ap.add_argument("--extra", default="cfg5_4k", help="comma-separated extra workloads reported under "
+                    "'workloads' (default: the metric's 3840x2160 RGB half); 'none' for none")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="rank/communicator logic only (gloo, no GPU work)")
+    args = ap.parse_args()
+    w = dict(WORKLOADS[args.workload])
+    in_torchrun = "WORLD_SIZE" in os.environ
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, w, rank, world if in_torchrun else args.gpus)
+        return
+    if args.gpus > 1 and not in_torchrun:
+        sys.exit(relaunch_under_torchrun(args))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+
+    comm = None
+    if world > 1:
+        comm = init_comm(world, local, args.dry_run)
+    if args.dry_run:
+        import torch.distributed as dist
+        from paper_2210_06713_b200 import runner
+        total = args.warmup + 2 * args.steps + 1
+        mine = [runner.bench_frames(s, rank, w["F"], total, w["ar_alpha"] != 0.0) for s in range(total)]
+        if world > 1:
+            allf = [None] * world
+            dist.all_gather_object(allf, mine)
+        else:
+            allf = [mine]
+        if rank == 0:
+            blocks = {(so, f0 + i) for m in allf for so, f0 in m for i in range(w["F"])}
+            print(json.dumps({"metric": METRIC, "dry_run": True, "value": None, "n_gpus": world, "steps": args.steps,
+                              "warmup": args.warmup, "config": config_dict(w, args.workload, world), "comm": comm,
+                              "distinct_frames": len(blocks), "frames_expected": world * total * w["F"]}),
+                  flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    peaks = load_peaks()
+    main_res = measure(args.workload, args, rank, world, local, peaks)
+    extras = {}
+    for name in [x for x in args.extra.split(",") if x and x != "none" and x != args.workload]:
+        r = measure(name, args, rank, world, local, peaks)
+        if rank == 0:
+            extras[name] = {"config": config_dict(r["w"], name, world), "value": r["value"], "unit": "frames/s",
+                            "ms_per_step": r["ms_per_step"], "e2e": r["e2e"], "clocks": r["clocks"],
+                            "gpu_launches": r["gpu_launches"], "roofline": r["roofline"], "stages": r["stages"]}
 
     if rank == 0:
-        peaks = load_peaks()
-        work = algorithmic_work(w)
-        if stages.get("k_warp", (0.0, 0))[1] == 0:
-            # step 2 fused into the 512-point column kernel: its bytes move there (Iw written
-            # and the image read instead of the fp32 tilt planes)
-            kind, amount = work["k_cols"]
-            HW, C, F = w["H"] * w["W"], w["C"], w["F"]
-            work["k_cols"] = (kind, amount - F * 2 * HW * 4 + F * C * HW * 2 + C * HW * 4)
-            del work["k_warp"]
-        st = {}
-        for name, (kind, amount) in work.items():
-            tot_ms, n = stages[name]
-            per = tot_ms / max(n, 1)
-            if kind == "hbm":
-                ach = amount / (per / 1e3) / 1e9
-                peak = peaks["hbm_gbs"]
-                st[name] = {"ms_per_launch": per, "launches": n, "bound": "hbm", "bytes_per_launch": amount,
-                            "achieved": ach, "unit": "GB/s", "peak": peak, "frac": ach / peak}
-            else:
-                ach = amount / (per / 1e3) / 1e12
-                peak, peak_kind = tensor_peak(peaks, clocks)
-                st[name] = {"ms_per_launch": per, "launches": n, "bound": "tensor", "flops_per_launch": amount,
-                            "achieved": ach, "unit": "TFLOP/s", "peak": peak, "frac": ach / peak}
-            st[name]["share_of_step"] = tot_ms / ms if ms > 0 else None
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(args.workload, {}).get("k_blur")
-        b = st["k_blur"]
-        roofline = {"kernel": "k_blur (Eq.9 implicit GEMM, tcgen05)", "bound": "tensor", "achieved": b["achieved"],
-                    "peak": b["peak"], "unit": "TFLOP/s", "frac": b["frac"], "traffic": traffic,
-                    "work": "2*H*W*C*K*T^2 flop/frame (direct Eq.9)",
-                    "peak_source": peaks["source"] + " " + tensor_peak(peaks, clocks)[1]}
-        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        r = main_res
+        line = {"metric": METRIC, "value": r["value"], "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32 field / bf16 tensor (f32 acc)",
-                "data": "synthetic", "config": config_dict(w, args, world), "clocks": clocks,
-                "e2e": e2e, "gpu_launches": int(sum(n for _, n in stages.values())), "roofline": roofline,
-                "stages": st}
+                "data": "synthetic", "config": config_dict(w, args.workload, world), "clocks": r["clocks"],
+                "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "roofline": r["roofline"],
+                "stages": r["stages"]}
+        if comm:
+            line["comm"] = comm
+        if extras:
+            line["workloads"] = extras
         if world == 1 and not args.no_cpu_baseline:
-            s, desc = oracle_sample(w)
+            m, s, desc = oracle_sample(w)
             line["cpu_baseline"] = {"value": 1.0 / s, "unit": "frames/s", "cores": oracle_threads(),
-                                    "kind": "oracle", "sample": desc}
+                                    "kind": "oracle", "sample": desc, "s_per_frame_extrapolated": s,
+                                    **cpu_info()}
         print(json.dumps(line), flush=True)
     if world > 1:
+        import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
 

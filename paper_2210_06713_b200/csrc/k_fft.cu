@@ -704,9 +704,11 @@ __global__ void __launch_bounds__(NT) k_rows_ar(RowArgs a) {
 // Philox once per bin pair and feeds the mirror row with the conjugate.  Half the draws and
 // half the state traffic of k_rows_ar; the same values up to the FFT's rounding order.
 // It pays where the rows are long (Q > 1024: 4K AR rows 5.48 -> 3.84 ms, 1080p 3.89 -> 3.56
-// per launch); at Q = 256 (cfg2) the one-CTA-per-row kernel's twice-as-large grid wins
-// (1.57 vs 1.83 ms: 100 sequential frames per CTA), so short rows keep k_rows_ar.
-// 128 registers, no spills (an 80-register cap spills and is slower at 1080p).
+// per launch).  Rows of up to 512 points run it with 128-thread CTAs (MB = 4 bins per
+// thread): at Q = 256 (cfg2, 100 sequential frames per CTA) that beats both k_rows_ar
+// (1.38 vs 1.57 ms) and 256-thread pair CTAs (1.84 ms, half the CTAs); 512 < Q <= 1024
+// keeps k_rows_ar (rows_variant).  128 registers, no spills (an 80-register cap spills and
+// is slower at 1080p).
 template <int NT, int MB>
 __global__ void __launch_bounds__(NT) k_rows_ar_pair(RowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];

@@ -138,7 +138,9 @@ struct p2s_plan_s {
   void* d_ws = nullptr;
   size_t ws_bytes = 0;
   float2* d_Z = nullptr;        // [mb][npairs][P][Q]
-  uint16_t* d_X = nullptr;      // bf16 [mb][nslots][H*W] (simulate) / [mb][Z-3][H*W] (blur API)
+  uint16_t* d_X = nullptr;      // bf16 MLP inputs, nin = nslots (simulate) or Z-3 (blur API) values per
+                                // pixel: planes [mb][nin][H*W], or (xtile) tile-major
+                                // [mb][H][ntx][nin][128 px] (x_index in p2s_dev.cuh)
   float* d_tilt = nullptr;      // [mb][2][H*W]
   uint16_t* d_Iw = nullptr;     // bf16 [mb][C][H][W]
   uint16_t* d_w = nullptr;      // bf16 [mb][H][ntx][n3/8][128 px][8]: per 128-pixel row tile, 8-basis chunks

@@ -26,6 +26,21 @@ def step_frame0(step: int, rank: int, world: int, frames_per_rank: int) -> int:
     return (step * world + rank) * frames_per_rank
 
 
+def bench_frames(step: int, rank: int, frames_per_step: int, total_steps: int, ar: bool):
+    """(seed offset, first frame) of `rank` in benchmark step `step` of `total_steps`.
+
+    White-noise frames are independent: rank r owns the contiguous global block
+    [r * total_steps * F, (r + 1) * total_steps * F) of the one sequence, step by step.
+    AR(1) workloads give every rank a whole sequence of its own (seed + r, frames 0, F,
+    2F, ... in step order), so each call continues from the stored AR state and no rank
+    ever replays frames (whole sequences per rank when there are >= G)."""
+    if not (0 <= step < total_steps) or rank < 0 or frames_per_step < 1:
+        raise ValueError("bad bench step arguments")
+    if ar:
+        return rank, step * frames_per_step
+    return 0, (rank * total_steps + step) * frames_per_step
+
+
 def sequence_assignment(n_sequences: int, world: int, rank: int):
     """Whole sequences per rank when there are at least as many sequences as ranks."""
     return list(range(rank, n_sequences, world))

@@ -74,3 +74,44 @@ def test_partition_edge_cases():
     assert [runner.frame_partition(7, 3, r) for r in range(3)] == [(0, 3), (3, 2), (5, 2)]
     with pytest.raises(ValueError):
         runner.frame_partition(5, 2, 2)
+
+
+def test_bench_frames_disjoint_and_ar_sequences_continue():
+    total, F = 7, 4
+    for world in (1, 2, 8):
+        seen = set()
+        for r in range(world):
+            prev = None
+            for s in range(total):
+                so, f0 = runner.bench_frames(s, r, F, total, False)
+                assert so == 0
+                if prev is not None:
+                    assert f0 == prev + F  # contiguous per rank
+                prev = f0
+                seen.update(range(f0, f0 + F))
+        assert seen == set(range(world * total * F))
+    for r in range(3):  # AR: a sequence per rank, frames 0, F, 2F, ... (never a replay)
+        assert [runner.bench_frames(s, r, F, total, True) for s in range(total)] == [(r, s * F) for s in range(total)]
+
+
+@pytest.mark.parametrize("workload", ["cfg3_512", "cfg4_1080p_ar"])
+def test_bench_gpus2_dry_run_launches_two_ranks(workload):
+    """`bench.py --gpus 2` without torchrun re-launches itself with two ranks (gloo in the
+    dry run): both ranks join the communicator and the frame blocks of all steps are
+    distinct."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "2",
+                        "--warmup", "1", "--workload", workload], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"]
+    assert d["comm"]["world_size"] == 2 and d["comm"]["allreduce_ranks"] == 2
+    assert d["distinct_frames"] == d["frames_expected"]
