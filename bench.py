@@ -283,7 +283,8 @@ def measure(name, args, rank, world, local, peaks):
     mlp = synth.mlp_weights(K, seed=0)
     img_np = synth.image(H, W, C, seed=0)
     plan = Plan(PlanConfig(H=H, W=W, C=C, d_over_r0=w["d_over_r0"], K=K, taps=T, ar_alpha=w["ar_alpha"],
-                           max_batch=F, device=local, flow=w.get("flow", (0.0, 0.0)), **STEP5), basis, mlp)
+                           max_batch=F, device=local, flow=w.get("flow", (0.0, 0.0)), force=args.force, **STEP5),
+                basis, mlp)
     dev = torch.device("cuda", local)
     img = torch.from_numpy(img_np).to(dev)
     out = torch.empty((F, C, H, W), device=dev)
@@ -429,6 +430,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="rank/communicator logic only (gloo, no GPU work)")
+    ap.add_argument("--force", type=lambda v: int(v, 0), default=0,
+                    help="p2s_options.force bits (kernel-variant A/B runs; 0 = production dispatch)")
     args = ap.parse_args()
     w = dict(WORKLOADS[args.workload])
     in_torchrun = "WORLD_SIZE" in os.environ
@@ -490,6 +493,8 @@ def main():
                 "stages": r["stages"]}
         if comm:
             line["comm"] = comm
+        if args.force:
+            line["force"] = hex(args.force)
         if extras:
             line["workloads"] = extras
         if world == 1 and not args.no_cpu_baseline:

@@ -320,6 +320,72 @@ __device__ __forceinline__ void smem_ifft_inplace(float2* x, const FFTPlanSmem* 
   }
 }
 
+// Compile-time three-pass plans (N = R1 R2 R3) for the long axes of the BASELINE grids
+// (1080 = 12 x 10 x 9, 2160 = 16 x 15 x 9): the same Stockham passes as smem_ifft_inplace,
+// with constant radices and spans (index division by the span is a multiply-shift) and
+// per-pass twiddle tables laid out [r-1][k], so the butterflies of consecutive threads read
+// consecutive entries (the shared e^{2 pi i m / N} table is read at stride r k N/(Ns R) by
+// consecutive k, which conflicts on the banks).
+template <int N, int R1, int R2, int R3>
+struct Plan3 {
+  static_assert(R1 * R2 * R3 == N, "three-pass plan");
+  static constexpr int tw2 = (R2 - 1) * R1;       // pass 2: span Ns = R1
+  static constexpr int tw3 = (R3 - 1) * R1 * R2;  // pass 3: span Ns = R1 R2
+  static constexpr int ntw = tw2 + tw3;
+};
+template <int N, int R1, int R2, int R3>
+__device__ __forceinline__ void build_twp3(float2* __restrict__ twp, const float2* __restrict__ tw) {
+  using PL = Plan3<N, R1, R2, R3>;
+  for (int i = threadIdx.x; i < PL::ntw; i += blockDim.x) {
+    int m;
+    if (i < PL::tw2) {
+      const int r = 1 + i / R1, k = i % R1;
+      m = r * k * (N / (R1 * R2));
+    } else {
+      const int o = i - PL::tw2, r = 1 + o / (R1 * R2), k = o % (R1 * R2);
+      m = r * k;
+    }
+    twp[i] = __ldg(&tw[m]);
+  }
+}
+template <int R, int NS, int N, int NT, int TCL>
+__device__ __forceinline__ void ifft_pass_ip_ct(float2* __restrict__ x, const float2* __restrict__ twp) {
+  constexpr int NR = N / R, TC = 1 << TCL, total = NR * TC;
+  constexpr int NB = (total + NT - 1) / NT;  // butterflies per thread (all loaded before any store)
+  float2 v[NB][R];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int w = threadIdx.x + b * NT;
+    const int c = w & (TC - 1), j = w < total ? w >> TCL : 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b][r] = x[pidx(((j + r * NR) << TCL) + c)];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int w = threadIdx.x + b * NT;
+    const int c = w & (TC - 1), j = w < total ? w >> TCL : 0;
+    const int k = j % NS, q = j / NS;
+    if (NS > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], twp[(r - 1) * NS + k]);
+    }
+    dft_inv<R>(v[b]);
+    if (w < total) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[pidx(((q * NS * R + k + r * NS) << TCL) + c)] = v[b][r];
+    }
+  }
+  __syncthreads();
+}
+template <int N, int R1, int R2, int R3, int NT, int TCL>
+__device__ __forceinline__ void smem_ifft3_inplace(float2* x, const float2* twp) {
+  using PL = Plan3<N, R1, R2, R3>;
+  ifft_pass_ip_ct<R1, 1, N, NT, TCL>(x, twp);
+  ifft_pass_ip_ct<R2, R1, N, NT, TCL>(x, twp);
+  ifft_pass_ip_ct<R3, R1 * R2, N, NT, TCL>(x, twp + PL::tw2);
+}
+
 static void fill_fft_args(FFTArgs& a, const AxisFFT& ax) {
   a.N = ax.N;
   a.nrad = ax.nrad;
@@ -506,14 +572,18 @@ __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
 // ((Q/R)*2 <= NT): one exchange buffer and the sqrt(S) rows read straight from global memory
 // (once per frame and bin) halve the shared memory (4K: 222 -> 95 KB), so two CTAs share
 // an SM and one's Philox/butterfly work overlaps the other's barriers and stores.
-template <int NT, bool ETA = false>
+// QN > 0: the compile-time plan QN = R1 R2 R3 (smem_ifft3_inplace, per-pass twiddles).
+template <int NT, bool ETA = false, int QN = 0, int R1 = 1, int R2 = 1, int R3 = 1>
 __global__ void __launch_bounds__(NT, 2) k_rows_pair_ip(RowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int Q = a.Q;
   float2* twq = reinterpret_cast<float2*>(smem);  // [Q] twiddles
   float2* X = twq + Q;                             // [Q][2] interleaved rows (padded)
   __shared__ FFTPlanSmem fpl;
-  stage_fft_plan(&fpl, a.fq, twq);
+  if constexpr (QN > 0)
+    build_twp3<QN, R1, R2, R3>(twq, a.fq.tw);
+  else
+    stage_fft_plan(&fpl, a.fq, twq);
   const int ky = blockIdx.x, p = blockIdx.y;
   const int k1 = ky ? a.P - ky : 0;
   const size_t plane = (size_t)p * a.P * Q;
@@ -551,7 +621,10 @@ __global__ void __launch_bounds__(NT, 2) k_rows_pair_ip(RowArgs a) {
       X[pidx(2 * km + 1)] = y1;
     }
     __syncthreads();
-    smem_ifft_inplace<NT>(X, &fpl, 1);
+    if constexpr (QN > 0)
+      smem_ifft3_inplace<QN, R1, R2, R3, NT, 1>(X, twq);
+    else
+      smem_ifft_inplace<NT>(X, &fpl, 1);
     const float2* R = X;
     float2* dst = a.Zout + (size_t)t * a.npairs * a.P * Q + plane;
     for (int x = threadIdx.x; x < Q; x += NT) {
@@ -801,6 +874,8 @@ enum RowVariant {
   RV_AR_ROW_128, RV_AR_ROW_512,  // k_rows_ar<NT>: one CTA per spectral row
   RV_REG512,        // k_rows_pair512<4>
   RV_PAIR_IP_512,   // k_rows_pair_ip<512>: in place, long rows
+  RV_PAIR_IP_3840,  // k_rows_pair_ip<512, false, 3840, 16, 16, 15>: compile-time plan
+  RV_PAIR_IP_1920,  // k_rows_pair_ip<512, false, 1920, 16, 15, 8>
   RV_PAIR_256, RV_PAIR_512  // k_rows_pair<NT>: ping-pong
 };
 
@@ -848,6 +923,19 @@ static RowVariant rows_variant(const p2s_plan_s* pl, bool ar, bool given, size_t
   // in place only where the ping-pong kernel fits one CTA per SM (4K: 222 KB; at 1920
   // points it already fits two, and the in-place variant measured slower there: 2.94 vs
   // 2.50 ms), or does not fit at all (4096 = 16 x 16 x 16)
+  // compile-time in-place plans for the BASELINE row lengths (per-pass twiddles, constant
+  // index arithmetic): two CTAs per SM at both
+  const auto& rq = pl->fq;
+  if (!(pl->force & (P2S_FORCE_ROWS_PINGPONG | P2S_FORCE_FFT_GENERIC)) && rq.nrad == 3) {
+    if (Q == 3840 && rq.rad[0] == 16 && rq.rad[1] == 16 && rq.rad[2] == 15) {
+      *sm = smem_pair_ip(Q);
+      return RV_PAIR_IP_3840;
+    }
+    if (Q == 1920 && rq.rad[0] == 16 && rq.rad[1] == 15 && rq.rad[2] == 8) {
+      *sm = smem_pair_ip(Q);
+      return RV_PAIR_IP_1920;
+    }
+  }
   if (Q > 1024 && 2 * smem_pair(Q) > kSmemMax && one && !(pl->force & P2S_FORCE_ROWS_PINGPONG)) {
     *sm = smem_pair_ip(Q);
     return RV_PAIR_IP_512;
@@ -924,6 +1012,14 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
     case RV_PAIR_IP_512:
       P2S_SMEM_OPTIN(k_rows_pair_ip<512>, sm);
       k_rows_pair_ip<512><<<gpair, 512, sm, s>>>(a);
+      break;
+    case RV_PAIR_IP_3840:
+      P2S_SMEM_OPTIN((k_rows_pair_ip<512, false, 3840, 16, 16, 15>), sm);
+      k_rows_pair_ip<512, false, 3840, 16, 16, 15><<<gpair, 512, sm, s>>>(a);
+      break;
+    case RV_PAIR_IP_1920:
+      P2S_SMEM_OPTIN((k_rows_pair_ip<512, false, 1920, 16, 15, 8>), sm);
+      k_rows_pair_ip<512, false, 1920, 16, 15, 8><<<gpair, 512, sm, s>>>(a);
       break;
     case RV_PAIR_512:
       P2S_SMEM_OPTIN((k_rows_pair<512>), sm);
@@ -1051,6 +1147,154 @@ __device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc, uint32_t
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Long columns (1080p / 4K), in place, two CTAs per SM: one CTA per (block of TC = 2^TCL
+// columns, mode pair, frame), one shared buffer transformed in place (every pass has at
+// most one butterfly per thread, (P / R) TC <= NT), twiddles staged in shared memory.  The
+// second resident CTA's loads and stores overlap this one's barrier-separated passes (the
+// persistent single-CTA kernel below serialises them: its transform phase is
+// barrier-bound).  Each thread then writes the TC adjacent columns of a row with one
+// vector store per output plane (TC bf16 = 4 or 8 bytes, TC fp32 tilt / zern values).
+// PN > 0: the compile-time plan PN = R1 R2 R3 (smem_ifft3_inplace), else the runtime plan.
+template <int MODE, int NT, int TCL, int PN = 0, int R1 = 1, int R2 = 1, int R3 = 1>
+__global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_cols_ip(ColArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int TC = 1 << TCL;
+  float2* twp = reinterpret_cast<float2*>(smem);
+  float2* X = twp + a.P;
+  __shared__ FFTPlanSmem fpl;
+  if constexpr (PN > 0)
+    build_twp3<PN, R1, R2, R3>(twp, a.fp.tw);
+  else
+    stage_fft_plan(&fpl, a.fp, twp);
+  const int x0 = blockIdx.x * TC, p = blockIdx.y, f = blockIdx.z;
+  const float2* src = a.Zin + ((size_t)f * a.npairs + p) * a.P * a.Q + x0;
+  const bool full = x0 + TC <= a.Q && (a.Q & 1) == 0;  // 16-byte loads need an even row length
+  // loads: row ky of the block is TC consecutive float2 (16 or 32 bytes)
+  constexpr int U = 4;
+  for (int r0 = threadIdx.x; r0 < a.P * (TC / 2); r0 += NT * U) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = r0 + u * NT;
+      const int ky = r / (TC / 2), h = r % (TC / 2);
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < a.P * (TC / 2)) {
+        if (full) {
+          v[u] = __ldg(reinterpret_cast<const float4*>(src + (size_t)ky * a.Q) + h);
+        } else {
+          if (x0 + 2 * h < a.Q) {
+            const float2 e = __ldg(src + (size_t)ky * a.Q + 2 * h);
+            v[u].x = e.x;
+            v[u].y = e.y;
+          }
+          if (x0 + 2 * h + 1 < a.Q) {
+            const float2 e = __ldg(src + (size_t)ky * a.Q + 2 * h + 1);
+            v[u].z = e.x;
+            v[u].w = e.y;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = r0 + u * NT;
+      if (r < a.P * (TC / 2)) {
+        const int w = 2 * r;  // element index (ky << TCL) + 2 h
+        X[pidx(w)] = make_float2(v[u].x, v[u].y);
+        X[pidx(w + 1)] = make_float2(v[u].z, v[u].w);
+      }
+    }
+  }
+  __syncthreads();
+  if constexpr (PN > 0)
+    smem_ifft3_inplace<PN, R1, R2, R3, NT, TCL>(X, twp);
+  else
+    smem_ifft_inplace<NT>(X, &fpl, TCL);
+  const int sa = 2 * p, sb = 2 * p + 1;
+  const size_t HW = (size_t)a.H * a.W;
+  const bool vec = (a.W % TC == 0) && x0 + TC <= a.W;
+  for (int yy = threadIdx.x; yy < a.H; yy += NT) {
+    float2 v[TC];
+#pragma unroll
+    for (int c = 0; c < TC; ++c) v[c] = X[pidx((yy << TCL) + c)];
+    const size_t pix = (size_t)yy * a.W + x0;
+    if (MODE == 0) {
+      float* za = a.zern + ((size_t)f * a.Z + sa + 1) * HW + pix;
+      float* zb = a.zern + ((size_t)f * a.Z + sb + 1) * HW + pix;
+      const bool hb = sb < a.nslots;
+      if (vec) {
+        if (TC == 2) {
+          *reinterpret_cast<float2*>(za) = make_float2(v[0].x, v[1].x);
+          if (hb) *reinterpret_cast<float2*>(zb) = make_float2(v[0].y, v[1].y);
+        } else {
+#pragma unroll
+          for (int c = 0; c < TC; c += 4) {
+            *reinterpret_cast<float4*>(za + c) = make_float4(v[c].x, v[c + 1].x, v[c + 2].x, v[c + 3].x);
+            if (hb) *reinterpret_cast<float4*>(zb + c) = make_float4(v[c].y, v[c + 1].y, v[c + 2].y, v[c + 3].y);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < TC; ++c)
+          if (x0 + c < a.W) {
+            za[c] = v[c].x;
+            if (hb) zb[c] = v[c].y;
+          }
+      }
+    } else {
+      uint16_t* Xa = a.X + x_index(a.xtile, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x0);
+      // the second mode of the pair: the next plane (planes) or the next 128-pixel row of the tile
+      const size_t db = a.xtile ? 128 : HW;
+      const bool hb = sb < a.nslots;
+      if (vec) {
+        uint32_t ua[TC / 2], ub[TC / 2];
+#pragma unroll
+        for (int c = 0; c < TC; c += 2) {
+          ua[c / 2] = pack_bf16x2(v[c].x, v[c + 1].x);
+          ub[c / 2] = pack_bf16x2(v[c].y, v[c + 1].y);
+        }
+        if (TC == 2) {
+          *reinterpret_cast<uint32_t*>(Xa) = ua[0];
+          if (hb) *reinterpret_cast<uint32_t*>(Xa + db) = ub[0];
+        } else {
+#pragma unroll
+          for (int c = 0; c < TC; c += 4) {
+            *reinterpret_cast<uint2*>(Xa + c) = make_uint2(ua[c / 2], ua[c / 2 + 1]);
+            if (hb) *reinterpret_cast<uint2*>(Xa + db + c) = make_uint2(ub[c / 2], ub[c / 2 + 1]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < TC; ++c)
+          if (x0 + c < a.W) {
+            Xa[c] = f_to_bf16(v[c].x);
+            if (hb) Xa[db + c] = f_to_bf16(v[c].y);
+          }
+      }
+      if (p == 0) {
+        float* t = a.tilt + (size_t)f * 2 * HW + pix;
+        if (vec && TC == 2) {
+          *reinterpret_cast<float2*>(t) = make_float2(v[0].x, v[1].x);
+          *reinterpret_cast<float2*>(t + HW) = make_float2(v[0].y, v[1].y);
+        } else if (vec) {
+#pragma unroll
+          for (int c = 0; c < TC; c += 4) {
+            *reinterpret_cast<float4*>(t + c) = make_float4(v[c].x, v[c + 1].x, v[c + 2].x, v[c + 3].x);
+            *reinterpret_cast<float4*>(t + HW + c) = make_float4(v[c].y, v[c + 1].y, v[c + 2].y, v[c + 3].y);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < TC; ++c)
+            if (x0 + c < a.W) {
+              t[c] = v[c].x;
+              t[HW + c] = v[c].y;
+            }
+        }
+      }
+    }
+  }
+}
 
 // Long columns (1080p / 4K), persistent: one CTA per SM walks the column blocks; the next
 // block's loads (cp.async, zero-filled past Q) land in the second buffer while the current
@@ -1285,6 +1529,57 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
       k_cols512<1><<<grid, 512, sm, s>>>(a);
     }
     return (int)cudaGetLastError();
+  }
+  // Long columns whose plan has at most 512 / TC butterflies per pass: the in-place
+  // two-CTAs-per-SM kernel with the widest block that fits (TC = 4 at 1080 = 12 x 10 x 9,
+  // TC = 2 at 2160 = 16 x 15 x 9).
+  if (pl->P > 512 && !(pl->force & (P2S_FORCE_COLS_PER_BLOCK | P2S_FORCE_COLS_PERSISTENT))) {
+    const auto& rp = pl->fp;
+    const bool ct = !(pl->force & P2S_FORCE_FFT_GENERIC) && rp.nrad == 3;
+#define P2S_COLS_CT(NT_, TL_, ...)                                                       \
+  do {                                                                                   \
+    a.tc_log2 = TL_;                                                                     \
+    const size_t sm = ((size_t)pl->P + padded_len((size_t)pl->P << TL_)) * sizeof(float2); \
+    dim3 grid((pl->W + (1 << TL_) - 1) >> TL_, pl->npairs, F);                           \
+    if (mode == 0) {                                                                     \
+      P2S_SMEM_OPTIN((k_cols_ip<0, NT_, TL_, __VA_ARGS__>), sm);                         \
+      k_cols_ip<0, NT_, TL_, __VA_ARGS__><<<grid, NT_, sm, s>>>(a);                      \
+    } else {                                                                             \
+      P2S_SMEM_OPTIN((k_cols_ip<1, NT_, TL_, __VA_ARGS__>), sm);                         \
+      k_cols_ip<1, NT_, TL_, __VA_ARGS__><<<grid, NT_, sm, s>>>(a);                      \
+    }                                                                                    \
+    return (int)cudaGetLastError();                                                      \
+  } while (0)
+    // measured (cfg5 / cfg4, per launch): 2160 with 4 columns and 384 threads, two CTAs per
+    // SM (up to 3 butterflies per thread): 2.58 ms per 2 frames (8 columns, 768 threads, one
+    // CTA: 2.66; 2 columns, 512 threads: 3.86; the persistent k_cols_p: 3.81); 1080 with 8
+    // columns and 512 threads: 2.28 ms per 8 frames (4 columns: 2.57; k_cols_p: 2.73).  The
+    // stores set the pace: TC columns of a row are TC * 2 bytes per output plane.
+    if (ct && pl->P == 2160 && rp.rad[0] == 16 && rp.rad[1] == 15 && rp.rad[2] == 9)
+      P2S_COLS_CT(384, 2, 2160, 16, 15, 9);
+    if (ct && pl->P == 1080 && rp.rad[0] == 12 && rp.rad[1] == 10 && rp.rad[2] == 9)
+      P2S_COLS_CT(512, 3, 1080, 12, 10, 9);
+#undef P2S_COLS_CT
+    for (int tl = 2; tl >= 1; --tl) {
+      bool one = true;
+      for (int i = 0; i < pl->fp.nrad; ++i) one = one && ((pl->P / pl->fp.rad[i]) << tl) <= 512;
+      const size_t sm = ((size_t)pl->P + padded_len((size_t)pl->P << tl)) * sizeof(float2);
+      if (!one || 2 * (sm + 1024) > kSmemMax) continue;
+      a.tc_log2 = tl;
+      dim3 grid((pl->W + (1 << tl) - 1) >> tl, pl->npairs, F);
+#define P2S_COLS_IP(...)                                \
+  do {                                                  \
+    P2S_SMEM_OPTIN((k_cols_ip<__VA_ARGS__>), sm);       \
+    k_cols_ip<__VA_ARGS__><<<grid, 512, sm, s>>>(a);    \
+  } while (0)
+      if (mode == 0) {
+        if (tl == 2) P2S_COLS_IP(0, 512, 2); else P2S_COLS_IP(0, 512, 1);
+      } else {
+        if (tl == 2) P2S_COLS_IP(1, 512, 2); else P2S_COLS_IP(1, 512, 1);
+      }
+#undef P2S_COLS_IP
+      return (int)cudaGetLastError();
+    }
   }
   // Long columns: 1024 threads and up to 8640 elements per CTA double the columns per CTA
   // where that is still below 16 (1080 points: 8 columns, 64-byte row segments, 3.26 ->

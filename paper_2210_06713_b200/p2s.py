@@ -52,6 +52,7 @@ FORCE_X_PLANES = 0x040
 FORCE_X_TILES = 0x080
 FORCE_NO_WARP_FUSION = 0x100
 FORCE_BLUR_SINGLE = 0x200
+FORCE_COLS_PERSISTENT = 0x400
 
 
 def _load():

@@ -1,0 +1,93 @@
+"""Out-of-bounds and race screening without compute-sanitizer (closed on this GPU pool).
+
+Every kernel variant of tools/sanitize_cases.py runs with its caller-visible outputs
+placed inside guard bands (1 MB of a NaN sentinel pattern on both sides): any store
+outside [out, out + size) changes a guard.  Every case also runs twice on fresh
+buffers: a shared-memory / TMEM / mbarrier race shows up as non-deterministic output,
+so both runs must be bit-identical.
+"""
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+SEED = 2210
+GUARD = 1 << 18  # floats per side
+SENTINEL = 0x7FC0DEAD  # a quiet NaN no kernel writes
+
+
+def guarded(shape):
+    n = int(np.prod(shape))
+    buf = torch.full((n + 2 * GUARD,), SENTINEL, dtype=torch.int32, device="cuda")
+    return buf, buf[GUARD:GUARD + n].view(torch.float32).view(*shape)
+
+
+def guards_intact(buf):
+    g = torch.cat([buf[:GUARD], buf[-GUARD:]])
+    return bool((g == SENTINEL).all())
+
+
+CASES = [
+    # (H, W, C, K, T, plan kwargs, F)
+    (64, 96, 2, 16, 17, {}, 2),                           # generic FFTs, CTA-pair blur
+    (512, 64, 3, 100, 33, {}, 1),                         # 512-point columns, fused warp
+    (48, 512, 1, 16, 17, {}, 2),                          # 512-point register rows
+    (64, 160, 3, 16, 17, {"force": 0x080}, 2),            # tile-major MLP inputs
+    (1000, 40, 1, 16, 17, {}, 1),                         # persistent in-place columns
+    (20, 2400, 1, 16, 17, {}, 1),                         # in-place long rows
+    (20, 2400, 1, 16, 17, {"ar_alpha": 0.9}, 2),          # AR row pairs, long rows
+    (45, 75, 1, 16, 17, {"ar_alpha": 0.9, "force": 0x004}, 2),  # AR row kernel, odd grid
+    (72, 136, 4, 128, 33, {"force": 0x200}, 1),           # single-CTA blur, widest K
+    (64, 64, 1, 16, 15, {}, 1),                           # padded tap group
+    (40, 48, 1, 1, 3, {}, 2),                             # smallest shapes
+]
+
+
+def run_case(H, W, C, K, T, kw, F):
+    from paper_2210_06713_b200 import Plan, PlanConfig
+    plan = Plan(PlanConfig(H=H, W=W, C=C, d_over_r0=2.0, K=K, taps=T, **kw), synth.basis(K, T, seed=1),
+                synth.mlp_weights(K, seed=1))
+    img = torch.from_numpy(synth.image(H, W, C, seed=0)).cuda()
+    res = []
+    bufs = []
+    bz, z = guarded((F, 36, H, W))
+    plan.sample_zernike(SEED, 0, F, z)
+    bo, out = guarded((F, C, H, W))
+    plan.simulate_frames(img, 0, SEED, 0, F, out)
+    bw, warped = guarded((F, C, H, W))
+    plan.warp(img, 0, z, warped, F)
+    bb, blurred = guarded((F, C, H, W))
+    plan.blur(warped, z, SEED, 0, blurred, F)
+    torch.cuda.synchronize()
+    for b, t in ((bz, z), (bo, out), (bw, warped), (bb, blurred)):
+        bufs.append(b)
+        res.append(t.clone())
+    return bufs, res
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_outputs_stay_inside_their_buffers_and_are_deterministic(case):
+    H, W, C, K, T, kw, F = CASES[case]
+    bufs1, r1 = run_case(H, W, C, K, T, kw, F)
+    bufs2, r2 = run_case(H, W, C, K, T, kw, F)
+    for b in bufs1 + bufs2:
+        assert guards_intact(b)
+    for a, b in zip(r1, r2):
+        assert torch.isfinite(a).all()
+        assert torch.equal(a, b)
+
+
+def test_host_entry_stays_inside_its_buffer():
+    from paper_2210_06713_b200 import Plan, PlanConfig
+    H, W, C, F = 64, 96, 3, 5
+    plan = Plan(PlanConfig(H=H, W=W, C=C, d_over_r0=2.0, K=16, taps=17, max_batch=2), synth.basis(16, 17, seed=1),
+                synth.mlp_weights(16, seed=1))
+    img = torch.from_numpy(synth.image(H, W, C, seed=0)).pin_memory().numpy()
+    n = F * C * H * W
+    host = torch.full((n + 2 * GUARD,), SENTINEL, dtype=torch.int32).pin_memory().numpy()
+    out = host[GUARD:GUARD + n].view(np.float32)
+    plan.simulate_frames_host(img, 0, SEED, 0, F, out)
+    assert np.all(host[:GUARD] == SENTINEL) and np.all(host[-GUARD:] == SENTINEL)
+    assert np.all(np.isfinite(out))
