@@ -782,7 +782,8 @@ __global__ void __launch_bounds__(NT) k_rows_ar(RowArgs a) {
 // (1.38 vs 1.57 ms) and 256-thread pair CTAs (1.84 ms, half the CTAs); 512 < Q <= 1024
 // keeps k_rows_ar (rows_variant).  128 registers, no spills (an 80-register cap spills and
 // is slower at 1080p).
-template <int NT, int MB>
+// QN > 0: compile-time in-place plan QN = R1 R2 R3 (one exchange buffer, per-pass twiddles).
+template <int NT, int MB, int QN = 0, int R1 = 1, int R2 = 1, int R3 = 1>
 __global__ void __launch_bounds__(NT) k_rows_ar_pair(RowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int Q = a.Q;
@@ -791,7 +792,10 @@ __global__ void __launch_bounds__(NT) k_rows_ar_pair(RowArgs a) {
   float2* X = sS + 2 * Q;                          // [Q][2] interleaved rows (padded)
   float2* Xb = X + padded_len(2 * Q);
   __shared__ FFTPlanSmem fpl;
-  stage_fft_plan(&fpl, a.fq, twq);
+  if constexpr (QN > 0)
+    build_twp3<QN, R1, R2, R3>(twq, a.fq.tw);
+  else
+    stage_fft_plan(&fpl, a.fq, twq);
   const int ky = blockIdx.x, p = blockIdx.y;
   const int k1 = ky ? a.P - ky : 0;
   const size_t plane = (size_t)p * a.P * Q;
@@ -830,7 +834,13 @@ __global__ void __launch_bounds__(NT) k_rows_ar_pair(RowArgs a) {
     }
     if (!out) continue;  // replay: state only
     __syncthreads();
-    const float2* R = smem_ifft<NT>(X, Xb, &fpl, 1);
+    const float2* R;
+    if constexpr (QN > 0) {
+      smem_ifft3_inplace<QN, R1, R2, R3, NT, 1>(X, twq);
+      R = X;
+    } else {
+      R = smem_ifft<NT>(X, Xb, &fpl, 1);
+    }
     float2* dst = a.Zout + (size_t)(t - a.frame0) * a.npairs * a.P * Q + plane;
     for (int x = threadIdx.x; x < Q; x += NT) {
       dst[(size_t)ky * Q + x] = R[pidx(2 * x)];
@@ -871,6 +881,7 @@ enum RowVariant {
   RV_GIVEN_NOISE,   // k_rows_pair<256, true>: caller-supplied spectral noise
   RV_AR_PAIR_128,   // k_rows_ar_pair<128, 4>: AR(1), Q <= 512
   RV_AR_PAIR_256_1, RV_AR_PAIR_256_2, RV_AR_PAIR_256_4, RV_AR_PAIR_512_4, RV_AR_PAIR_512_8,
+  RV_AR_PAIR_3840, RV_AR_PAIR_1920,  // k_rows_ar_pair with the compile-time in-place plans
   RV_AR_ROW_128, RV_AR_ROW_512,  // k_rows_ar<NT>: one CTA per spectral row
   RV_REG512,        // k_rows_pair512<4>
   RV_PAIR_IP_512,   // k_rows_pair_ip<512>: in place, long rows
@@ -907,6 +918,18 @@ static RowVariant rows_variant(const p2s_plan_s* pl, bool ar, bool given, size_t
       // 256-thread pair CTAs 1.84 ms)
       *sm = smem_pair(Q);
       return RV_AR_PAIR_128;
+    }
+    const auto& rq = pl->fq;
+    if (ar_rows != 1 && !(pl->force & P2S_FORCE_FFT_GENERIC) && rq.nrad == 3) {
+      const size_t sm_ip = ((size_t)3 * Q + padded_len(2 * (size_t)Q)) * sizeof(float2);
+      if (Q == 3840 && rq.rad[0] == 16 && rq.rad[1] == 16 && rq.rad[2] == 15) {
+        *sm = sm_ip;
+        return RV_AR_PAIR_3840;
+      }
+      if (Q == 1920 && rq.rad[0] == 16 && rq.rad[1] == 15 && rq.rad[2] == 8) {
+        *sm = sm_ip;
+        return RV_AR_PAIR_1920;
+      }
     }
     if (mb <= 8 && ar_rows != 1 && (Q > 1024 || ar_rows == 2) && smem_pair(Q) <= kSmemMax) {
       *sm = smem_pair(Q);
@@ -950,11 +973,11 @@ size_t rows_smem_bytes(const p2s_plan_s* pl, bool ar, bool given_noise) {
   return sm;
 }
 
-template <int NT, int MB>
+template <int NT, int MB, int QN = 0, int R1 = 1, int R2 = 1, int R3 = 1>
 static int launch_rows_ar_pair(const RowArgs& a, int P, int npairs, size_t sm, cudaStream_t s) {
   dim3 grid(P / 2 + 1, npairs);
-  P2S_SMEM_OPTIN((k_rows_ar_pair<NT, MB>), sm);
-  k_rows_ar_pair<NT, MB><<<grid, NT, sm, s>>>(a);
+  P2S_SMEM_OPTIN((k_rows_ar_pair<NT, MB, QN, R1, R2, R3>), sm);
+  k_rows_ar_pair<NT, MB, QN, R1, R2, R3><<<grid, NT, sm, s>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -997,6 +1020,8 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
     case RV_AR_PAIR_256_4: return launch_rows_ar_pair<256, 4>(a, pl->P, pl->npairs, sm, s);
     case RV_AR_PAIR_512_4: return launch_rows_ar_pair<512, 4>(a, pl->P, pl->npairs, sm, s);
     case RV_AR_PAIR_512_8: return launch_rows_ar_pair<512, 8>(a, pl->P, pl->npairs, sm, s);
+    case RV_AR_PAIR_3840: return launch_rows_ar_pair<512, 8, 3840, 16, 16, 15>(a, pl->P, pl->npairs, sm, s);
+    case RV_AR_PAIR_1920: return launch_rows_ar_pair<512, 4, 1920, 16, 15, 8>(a, pl->P, pl->npairs, sm, s);
     case RV_AR_ROW_512:
       P2S_SMEM_OPTIN(k_rows_ar<512>, sm);
       k_rows_ar<512><<<grow, 512, sm, s>>>(a);
@@ -1534,6 +1559,8 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   // two-CTAs-per-SM kernel with the widest block that fits (TC = 4 at 1080 = 12 x 10 x 9,
   // TC = 2 at 2160 = 16 x 15 x 9).
   if (pl->P > 512 && !(pl->force & (P2S_FORCE_COLS_PER_BLOCK | P2S_FORCE_COLS_PERSISTENT))) {
+    // (step 2 stays a kernel of its own here: fused into the mode-pair-0 CTAs it made them
+    // stragglers -- 4K k_cols 2.59 -> 3.47 ms against k_warp's 0.29 ms; 1080p 2.30 -> 3.17)
     const auto& rp = pl->fp;
     const bool ct = !(pl->force & P2S_FORCE_FFT_GENERIC) && rp.nrad == 3;
 #define P2S_COLS_CT(NT_, TL_, ...)                                                       \
@@ -1581,6 +1608,7 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
       return (int)cudaGetLastError();
     }
   }
+
   // Long columns: 1024 threads and up to 8640 elements per CTA double the columns per CTA
   // where that is still below 16 (1080 points: 8 columns, 64-byte row segments, 3.26 ->
   // 3.10 ms per 8 frames; 2160: 4 columns, 5.53 -> 4.67 ms per 2 frames).
