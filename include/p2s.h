@@ -39,6 +39,14 @@
  *   - Noise is counter-based (Philox4x32-10 keyed by the 64-bit seed, counter by
  *     global frame index and spectral bin), so any frame range, batch split or
  *     GPU partition reproduces the same bits.
+ *   - Kernel watchdog: the tensor-core kernels (MLP, blur) wait on mbarriers; a wait that
+ *     has not completed after 4 s (a pipeline deadlock -- a library or hardware fault,
+ *     never an input condition: every input is validated before launch) executes a trap
+ *     rather than hanging the GPU.  A trap is a sticky CUDA error: the calling process's
+ *     CUDA context is unusable afterwards (every later call, ours or the caller's,
+ *     returns cudaErrorLaunchFailure / P2S_ERR_CUDA) and must be torn down.
+ *   - The library reads no environment variables; kernel variants are chosen at plan
+ *     creation (p2s_options.force pins them for tests and A/B runs).
  */
 #ifndef P2S_H
 #define P2S_H
@@ -83,6 +91,10 @@ typedef struct {
                               * frame; nonzero selects it: the fields of frame t are those of
                               * frame 0 of the sequence translated by t (vx, vy) on the periodic
                               * grid (exact sub-pixel shift in the spectral domain, Q23).
+                              * The translation is periodic on the P x Q grid: frame
+                              * t + P/|vy| (t + Q/|vx|) repeats frame t along that axis
+                              * (512 px at 0.5 px/frame: every 1024 frames); use pad > 1 or
+                              * shorter sequences for longer non-repeating flows.
                               * Exclusive with ar_alpha.  Default (0, 0). */
   unsigned int force;       /* kernel-selection overrides, P2S_FORCE_* bits; 0 = the production
                                dispatch.  For parity tests that pin one kernel variant against
