@@ -399,6 +399,43 @@ def measure(name, args, rank, world, local, peaks):
             "gpu_launches": int(sum(n for _, n in stages.values())), "roofline": roofline, "stages": st}
 
 
+def measure_slab(args, rank, world, local, name="cfg5_4k"):
+    """Single-frame latency mode (SURVEY 8(e) NEXT-4, N > 1 only): one frame of `name` sharded
+    over the N ranks -- each rank's row pass, the NCCL all-to-all transpose, each rank's strip
+    (columns, warp, MLP, blur) -- timed per frame with CUDA events, max over ranks."""
+    import torch
+    import synth
+    from paper_2210_06713_b200 import Plan, PlanConfig, runner, slab_geometry
+    w = dict(WORKLOADS[name])
+    H, W, C, K, T = w["H"], w["W"], w["C"], w["K"], w["T"]
+    plan = Plan(PlanConfig(H=H, W=W, C=C, d_over_r0=w["d_over_r0"], K=K, taps=T, device=local, slab_count=world,
+                           slab_rank=rank, **STEP5), synth.basis(K, T, seed=0), synth.mlp_weights(K, seed=0))
+    dev = torch.device("cuda", local)
+    img = torch.from_numpy(synth.image(H, W, C, seed=0)).to(dev)
+    snd, rcv = plan.slab_counts()
+    send = torch.empty(int(snd.sum()), device=dev)
+    recv = torch.empty(int(rcv.sum()), device=dev)
+    g = slab_geometry(H, W, T, world, rank)
+    strip = torch.empty((C, H, g["x1"] - g["x0"]), device=dev)
+    for f in range(args.warmup):
+        runner.slab_simulate_frame(plan, img, SEED, f, send, recv, strip)
+    torch.cuda.synchronize()
+    import torch.distributed as dist
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for f in range(args.steps):
+        runner.slab_simulate_frame(plan, img, SEED, args.warmup + f, send, recv, strip)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = runner.max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    del plan, send, recv, strip
+    torch.cuda.empty_cache()
+    return {"config": config_dict(w, name + " sharded over the ranks (one frame, row-slab + all-to-all)", world),
+            "latency_ms_per_frame": ms, "value": 1e3 / ms, "unit": "frames/s",
+            "exchange_bytes_per_rank": int(snd.sum() - snd[rank]) * 4}
+
+
 def relaunch_under_torchrun(args):
     """`python bench.py --gpus N` (N > 1) without torchrun: run N ranks via torch.distributed.run."""
     import socket
@@ -445,6 +482,7 @@ def main():
                     "'workloads' (default: the metric's 3840x2160 RGB half); 'none' for none")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-slab", action="store_true", help="N > 1: skip the single-frame 4K slab-mode latency")
     ap.add_argument("--dry-run", action="store_true", help="rank/communicator logic only (gloo, no GPU work)")
     ap.add_argument("--force", type=lambda v: int(v, 0), default=0,
                     help="p2s_options.force bits (kernel-variant A/B runs; 0 = production dispatch)")
@@ -498,6 +536,11 @@ def main():
             extras[name] = {"config": config_dict(r["w"], name, world), "value": r["value"], "unit": "frames/s",
                             "ms_per_step": r["ms_per_step"], "e2e": r["e2e"], "clocks": r["clocks"],
                             "gpu_launches": r["gpu_launches"], "roofline": r["roofline"], "stages": r["stages"]}
+
+    if world > 1 and not args.no_slab:
+        sl = measure_slab(args, rank, world, local)
+        if rank == 0:
+            extras["cfg5_4k_slab"] = sl
 
     if rank == 0:
         r = main_res

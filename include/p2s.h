@@ -96,6 +96,10 @@ typedef struct {
                               * (512 px at 0.5 px/frame: every 1024 frames); use pad > 1 or
                               * shorter sequences for longer non-repeating flows.
                               * Exclusive with ar_alpha.  Default (0, 0). */
+  int    slab_count;        /* G >= 2: the plan is rank slab_rank's share of ONE frame sharded
+                               over G ranks (single-frame latency mode; see
+                               p2s_slab_*).  0 or 1: a normal plan.  White noise only. */
+  int    slab_rank;         /* 0 <= slab_rank < slab_count */
   unsigned int force;       /* kernel-selection overrides, P2S_FORCE_* bits; 0 = the production
                                dispatch.  For parity tests that pin one kernel variant against
                                another and for A/B measurements: every variant computes the
@@ -336,6 +340,44 @@ p2s_status p2s_host_tables(int P, int Q, double s_per_px, double d_over_r0, int 
 
 /* Smallest 5-smooth n >= x (the FFT grid rule of p2s_plan_create). */
 int p2s_grid_size(int x);
+
+/* ---------------------------------------------------------------------------------------
+ * Single-frame latency mode: one frame sharded over G ranks.
+ * Step 1's first pass (noise + PSD + row IDFT) is split by Hermitian spectral
+ * row pairs {ky, P-ky}: rank r transforms pairs kp in [kp0, kp1).  The second pass needs
+ * whole columns, so the row-transformed spectrum is transposed across ranks by one
+ * all-to-all (the caller's collective, e.g. NCCL all_to_all_single): rank r then owns the
+ * output column strip [x0, x1) of the frame plus a halo of T/2 columns each side (clipped
+ * at the frame edges), runs the column pass, the warp, the MLP and the blur on that strip
+ * and returns the strip [x0, x1).  The strips of all ranks tile the frame and are
+ * bit-identical to p2s_simulate_frames of the unsharded frame (same kernels, same
+ * per-pixel and per-bin arithmetic; the halo makes the mirror boundary exact).
+ * The plan is created with opt->slab_count = G >= 2, opt->slab_rank = r and the GLOBAL
+ * H, W; max_batch is 1.  ar_alpha and frozen flow must be 0.
+ *
+ * Exchange buffers (dev float, complex values as interleaved pairs):
+ *   send [G dest][rows_r][npairs][Ws(dest)] x 2 floats, recv [G src][rows_src][npairs][Ws(r)]
+ *   x 2 floats, rows_r = spectral rows of rank r, Ws(d) = x-halo strip width of rank d,
+ *   npairs = (Z-1+1)/2.  p2s_slab_counts gives the per-peer float counts (the split sizes
+ *   of an all_to_all_single). */
+
+/* Geometry of rank `rank` of G for a frame H x W with T taps (host only, no GPU):
+ * info[0..8] = x0, x1, hx0, hx1, kp0, kp1, rows, P, Q. */
+p2s_status p2s_slab_geometry(int H, int W, int T, int pad, int G, int rank, int64_t* info);
+
+/* Per-peer float counts of this plan's rank: send_counts[d] (to rank d), recv_counts[s]
+ * (from rank s); either pointer nullable.  Host arrays of G int64. */
+p2s_status p2s_slab_counts(p2s_plan p, int64_t* send_counts, int64_t* recv_counts);
+
+/* Phase 1 (rank r): spectral noise, PSD and the row IDFT of this rank's row pairs for frame
+ * `frame` of sequence `seed`, packed into send (see above).  Enqueued on stream. */
+p2s_status p2s_slab_rows(p2s_plan p, uint64_t seed, int64_t frame, float* send, void* stream);
+
+/* Phase 2 (rank r), after the all-to-all delivered recv: column IDFT of the halo strip,
+ * warp (gathering from the whole image img, dev float [C][H][W]), MLP, Eq.9 blur and step 5;
+ * out_strip (dev float [C][H][x1-x0]) <- the rank's output columns [x0, x1). */
+p2s_status p2s_slab_finish(p2s_plan p, const float* recv, const float* img, uint64_t seed, int64_t frame,
+                           float* out_strip, void* stream);
 
 #ifdef __cplusplus
 }

@@ -8,4 +8,4 @@ from .p2s import (FORCE_AR_PAIR_KERNEL, FORCE_AR_ROW_KERNEL, FORCE_BLUR_SINGLE, 
                   FORCE_COLS_PERSISTENT,
                   FORCE_FFT_GENERIC, FORCE_FFT_SMALL_RADIX, FORCE_NO_WARP_FUSION, FORCE_ROWS_PINGPONG,
                   FORCE_X_PLANES, FORCE_X_TILES, EXPORTS, LIB_PATH, Options, P2SError, Plan, PlanConfig, correlation_energies, fit_basis, fit_readout, train_mlp,  # noqa: F401
-                  grid_size, host_tables, lib, philox_fill)
+                  grid_size, host_tables, lib, philox_fill, slab_geometry)

@@ -387,6 +387,8 @@ static void clear_timing(p2s_plan_s* p);
 static void free_plan(p2s_plan_s* p) {
   if (!p) return;
   clear_timing(p);
+  cudaFree(p->d_slab_ky);
+  cudaFree(p->d_slab_dest);
   cudaFree(p->d_sqrtS);
   cudaFree(p->d_ar);
   cudaFree(p->d_L);
@@ -470,6 +472,47 @@ static p2s_status run_step1(p2s_plan_s* p, uint64_t seed, int64_t f0, int F, cud
   return P2S_OK;
 }
 
+// Slab-mode tables (NEXT-4): this rank's spectral rows in pack order, the destinations'
+// strip columns and block offsets, the rows of the receive buffer in source order, and the
+// per-peer float counts of the all-to-all.
+static p2s_status build_slab_tables(p2s_plan_s* p) {
+  const int G = p->slab_G, P = p->P, W = p->W_glob, T = p->T, np = p->npairs;
+  auto rows_of = [&](const SlabGeom& g, std::vector<int>& v) {
+    for (int kp = g.kp0; kp < g.kp1; ++kp) {
+      v.push_back(kp);
+      if (kp != 0 && 2 * kp != P) v.push_back(P - kp);
+    }
+  };
+  const SlabGeom me = slab_geometry(W, T, P, G, p->slab_r);
+  std::vector<int> ky;  // [rows_r] pack order, then [P] receive order
+  rows_of(me, ky);
+  std::vector<int> dest(3 * (size_t)G);
+  p->slab_send.assign(G, 0);
+  p->slab_recv.assign(G, 0);
+  int64_t off = 0;
+  const int ws_me = p->W;
+  for (int d = 0; d < G; ++d) {
+    const SlabGeom gd = slab_geometry(W, T, P, G, d);
+    const int ws = gd.hx1 - gd.hx0;
+    dest[3 * d] = gd.hx0;
+    dest[3 * d + 1] = ws;
+    if (off > INT32_MAX) return set_error(P2S_ERR_UNSUPPORTED, "slab send buffer above 2^31 complex values");
+    dest[3 * d + 2] = (int)off;
+    const int64_t n = (int64_t)me.rows * np * ws;
+    off += n;
+    p->slab_send[d] = 2 * n;
+    rows_of(gd, ky);  // rows sent by rank d, in its pack order = their order in our recv buffer
+    p->slab_recv[d] = 2 * (int64_t)gd.rows * np * ws_me;
+  }
+  if ((int)ky.size() != me.rows + P) return set_error(P2S_ERR_NUMERIC, "slab row partition does not cover the grid");
+  P2S_CUDA(cudaMalloc(&p->d_slab_ky, sizeof(int) * ky.size()), "cudaMalloc slab rows");
+  P2S_CUDA(cudaMemcpy(p->d_slab_ky, ky.data(), sizeof(int) * ky.size(), cudaMemcpyHostToDevice), "copy slab rows");
+  P2S_CUDA(cudaMalloc(&p->d_slab_dest, sizeof(int) * dest.size()), "cudaMalloc slab dests");
+  P2S_CUDA(cudaMemcpy(p->d_slab_dest, dest.data(), sizeof(int) * dest.size(), cudaMemcpyHostToDevice),
+           "copy slab dests");
+  return P2S_OK;
+}
+
 }  // namespace p2s
 
 using namespace p2s;
@@ -529,13 +572,37 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
     return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "P2S_FORCE_X_PLANES and _X_TILES are exclusive");
   if ((o.force & P2S_FORCE_AR_ROW_KERNEL) && (o.force & P2S_FORCE_AR_PAIR_KERNEL))
     return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "P2S_FORCE_AR_ROW_KERNEL and _AR_PAIR_KERNEL are exclusive");
-  p->xtile = x_tile_layout(p);
   p->P = grid_size(pad * H);
   p->Q = grid_size(pad * W);
   if (p->P > 4096 || p->Q > 4096) {
     delete p;
     return set_error(P2S_ERR_UNSUPPORTED, "FFT grid larger than 4096 per axis");
   }
+  p->W_glob = W;
+  if (o.slab_count > 1) {  // NEXT-4: this rank's share of one frame; steps 1b-5 on its halo strip
+    const int G = o.slab_count, r = o.slab_rank;
+    if (r < 0 || r >= G || G > 64)
+      return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "slab_rank must be in [0, slab_count), slab_count <= 64");
+    if (o.ar_alpha != 0.f || o.flow_px_per_frame[0] != 0.f || o.flow_px_per_frame[1] != 0.f)
+      return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "slab mode samples white-noise frames only");
+    const SlabGeom g = slab_geometry(W, T, p->P, G, r);
+    for (int d = 0; d < G; ++d) {
+      const SlabGeom gd = slab_geometry(W, T, p->P, G, d);
+      if (gd.hx1 - gd.hx0 < T || gd.x1 <= gd.x0)
+        return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "slab strips narrower than the taps: fewer ranks");
+    }
+    p->slab_G = G;
+    p->slab_r = r;
+    p->slab_x0 = g.x0;
+    p->slab_x1 = g.x1;
+    p->slab_hx0 = g.hx0;
+    p->slab_kp0 = g.kp0;
+    p->slab_kp1 = g.kp1;
+    p->slab_rows = g.rows;
+    p->W = g.hx1 - g.hx0;
+    o.max_batch = 1;
+  }
+  p->xtile = x_tile_layout(p);
   p->nslots = Z - 1;
   p->npairs = (p->nslots + 1) / 2;
 
@@ -639,6 +706,7 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
   p->basis_host.assign(basis, basis + (size_t)K * T * T);
   P2S_TRY(build_blur(p, basis));
   P2S_TRY(alloc_workspace(p));
+  if (p->slab_G > 1) P2S_TRY(build_slab_tables(p));
   if (p->ar_alpha != 0.f) {
     cudaError_t e = cudaMalloc(&p->d_ar, sizeof(float4) * (size_t)p->npairs * p->P * p->Q);
     if (e != cudaSuccess) {
@@ -665,6 +733,8 @@ extern "C" p2s_status p2s_plan_destroy(p2s_plan p) {
 
 #define CHECK_PLAN()                                                         \
   if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");       \
+  if (p->slab_G > 1)                                                         \
+    return set_error(P2S_ERR_INVALID_ARGUMENT, "slab plans run through p2s_slab_rows / p2s_slab_finish"); \
   if (nframes < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "nframes < 0"); \
   if (frame0 < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "frame0 < 0");
 
@@ -1028,5 +1098,77 @@ extern "C" p2s_status p2s_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uin
                                       uint32_t* out, void* stream) {
   if (n < 0 || (n > 0 && !out)) return set_error(P2S_ERR_INVALID_ARGUMENT, "bad argument");
   P2S_LAUNCH(launch_philox_fill(c1, c2, c3, k0, k1, n, out, (cudaStream_t)stream), "k_philox_fill");
+  return P2S_OK;
+}
+
+// ------------------------------------------------------------------ slab mode (NEXT-4)
+extern "C" p2s_status p2s_slab_geometry(int H, int W, int T, int pad, int G, int rank, int64_t* info) {
+  g_err.clear();
+  if (!info) return set_error(P2S_ERR_INVALID_ARGUMENT, "info is NULL");
+  if (H < 1 || W < 1 || T < 1 || G < 1 || rank < 0 || rank >= G)
+    return set_error(P2S_ERR_INVALID_ARGUMENT, "bad slab geometry arguments");
+  const int P = grid_size((pad > 0 ? pad : 1) * H), Q = grid_size((pad > 0 ? pad : 1) * W);
+  const SlabGeom g = slab_geometry(W, T, P, G, rank);
+  const int64_t v[9] = {g.x0, g.x1, g.hx0, g.hx1, g.kp0, g.kp1, g.rows, P, Q};
+  std::memcpy(info, v, sizeof(v));
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_slab_counts(p2s_plan p, int64_t* send_counts, int64_t* recv_counts) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (p->slab_G < 2) return set_error(P2S_ERR_INVALID_ARGUMENT, "not a slab plan");
+  for (int d = 0; d < p->slab_G; ++d) {
+    if (send_counts) send_counts[d] = p->slab_send[d];
+    if (recv_counts) recv_counts[d] = p->slab_recv[d];
+  }
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_slab_rows(p2s_plan p, uint64_t seed, int64_t frame, float* send, void* stream) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (p->slab_G < 2) return set_error(P2S_ERR_INVALID_ARGUMENT, "not a slab plan");
+  if (frame < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "frame < 0");
+  if (!send) return set_error(P2S_ERR_INVALID_ARGUMENT, "send is NULL");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    StageScope sc(p, 0, s);
+    P2S_LAUNCH(launch_rows(p, seed, frame, 1, false, 1, frame, s), "k_rows (slab)");
+    P2S_LAUNCH(launch_slab_pack(p, reinterpret_cast<float2*>(send), s), "k_slab_pack");
+  }
+  return P2S_OK;
+}
+
+extern "C" p2s_status p2s_slab_finish(p2s_plan p, const float* recv, const float* img, uint64_t seed, int64_t frame,
+                                      float* out_strip, void* stream) {
+  if (!p) return set_error(P2S_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (p->slab_G < 2) return set_error(P2S_ERR_INVALID_ARGUMENT, "not a slab plan");
+  if (frame < 0) return set_error(P2S_ERR_INVALID_ARGUMENT, "frame < 0");
+  if (!recv || !img || !out_strip) return set_error(P2S_ERR_INVALID_ARGUMENT, "NULL buffer");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    StageScope sc(p, 1, s);
+    P2S_LAUNCH(launch_slab_unpack(p, reinterpret_cast<const float2*>(recv), s), "k_slab_unpack");
+    P2S_LAUNCH(launch_cols(p, 1, 1, nullptr, s, nullptr, 0, nullptr), "k_cols (slab strip)");
+  }
+  {
+    StageScope sc(p, 2, s);
+    P2S_LAUNCH(launch_warp_sim(p, 1, img, 0, s), "k_warp (slab strip)");
+  }
+  {
+    StageScope sc(p, 3, s);
+    P2S_LAUNCH(launch_mlp(p, 1, true, s), "k_mlp");
+  }
+  const size_t HWs = (size_t)p->H * p->W;
+  {
+    StageScope sc(p, 4, s);
+    P2S_LAUNCH(launch_blur(p, 1, p->d_Iw, false, seed, frame, p->d_out, s), "k_blur");
+  }
+  const int wo = p->slab_x1 - p->slab_x0;
+  P2S_CUDA(cudaMemcpy2DAsync(out_strip, (size_t)wo * 4, p->d_out + (p->slab_x0 - p->slab_hx0), (size_t)p->W * 4,
+                             (size_t)wo * 4, (size_t)p->C * p->H, cudaMemcpyDeviceToDevice, s),
+           "copy slab strip");
+  (void)HWs;
   return P2S_OK;
 }

@@ -57,6 +57,7 @@ struct BlurArgs {
   int64_t frame0;
   float sigma;
   int normalize, clamp01;
+  int noise_x0, noise_W;    // step-5 noise counter y * noise_W + noise_x0 + x (slab strips: frame coordinates)
   unsigned long long* probe;  // optional [8] cycle counters (P2S_BLUR_PROBE), else null
   int brep, brows;            // B image copies; rows between copies (pair mode tensor map)
   size_t bstride;             // bytes between copies (bulk path)
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
               if (a.normalize) o = o / g;
               if (a.sigma != 0.f) {
                 const int64_t fr = a.frame0 + f;
-                uint4 rx = philox4x32_10(make_uint4((uint32_t)(y * a.W + x), (uint32_t)ch | (1u << 16), (uint32_t)fr,
+                uint4 rx = philox4x32_10(make_uint4((uint32_t)(y * a.noise_W + a.noise_x0 + x), (uint32_t)ch | (1u << 16), (uint32_t)fr,
                                                     (uint32_t)((uint64_t)fr >> 32)),
                                          a.k0, a.k1);
                 o += a.sigma * box_muller(rx.x, rx.y).x;
@@ -593,6 +594,8 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   a.k1 = (uint32_t)(seed >> 32);
   a.frame0 = frame0;
   a.sigma = p->noise_sigma;
+  a.noise_x0 = p->slab_G > 1 ? p->slab_hx0 : 0;
+  a.noise_W = p->slab_G > 1 ? p->W_glob : p->W;
   a.normalize = p->normalize;
   a.clamp01 = p->clamp01;
   a.probe = nullptr;

@@ -18,6 +18,8 @@
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
+#include <algorithm>
+
 #include <cstdlib>
 
 namespace p2s {
@@ -465,6 +467,7 @@ struct RowArgs {
   int load_state;       // AR: state holds eta_{frame0-1}
   int flow;             // frozen flow: frame-0 noise translated by (vx, vy) * frame pixels
   double vx, vy;
+  int ky0;              // first Hermitian row pair of the launch (slab mode; 0 otherwise)
 };
 
 // Frozen flow (reading Q23): shift factor of bin k of an n-point axis for a
@@ -519,7 +522,7 @@ __global__ void __launch_bounds__(NT) k_rows_pair(RowArgs a) {
   float2* Xb = X + padded_len(2 * Q);              // ping-pong partner
   __shared__ FFTPlanSmem fpl;
   stage_fft_plan(&fpl, a.fq, twq);
-  const int ky = blockIdx.x, p = blockIdx.y;
+  const int ky = a.ky0 + (int)blockIdx.x, p = blockIdx.y;
   const int k1 = ky ? a.P - ky : 0;
   const size_t plane = (size_t)p * a.P * Q;
   for (int kx = threadIdx.x; kx < Q; kx += NT) {
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(NT, 2) k_rows_pair_ip(RowArgs a) {
     build_twp3<QN, R1, R2, R3>(twq, a.fq.tw);
   else
     stage_fft_plan(&fpl, a.fq, twq);
-  const int ky = blockIdx.x, p = blockIdx.y;
+  const int ky = a.ky0 + (int)blockIdx.x, p = blockIdx.y;
   const int k1 = ky ? a.P - ky : 0;
   const size_t plane = (size_t)p * a.P * Q;
   const float2* sS0 = a.sqrtS + plane + (size_t)ky * Q;
@@ -646,7 +649,7 @@ __global__ void __launch_bounds__(64 * NG, 3) k_rows_pair512(RowArgs a) {
   float2* tw = reinterpret_cast<float2*>(smem);  // [N] per-pass twiddle table (build_twp)
   float2* sS = tw + N;                           // [2][N] sqrt(S) of both rows
   float2* xb = sS + 2 * N;                       // [NG][2][XL] exchange buffers
-  const int ky = blockIdx.x, p = blockIdx.y;
+  const int ky = a.ky0 + (int)blockIdx.x, p = blockIdx.y;
   const int k1 = ky ? a.P - ky : 0;
   const size_t plane = (size_t)p * a.P * N;
   build_twp(tw, a.fq.tw, threadIdx.x, 64 * NG);
@@ -739,7 +742,7 @@ __global__ void __launch_bounds__(NT) k_rows_ar(RowArgs a) {
   float2* Xb = X + padded_len(Q);
   __shared__ FFTPlanSmem fpl;
   stage_fft_plan(&fpl, a.fq, twq);
-  const int ky = blockIdx.x, p = blockIdx.y;
+  const int ky = a.ky0 + (int)blockIdx.x, p = blockIdx.y;
   const size_t row = ((size_t)p * a.P + ky) * Q;
   for (int kx = threadIdx.x; kx < Q; kx += NT) {
     sS[kx] = a.sqrtS[row + kx];
@@ -796,7 +799,7 @@ __global__ void __launch_bounds__(NT) k_rows_ar_pair(RowArgs a) {
     build_twp3<QN, R1, R2, R3>(twq, a.fq.tw);
   else
     stage_fft_plan(&fpl, a.fq, twq);
-  const int ky = blockIdx.x, p = blockIdx.y;
+  const int ky = a.ky0 + (int)blockIdx.x, p = blockIdx.y;
   const int k1 = ky ? a.P - ky : 0;
   const size_t plane = (size_t)p * a.P * Q;
   const size_t row = plane + (size_t)ky * Q, rowm = plane + (size_t)k1 * Q;
@@ -1008,7 +1011,11 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
   size_t sm = 0;
   const RowVariant v = rows_variant(pl, ar, eta != nullptr, &sm);
   if (sm > kSmemMax) return (int)cudaErrorInvalidConfiguration;
-  const dim3 gpair(pl->P / 2 + 1, pl->npairs), grow(pl->P, pl->npairs);
+  // slab mode: this rank's Hermitian row pairs [kp0, kp1) only (white noise)
+  a.ky0 = pl->slab_G > 1 ? pl->slab_kp0 : 0;
+  const int npr = pl->slab_G > 1 ? pl->slab_kp1 - pl->slab_kp0 : pl->P / 2 + 1;
+  if (npr <= 0) return 0;
+  const dim3 gpair(npr, pl->npairs), grow(pl->P, pl->npairs);
   switch (v) {
     case RV_GIVEN_NOISE:
       P2S_SMEM_OPTIN((k_rows_pair<256, true>), sm);
@@ -1514,7 +1521,7 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   fill_fft_args(a.fp, pl->fp);
   a.Zin = pl->d_Z;
   a.P = pl->P;
-  a.Q = pl->Q;
+  a.Q = pl->slab_G > 1 ? pl->W : pl->Q;  // slab mode: the unpacked halo strip [npairs][P][W]
   a.H = pl->H;
   a.W = pl->W;
   a.npairs = pl->npairs;
@@ -1712,6 +1719,63 @@ int launch_philox_fill(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint3
                        cudaStream_t s) {
   if (n <= 0) return 0;
   k_philox_fill<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c1, c2, c3, k0, k1, n, reinterpret_cast<uint4*>(out));
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ slab mode (NEXT-4)
+// Rank r's geometry: output columns [x0, x1) balanced over G, halo T/2 each side clipped to
+// the frame, Hermitian row pairs [kp0, kp1) of the P/2 + 1 balanced over G, and the number
+// of spectral rows they hold (pair 0 and, for even P, pair P/2 are their own mirror).
+SlabGeom slab_geometry(int W, int T, int P, int G, int r) {
+  SlabGeom g;
+  const int c = T / 2;
+  g.x0 = (int)((int64_t)W * r / G);
+  g.x1 = (int)((int64_t)W * (r + 1) / G);
+  g.hx0 = std::max(0, g.x0 - c);
+  g.hx1 = std::min(W, g.x1 + c);
+  const int npr = P / 2 + 1;
+  g.kp0 = (int)((int64_t)npr * r / G);
+  g.kp1 = (int)((int64_t)npr * (r + 1) / G);
+  g.rows = 0;
+  for (int kp = g.kp0; kp < g.kp1; ++kp) g.rows += (kp == 0 || 2 * kp == P) ? 1 : 2;
+  return g;
+}
+
+// Pack this rank's row-transformed rows (d_Z [npairs][P][Q]) into the send blocks:
+// block d = [rows_r][npairs][Ws(d)], columns [hx0(d), hx0(d) + Ws(d)) of each row.
+__global__ void k_slab_pack(const float2* __restrict__ Z, float2* __restrict__ send, const int* __restrict__ ky_of,
+                            const int* __restrict__ dest, int G, int P, int Q, int npairs, int rows) {
+  const int l = blockIdx.x, p = blockIdx.y;
+  const int ky = ky_of[l];
+  const float2* src = Z + ((size_t)p * P + ky) * Q;
+  for (int d = 0; d < G; ++d) {
+    const int hx0 = dest[3 * d], ws = dest[3 * d + 1];
+    float2* dst = send + (size_t)dest[3 * d + 2] + ((size_t)l * npairs + p) * ws;
+    for (int x = threadIdx.x; x < ws; x += blockDim.x) dst[x] = src[hx0 + x];
+  }
+}
+
+// Unpack the received rows (recv [G src][rows_src][npairs][Ws], i.e. rows in source order)
+// into the strip spectrum d_Z [npairs][P][Ws] for the column pass.
+__global__ void k_slab_unpack(const float2* __restrict__ recv, float2* __restrict__ Z, const int* __restrict__ ky_of,
+                              int P, int npairs, int ws) {
+  const int i = blockIdx.x, p = blockIdx.y;
+  const float2* src = recv + ((size_t)i * npairs + p) * ws;
+  float2* dst = Z + ((size_t)p * P + ky_of[i]) * ws;
+  for (int x = threadIdx.x; x < ws; x += blockDim.x) dst[x] = src[x];
+}
+
+int launch_slab_pack(const p2s_plan_s* pl, float2* send, cudaStream_t s) {
+  if (pl->slab_rows == 0) return 0;
+  dim3 grid(pl->slab_rows, pl->npairs);
+  k_slab_pack<<<grid, 256, 0, s>>>(pl->d_Z, send, pl->d_slab_ky, pl->d_slab_dest, pl->slab_G, pl->P, pl->Q,
+                                   pl->npairs, pl->slab_rows);
+  return (int)cudaGetLastError();
+}
+
+int launch_slab_unpack(const p2s_plan_s* pl, const float2* recv, cudaStream_t s) {
+  dim3 grid(pl->P, pl->npairs);
+  k_slab_unpack<<<grid, 256, 0, s>>>(recv, pl->d_Z, pl->d_slab_ky + pl->slab_rows, pl->P, pl->npairs, pl->W);
   return (int)cudaGetLastError();
 }
 

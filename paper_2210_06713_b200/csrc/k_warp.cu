@@ -19,6 +19,8 @@ struct WarpArgs {
   float cx, cy0, cy1;  // dx = cx t0 ; dy = cy0 t0 + cy1 t1
   void* out;           // [F][C][H][W] fp32 or bf16
   int C, H, W;
+  int x_off, W_img;    // output column x samples image column x_off + x of an H x W_img image
+                       // (slab mode: the rank's halo strip of the frame; else 0, W)
 };
 
 template <bool BF16_OUT>
@@ -30,20 +32,22 @@ __global__ void __launch_bounds__(256) k_warp(WarpArgs a) {
   const int y = pix / a.W, x = pix - y * a.W;
   const float u = __ldg(&a.t0[(size_t)f * a.t_stride + pix]);
   const float v = __ldg(&a.t1[(size_t)f * a.t_stride + pix]);
-  const float X = (float)x + a.cx * u;
+  const float X = (float)(a.x_off + x) + a.cx * u;
   const float Y = (float)y + a.cy0 * u + a.cy1 * v;
   const float fx = floorf(X), fy = floorf(Y);
   const float tx = X - fx, ty = Y - fy;
-  int xa = (int)fmaxf(fminf(fx, (float)(a.W - 1)), -1.f);
+  const int Wi = a.W_img;
+  int xa = (int)fmaxf(fminf(fx, (float)(Wi - 1)), -1.f);
   int ya = (int)fmaxf(fminf(fy, (float)(a.H - 1)), -1.f);
-  int xb = min(xa + 1, a.W - 1), yb = min(ya + 1, a.H - 1);
+  int xb = min(xa + 1, Wi - 1), yb = min(ya + 1, a.H - 1);
   xa = max(xa, 0);
   ya = max(ya, 0);
   const float* I = a.img + (size_t)f * a.img_stride;
+  const size_t HWi = (size_t)a.H * Wi;
   for (int c = 0; c < a.C; ++c) {
-    const float* Ic = I + (size_t)c * HW;
-    const float i00 = __ldg(&Ic[ya * a.W + xa]), i01 = __ldg(&Ic[ya * a.W + xb]);
-    const float i10 = __ldg(&Ic[yb * a.W + xa]), i11 = __ldg(&Ic[yb * a.W + xb]);
+    const float* Ic = I + (size_t)c * HWi;
+    const float i00 = __ldg(&Ic[ya * Wi + xa]), i01 = __ldg(&Ic[ya * Wi + xb]);
+    const float i10 = __ldg(&Ic[yb * Wi + xa]), i11 = __ldg(&Ic[yb * Wi + xb]);
     const float val = (1.f - ty) * ((1.f - tx) * i00 + tx * i01) + ty * ((1.f - tx) * i10 + tx * i11);
     const size_t o = ((size_t)f * a.C + c) * HW + pix;
     if (BF16_OUT)
@@ -69,6 +73,8 @@ int launch_warp_f32(const p2s_plan_s* p, int F, const float* img, int64_t stride
   a.C = p->C;
   a.H = p->H;
   a.W = p->W;
+  a.x_off = 0;
+  a.W_img = p->W;
   dim3 grid((unsigned)((HW + 255) / 256), F);
   k_warp<false><<<grid, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
@@ -91,6 +97,8 @@ int launch_warp_sim(const p2s_plan_s* p, int F, const float* img, int64_t stride
   a.C = p->C;
   a.H = p->H;
   a.W = p->W;
+  a.x_off = p->slab_G > 1 ? p->slab_hx0 : 0;
+  a.W_img = p->slab_G > 1 ? p->W_glob : p->W;
   dim3 grid((unsigned)((HW + 255) / 256), F);
   k_warp<true><<<grid, 256, 0, s>>>(a);
   return (int)cudaGetLastError();

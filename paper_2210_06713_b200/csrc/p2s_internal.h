@@ -118,6 +118,13 @@ struct p2s_plan_s {
   double flow_vx = 0, flow_vy = 0;  // frozen flow, pixels per frame (0 = off)
   int normalize = 0, clamp01 = 0, device = 0, max_batch = 0;
   unsigned force = 0;           // p2s_options.force (P2S_FORCE_* bits), fixed at plan creation
+  // single-frame slab mode (NEXT-4; slab_G > 1): this rank's geometry.  W above is then the
+  // rank's x-halo strip width (steps 1b-5 run on the strip), W_glob the frame's width.
+  int slab_G = 1, slab_r = 0, W_glob = 0;
+  int slab_x0 = 0, slab_x1 = 0, slab_hx0 = 0, slab_kp0 = 0, slab_kp1 = 0, slab_rows = 0;
+  int* d_slab_ky = nullptr;     // device: [rows_r] this rank's rows (pack) | [P] rows in recv order (unpack)
+  int* d_slab_dest = nullptr;   // device: [G][3] per destination: hx0, width, float2 offset of its block
+  std::vector<int64_t> slab_send, slab_recv;  // per-peer float counts
   int xtile = 0;                // MLP input layout, fixed at plan creation (1: tile-major, x_index)
   double clamped_max = 0;
   std::vector<double> A0, Lc;      // Z x Z
@@ -182,6 +189,12 @@ int launch_zern_to_x(const p2s_plan_s* p, int F, const float* zern, cudaStream_t
 int launch_warp_f32(const p2s_plan_s* p, int F, const float* img, int64_t stride, const float* zern, float* out,
                     cudaStream_t s);
 int launch_warp_sim(const p2s_plan_s* p, int F, const float* img, int64_t stride, cudaStream_t s);
+int launch_slab_pack(const p2s_plan_s* p, float2* send, cudaStream_t s);
+int launch_slab_unpack(const p2s_plan_s* p, const float2* recv, cudaStream_t s);
+struct SlabGeom {
+  int x0, x1, hx0, hx1, kp0, kp1, rows;
+};
+SlabGeom slab_geometry(int W, int T, int P, int G, int r);
 int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s);
 size_t rows_smem_bytes(const p2s_plan_s* p, bool ar, bool given_noise);  // row pass dynamic smem
 int x_tile_layout(const p2s_plan_s* p);  // decided at plan creation; 1: MLP input X tile-major (x_index)

@@ -24,7 +24,8 @@ EXPORTS = ("p2s_plan_create", "p2s_plan_destroy", "p2s_sample_zernike", "p2s_war
            "p2s_simulate_frames", "p2s_simulate_frames_host", "p2s_last_error", "p2s_plan_info",
            "p2s_plan_export_tables", "p2s_plan_import_sqrtS", "p2s_plan_stage_timing", "p2s_plan_stage_times", "p2s_field_autocorr", "p2s_exact_psf", "p2s_render_exact", "p2s_fit_basis", "p2s_fit_readout", "p2s_blur_weights", "p2s_correlation_energies", "p2s_aperture_stats", "p2s_train_mlp", "p2s_sample_zernike_from_noise",
            "p2s_philox_fill",
-           "p2s_host_tables", "p2s_grid_size")
+           "p2s_host_tables", "p2s_grid_size", "p2s_slab_geometry", "p2s_slab_counts", "p2s_slab_rows",
+           "p2s_slab_finish")
 
 
 class P2SError(RuntimeError):
@@ -38,7 +39,8 @@ class Options(ctypes.Structure):
                 ("s_per_px", ctypes.c_double), ("tilt_px_per_rad", ctypes.c_double), ("pad", ctypes.c_int),
                 ("mlp_hidden", ctypes.c_int * 2), ("max_batch", ctypes.c_int), ("ar_alpha", ctypes.c_float),
                 ("noise_sigma", ctypes.c_float), ("normalize_psf_sum", ctypes.c_int), ("clamp01", ctypes.c_int),
-                ("device", ctypes.c_int), ("flow_px_per_frame", ctypes.c_float * 2), ("force", ctypes.c_uint)]
+                ("device", ctypes.c_int), ("flow_px_per_frame", ctypes.c_float * 2), ("slab_count", ctypes.c_int),
+                ("slab_rank", ctypes.c_int), ("force", ctypes.c_uint)]
 
 
 # p2s_options.force bits (include/p2s.h): kernel-selection overrides for tests / A-B runs
@@ -88,6 +90,10 @@ def _load():
     lib.p2s_blur_weights.argtypes = [vp, vp, vp, u64, i64, vp, i32, vp]
     lib.p2s_render_exact.argtypes = [vp, vp, vp, i32, vp, vp]
     lib.p2s_host_tables.argtypes = [i32, i32, ctypes.c_double, ctypes.c_double, i32, vp, vp, vp, vp]
+    lib.p2s_slab_geometry.argtypes = [i32, i32, i32, i32, i32, i32, vp]
+    lib.p2s_slab_counts.argtypes = [vp, vp, vp]
+    lib.p2s_slab_rows.argtypes = [vp, u64, i64, vp, vp]
+    lib.p2s_slab_finish.argtypes = [vp, vp, vp, u64, i64, vp, vp]
     lib.p2s_grid_size.argtypes = [i32]
     lib.p2s_grid_size.restype = i32
     for name in EXPORTS:
@@ -125,6 +131,17 @@ def _stream(stream):
 
 def grid_size(x: int) -> int:
     return lib.p2s_grid_size(int(x))
+
+
+SLAB_KEYS = ("x0", "x1", "hx0", "hx1", "kp0", "kp1", "rows", "P", "Q")
+
+
+def slab_geometry(H, W, T, G, rank, pad=1):
+    """Rank `rank`'s share of one H x W frame over G ranks (single-frame slab mode, NEXT-4):
+    output columns [x0, x1), halo strip [hx0, hx1), Hermitian row pairs [kp0, kp1), rows."""
+    info = np.zeros(9, dtype=np.int64)
+    _check(lib.p2s_slab_geometry(H, W, T, pad, G, rank, info.ctypes.data))
+    return dict(zip(SLAB_KEYS, (int(v) for v in info)))
 
 
 def host_tables(P, Q, s_per_px, d_over_r0, Z=36, want_sqrtS=True):
@@ -213,6 +230,8 @@ class PlanConfig:
     clamp01: bool = False
     device: int = 0
     flow: tuple = (0.0, 0.0)  # frozen flow (vx, vy) pixels per frame (NEXT-3)
+    slab_count: int = 0  # >= 2: rank slab_rank's share of one frame (single-frame latency mode, NEXT-4)
+    slab_rank: int = 0
     force: int = 0  # FORCE_* bits (kernel-selection overrides; 0 = production dispatch)
     extra: dict = field(default_factory=dict)
 
@@ -239,6 +258,8 @@ class Plan:
         o.clamp01 = int(cfg.clamp01)
         o.device = cfg.device
         o.flow_px_per_frame[0], o.flow_px_per_frame[1] = cfg.flow
+        o.slab_count = cfg.slab_count
+        o.slab_rank = cfg.slab_rank
         o.force = cfg.force
         self._h = ctypes.c_void_p()
         _check(lib.p2s_plan_create(ctypes.byref(self._h), cfg.H, cfg.W, cfg.C, float(cfg.d_over_r0),
@@ -308,6 +329,23 @@ class Plan:
         assert out_host.dtype == np.float32 and out_host.flags.c_contiguous
         _check(lib.p2s_simulate_frames_host(self._h, ctypes.c_void_p(img_host.ctypes.data), img_frame_stride, seed,
                                             frame0, nframes, ctypes.c_void_p(out_host.ctypes.data), _stream(stream)))
+
+    # ---- single-frame slab mode (NEXT-4)
+    def slab_counts(self):
+        """(send, recv) per-peer float counts of the all-to-all (numpy int64 [G] each)."""
+        G = self.cfg.slab_count
+        snd = np.zeros(G, dtype=np.int64)
+        rcv = np.zeros(G, dtype=np.int64)
+        _check(lib.p2s_slab_counts(self._h, snd.ctypes.data, rcv.ctypes.data))
+        return snd, rcv
+
+    def slab_rows(self, seed, frame, send, stream=None):
+        """Phase 1: this rank's row pass packed into send (device float32, sum(send counts))."""
+        _check(lib.p2s_slab_rows(self._h, seed, frame, _ptr(send), _stream(stream)))
+
+    def slab_finish(self, recv, img, seed, frame, out_strip, stream=None):
+        """Phase 2 after the all-to-all: out_strip (device float32 [C][H][x1-x0]) <- this rank's columns."""
+        _check(lib.p2s_slab_finish(self._h, _ptr(recv), _ptr(img), seed, frame, _ptr(out_strip), _stream(stream)))
 
     # ---- introspection
     def export_tables(self):

@@ -85,3 +85,30 @@ class FrameShardedRunner:
             img_local = img if img_frame_stride == 0 else img[f0 - frame_base:]
             self.plan.simulate_frames(img_local, img_frame_stride, seed, f0, n, out_local, stream)
         return f0, n
+
+
+# ---------------------------------------------------------------- single-frame slab mode (NEXT-4)
+def slab_counts_host(H: int, W: int, T: int, G: int, rank: int, npairs: int = 18, pad: int = 1):
+    """Per-peer float counts of rank `rank`'s all-to-all (send[d], recv[s]), from the host
+    geometry alone: block (s -> d) = rows_s x npairs x strip width of d, complex as 2 floats."""
+    from .p2s import slab_geometry
+    geo = [slab_geometry(H, W, T, G, r, pad) for r in range(G)]
+    me = geo[rank]
+    send = [2 * me["rows"] * npairs * (g["hx1"] - g["hx0"]) for g in geo]
+    recv = [2 * g["rows"] * npairs * (me["hx1"] - me["hx0"]) for g in geo]
+    return send, recv
+
+
+def slab_exchange(send, recv, send_counts, recv_counts, group=None):
+    """The transpose of SURVEY 8(e) NEXT-4: one all_to_all_single (NCCL over NVLink on GPUs,
+    gloo in the CPU tests) with the per-peer split sizes of p2s_slab_counts."""
+    import torch.distributed as dist
+    dist.all_to_all_single(recv, send, [int(c) for c in recv_counts], [int(c) for c in send_counts], group=group)
+
+
+def slab_simulate_frame(plan, img, seed, frame, send, recv, out_strip, group=None):
+    """One frame on this rank in slab mode: row pass -> all-to-all -> strip pass."""
+    snd, rcv = plan.slab_counts()
+    plan.slab_rows(seed, frame, send)
+    slab_exchange(send, recv, snd, rcv, group)
+    plan.slab_finish(recv, img, seed, frame, out_strip)

@@ -115,3 +115,61 @@ def test_bench_gpus2_dry_run_launches_two_ranks(workload):
     assert d["n_gpus"] == 2 and d["dry_run"]
     assert d["comm"]["world_size"] == 2 and d["comm"]["allreduce_ranks"] == 2
     assert d["distinct_frames"] == d["frames_expected"]
+
+
+def _slab_worker(rank, world, port, q):
+    """Ranks exchange synthetic row blocks laid out as p2s_slab_rows packs them; every
+    received row must be the right (source row, pair, column) of the frame."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2210_06713_b200 import slab_geometry
+        H, W, T, npairs = 40, 70, 9, 3
+        geo = [slab_geometry(H, W, T, world, r) for r in range(world)]
+        P = geo[0]["P"]
+
+        def rows(g):
+            out = []
+            for kp in range(g["kp0"], g["kp1"]):
+                out.append(kp)
+                if kp != 0 and 2 * kp != P:
+                    out.append(P - kp)
+            return out
+
+        me = geo[rank]
+        snd_c, rcv_c = runner.slab_counts_host(H, W, T, world, rank, npairs)
+        # value of (row ky, pair p, column x) of the row-transformed spectrum: a unique tag
+        tag = lambda ky, p, x: float(ky * 1000 + p * 100000 + x)  # noqa: E731
+        blocks = []
+        for g in geo:
+            blk = [[tag(ky, p, x), 0.5] for ky in rows(me) for p in range(npairs) for x in range(g["hx0"], g["hx1"])]
+            blocks.append(torch.tensor(blk, dtype=torch.float32).reshape(-1))
+        send = torch.cat(blocks)
+        assert [b.numel() for b in blocks] == snd_c
+        recv = torch.empty(sum(rcv_c))
+        runner.slab_exchange(send, recv, snd_c, rcv_c)
+        exp = [[tag(ky, p, x), 0.5] for g in geo for ky in rows(g) for p in range(npairs)
+               for x in range(me["hx0"], me["hx1"])]
+        ok = torch.equal(recv, torch.tensor(exp, dtype=torch.float32).reshape(-1))
+        covered = sorted(ky for g in geo for ky in rows(g)) == list(range(P))
+        q.put((rank, ok and covered))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_slab_exchange_transposes_rows_to_strips():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(out.values())
