@@ -119,6 +119,7 @@ typedef struct {
 #define P2S_FORCE_NO_WARP_FUSION  0x100u /* step 2 as its own kernel, not in the column pass   */
 #define P2S_FORCE_BLUR_SINGLE     0x200u /* blur on single CTAs (cta_group::1), not CTA pairs  */
 #define P2S_FORCE_COLS_PERSISTENT 0x400u /* long columns: persistent one-CTA-per-SM kernel     */
+#define P2S_FORCE_WARP_GATHER     0x800u /* step 2 gathering from global memory, no TMA window  */
 
 /* Build a plan (P:312-330 generation setup; runs once, off the per-frame clock).
  *   H, W        image size in pixels (>= T, <= 8192)

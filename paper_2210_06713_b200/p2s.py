@@ -55,6 +55,7 @@ FORCE_X_TILES = 0x080
 FORCE_NO_WARP_FUSION = 0x100
 FORCE_BLUR_SINGLE = 0x200
 FORCE_COLS_PERSISTENT = 0x400
+FORCE_WARP_GATHER = 0x800
 
 
 def _load():

@@ -235,3 +235,23 @@ def test_row_length_without_a_fitting_kernel_is_unsupported():
     with pytest.raises(P2SError) as e:
         Plan(PlanConfig(H=20, W=4050, C=1, d_over_r0=1.0, K=16, taps=17), synth.basis(16, 17), synth.mlp_weights(16))
     assert e.value.status == 5  # P2S_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("H,W,C,img_frames", [(1080, 1920, 3, 1), (200, 328, 2, 3)])
+def test_tma_window_warp_matches_gather_warp(H, W, C, img_frames):
+    """Step 2 with the TMA-staged image window (default at long columns) against the plain
+    gather kernel (P2S_FORCE_WARP_GATHER): the same arithmetic on the same values, so the
+    frames are bit-identical -- broadcast image and per-frame images."""
+    from paper_2210_06713_b200 import FORCE_WARP_GATHER
+    imgs = np.stack([synth.image(H, W, C, seed=s) for s in range(img_frames)])
+    img = torch.from_numpy(imgs if img_frames > 1 else imgs[0]).cuda()
+    stride = C * H * W if img_frames > 1 else 0
+    F = img_frames if img_frames > 1 else 2
+    outs = []
+    for force in (0, FORCE_WARP_GATHER):
+        plan, *_ = plan_for(H, W, C, 5.0, K=16, T=17, max_batch=F, force=force)
+        o = torch.empty((F, C, H, W), device="cuda")
+        plan.simulate_frames(img, stride, SEED, 4, F, o)
+        torch.cuda.synchronize()
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1])
