@@ -401,6 +401,7 @@ static void free_plan(p2s_plan_s* p) {
     cudaEventDestroy(p->ev_sub);
     cudaEventDestroy(p->ev_copied);
     cudaEventDestroy(p->ev_img);
+    cudaEventDestroy(p->ev_half);
   }
   cudaFree(p->d_ztab);
   cudaFree(p->bg.koff);
@@ -828,16 +829,22 @@ extern "C" p2s_status p2s_blur_weights(p2s_plan p, const float* warped, const fl
   return P2S_OK;
 }
 
-// Steps 1-5; img_ready (nullable): an event the image upload records -- step 1's row pass
-// does not read the image, so the upload overlaps it and only the column/warp stage waits.
+// Steps 1-5; img_ready (nullable): an event the image upload records -- step 1 does not
+// read the image, so the upload overlaps the row pass and (when step 2 is its own kernel)
+// the column pass too; only the stage that reads the image waits.  half_done (nullable,
+// one-frame calls): the blur runs as two launches over the top and bottom halves of the
+// row bands and half_done is recorded between them, so the caller can copy rows
+// [0, *split_row) out while the bottom half is computed.
 static p2s_status simulate_impl(p2s_plan_s* p, const float* img, int64_t img_frame_stride, uint64_t seed,
-                                int64_t frame0, int nframes, float* out, cudaStream_t s, cudaEvent_t img_ready) {
+                                int64_t frame0, int nframes, float* out, cudaStream_t s, cudaEvent_t img_ready,
+                                cudaEvent_t half_done = nullptr, int* split_row = nullptr) {
   const size_t HW = (size_t)p->H * p->W;
+  const bool fused = cols_fuse_warp(p);
   for (int i0 = 0; i0 < nframes; i0 += p->max_batch) {
     const int F = std::min(p->max_batch, nframes - i0);
     p2s_status st = run_step1(p, seed, frame0 + i0, F, s);
     if (st != P2S_OK) return st;
-    if (img_ready) P2S_CUDA(cudaStreamWaitEvent(s, img_ready, 0), "wait image upload");
+    if (img_ready && fused) P2S_CUDA(cudaStreamWaitEvent(s, img_ready, 0), "wait image upload");
     bool warp_fused = false;  // 512-point columns: step 2 runs inside the column kernel
     {
       StageScope sc(p, 1, s);
@@ -845,6 +852,7 @@ static p2s_status simulate_impl(p2s_plan_s* p, const float* img, int64_t img_fra
                  "k_cols");
     }
     if (!warp_fused) {
+      if (img_ready && !fused) P2S_CUDA(cudaStreamWaitEvent(s, img_ready, 0), "wait image upload");
       StageScope sc(p, 2, s);
       P2S_LAUNCH(launch_warp_sim(p, F, img + (size_t)i0 * img_frame_stride, img_frame_stride, s), "k_warp");
     }
@@ -852,9 +860,23 @@ static p2s_status simulate_impl(p2s_plan_s* p, const float* img, int64_t img_fra
       StageScope sc(p, 3, s);
       P2S_LAUNCH(launch_mlp(p, F, true, s), "k_mlp");
     }
-    {
+    float* o = out + (size_t)i0 * p->C * HW;
+    const int bands = (p->H + p->bg.RB - 1) / p->bg.RB;
+    if (half_done && F == 1 && nframes == 1 && bands >= 2) {
+      const int b1 = bands / 2;
+      {
+        StageScope sc(p, 4, s);
+        P2S_LAUNCH(launch_blur(p, F, p->d_Iw, false, seed, frame0 + i0, o, s, 0, b1), "k_blur (top)");
+      }
+      P2S_CUDA(cudaEventRecord(half_done, s), "event record");
+      {
+        StageScope sc(p, 4, s);
+        P2S_LAUNCH(launch_blur(p, F, p->d_Iw, false, seed, frame0 + i0, o, s, b1, bands - b1), "k_blur (bottom)");
+      }
+      if (split_row) *split_row = b1 * p->bg.RB;
+    } else {
       StageScope sc(p, 4, s);
-      P2S_LAUNCH(launch_blur(p, F, p->d_Iw, false, seed, frame0 + i0, out + (size_t)i0 * p->C * HW, s), "k_blur");
+      P2S_LAUNCH(launch_blur(p, F, p->d_Iw, false, seed, frame0 + i0, o, s), "k_blur");
     }
   }
   return P2S_OK;
@@ -945,6 +967,7 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
     P2S_CUDA(cudaEventCreateWithFlags(&p->ev_sub, cudaEventDisableTiming), "cudaEventCreate");
     P2S_CUDA(cudaEventCreateWithFlags(&p->ev_copied, cudaEventDisableTiming), "cudaEventCreate");
     P2S_CUDA(cudaEventCreateWithFlags(&p->ev_img, cudaEventDisableTiming), "cudaEventCreate");
+    P2S_CUDA(cudaEventCreateWithFlags(&p->ev_half, cudaEventDisableTiming), "cudaEventCreate");
   }
   // The device->host copy of each sub-batch runs on a second stream while the next
   // sub-batch computes, so the PCIe transfer of the outputs hides behind the kernels; the
@@ -968,16 +991,39 @@ extern "C" p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host
     }
     P2S_CUDA(cudaEventRecord(p->ev_img, p->copy_stream), "event record");
     int j0 = 0;
-    for (const int Fs : subs) {
+    for (size_t si = 0; si < subs.size(); ++si) {
+      const int Fs = subs[si];
+      // the exposed copy tail: a one-frame last sub-batch runs its blur as two halves and
+      // its top rows leave while the bottom half is computed (4K: half of a 100 MB copy)
+      const bool split = si + 1 == subs.size() && i0 + F == nframes && Fs == 1 && p->H >= 256;
+      int ysplit = 0;
       p2s_status st = simulate_impl(p, p->d_img + (img_frame_stride ? (size_t)j0 * img_floats : 0),
                                     img_frame_stride ? (int64_t)img_floats : 0, seed, frame0 + i0 + j0, Fs,
-                                    p->d_out + (size_t)j0 * img_floats, s, p->ev_img);
+                                    p->d_out + (size_t)j0 * img_floats, s, p->ev_img, split ? p->ev_half : nullptr,
+                                    split ? &ysplit : nullptr);
       if (st != P2S_OK) return st;
+      const size_t plane = (size_t)p->H * p->W;
+      if (split && ysplit > 0) {
+        P2S_CUDA(cudaStreamWaitEvent(p->copy_stream, p->ev_half, 0), "wait top half");
+        for (int c = 0; c < p->C; ++c)
+          P2S_CUDA(cudaMemcpyAsync(out_host + (size_t)(i0 + j0) * img_floats + c * plane,
+                                   p->d_out + (size_t)j0 * img_floats + c * plane, (size_t)ysplit * p->W * 4,
+                                   cudaMemcpyDeviceToHost, p->copy_stream),
+                   "D2H out (top)");
+      }
       P2S_CUDA(cudaEventRecord(p->ev_sub, s), "event record");
       P2S_CUDA(cudaStreamWaitEvent(p->copy_stream, p->ev_sub, 0), "wait sub-batch");
-      P2S_CUDA(cudaMemcpyAsync(out_host + (size_t)(i0 + j0) * img_floats, p->d_out + (size_t)j0 * img_floats,
-                               (size_t)Fs * img_floats * 4, cudaMemcpyDeviceToHost, p->copy_stream),
-               "D2H out");
+      if (split && ysplit > 0) {
+        for (int c = 0; c < p->C; ++c)
+          P2S_CUDA(cudaMemcpyAsync(out_host + (size_t)(i0 + j0) * img_floats + c * plane + (size_t)ysplit * p->W,
+                                   p->d_out + (size_t)j0 * img_floats + c * plane + (size_t)ysplit * p->W,
+                                   (plane - (size_t)ysplit * p->W) * 4, cudaMemcpyDeviceToHost, p->copy_stream),
+                   "D2H out (bottom)");
+      } else {
+        P2S_CUDA(cudaMemcpyAsync(out_host + (size_t)(i0 + j0) * img_floats, p->d_out + (size_t)j0 * img_floats,
+                                 (size_t)Fs * img_floats * 4, cudaMemcpyDeviceToHost, p->copy_stream),
+                 "D2H out");
+      }
       j0 += Fs;
     }
     P2S_CUDA(cudaEventRecord(p->ev_copied, p->copy_stream), "event record");

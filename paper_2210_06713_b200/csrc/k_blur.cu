@@ -58,6 +58,7 @@ struct BlurArgs {
   float sigma;
   int normalize, clamp01;
   int noise_x0, noise_W;    // step-5 noise counter y * noise_W + noise_x0 + x (slab strips: frame coordinates)
+  int band0;                // first row band of the launch (a frame's blur split in two launches)
   unsigned long long* probe;  // optional [8] cycle counters (P2S_BLUR_PROBE), else null
   int brep, brows;            // B image copies; rows between copies (pair mode tensor map)
   size_t bstride;             // bytes between copies (bulk path)
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
 
-  const int x0 = blockIdx.x * 128, y0 = blockIdx.y * a.RB, f = blockIdx.z;
+  const int x0 = blockIdx.x * 128, y0 = (a.band0 + (int)blockIdx.y) * a.RB, f = blockIdx.z;
   const int HW = a.H * a.W;
   const uint32_t s_tile = smem_u32(smem);
   const uint64_t t_start = clk();
@@ -563,7 +564,7 @@ static int launch_blur_c(int C, const BlurArgs& a, const CUtensorMap& tb, dim3 g
 }
 
 int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0, float* out,
-                cudaStream_t s) {
+                cudaStream_t s, int band0, int nbands) {
   const BlurGeom& g = p->bg;
   BlurArgs a;
   a.src = src;
@@ -620,7 +621,11 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   size_t sm = L.total < 116 * 1024 ? 116 * 1024 : L.total;
   int gx = p->ntx;
   if (pair) gx = (gx + 1) / 2 * 2;  // whole CTA pairs; a trailing dummy CTA stores nothing
-  dim3 grid(gx, (p->H + g.RB - 1) / g.RB, F);
+  const int bands = (p->H + g.RB - 1) / g.RB;
+  a.band0 = std::max(0, std::min(band0, bands));
+  const int nb = nbands < 0 ? bands - a.band0 : std::min(nbands, bands - a.band0);
+  if (nb <= 0) return 0;
+  dim3 grid(gx, nb, F);
   int rc;
   if (pair)
     rc = src_f32 ? launch_blur_c<true, true>(p->C, a, p->tmap_b, grid, sm, s)

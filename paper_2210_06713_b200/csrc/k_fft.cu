@@ -1539,7 +1539,7 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
   a.fuse_warp = 0;
   if (warp_fused) *warp_fused = false;
   if (reg512(pl->fp) && !(pl->force & P2S_FORCE_FFT_GENERIC)) {
-    if (mode == 1 && img && warp_fused && !(pl->force & P2S_FORCE_NO_WARP_FUSION)) {
+    if (mode == 1 && img && warp_fused && cols_fuse_warp(pl)) {
       const int Z = pl->Z;
       a.fuse_warp = 1;
       a.img = img;
@@ -1662,6 +1662,11 @@ int launch_cols(const p2s_plan_s* pl, int F, int mode, float* zern, cudaStream_t
     k_cols<1, 256><<<grid, 256, sm, s>>>(a);
   }
   return (int)cudaGetLastError();
+}
+
+bool cols_fuse_warp(const p2s_plan_s* pl) {
+  return reg512(pl->fp) && !(pl->force & P2S_FORCE_FFT_GENERIC) && !(pl->force & P2S_FORCE_NO_WARP_FUSION) &&
+         pl->slab_G < 2;
 }
 
 // ------------------------------------------------------------------ K3: Noll mixing a = L f

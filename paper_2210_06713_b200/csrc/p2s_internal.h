@@ -162,7 +162,7 @@ struct p2s_plan_s {
   std::vector<int> t_stage;
   std::vector<cudaEvent_t> t_ev;  // pairs
   cudaStream_t copy_stream = nullptr;  // host entry: device->host copies overlapped with compute
-  cudaEvent_t ev_sub = nullptr, ev_copied = nullptr, ev_img = nullptr;
+  cudaEvent_t ev_sub = nullptr, ev_copied = nullptr, ev_img = nullptr, ev_half = nullptr;
   // AR bookkeeping
   bool ar_valid = false;
   uint64_t ar_seed = 0;
@@ -200,7 +200,8 @@ size_t rows_smem_bytes(const p2s_plan_s* p, bool ar, bool given_noise);  // row 
 int x_tile_layout(const p2s_plan_s* p);  // decided at plan creation; 1: MLP input X tile-major (x_index)
 int launch_pack_weights(const p2s_plan_s* p, int F, const float* wts, cudaStream_t s);
 int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint64_t seed, int64_t frame0,
-                float* out, cudaStream_t s);
+                float* out, cudaStream_t s, int band0 = 0, int nbands = -1);  // row bands [band0, band0 + nbands)
+bool cols_fuse_warp(const p2s_plan_s* p);  // step 2 runs inside the simulate path's column kernel
 int blur_rows_per_cta(int C, int T, int np, int racc, int H, int W, bool pair, int stages, int F, int nsm);
 int blur_waves(const p2s_plan_s* p, int F);
 size_t acorr_partial_bytes(int F, int Z, int W, int L);

@@ -155,3 +155,19 @@ def test_per_frame_images_stride():
     plan.simulate_frames(d[2], 0, SEED, 2, 1, one)
     torch.cuda.synchronize()
     assert torch.equal(out[2], one[0])
+
+
+@pytest.mark.parametrize("H,W,F,max_batch", [(512, 512, 3, 0), (1080, 1920, 2, 2), (2160, 3840, 1, 1)])
+def test_host_entry_split_tail_bit_identical(H, W, F, max_batch):
+    """p2s_simulate_frames_host at BASELINE geometries: a one-frame last sub-batch runs its
+    blur as two row-band halves (the top half's device->host copy overlaps the bottom half);
+    the host output equals the device entry point's bit for bit."""
+    plan, *_ = _plan(H, W, 3, 4.0, 100, 33, max_batch=max_batch)
+    img = synth.image(H, W, 3, seed=6)
+    dev = torch.empty((F, 3, H, W), device="cuda")
+    plan.simulate_frames(torch.from_numpy(img).cuda(), 0, SEED, 40, F, dev)
+    torch.cuda.synchronize()
+    img_h = torch.from_numpy(img).pin_memory().numpy()
+    out_h = torch.full((F, 3, H, W), float("nan")).pin_memory().numpy()
+    plan.simulate_frames_host(img_h, 0, SEED, 40, F, out_h)
+    assert np.array_equal(out_h, dev.cpu().numpy())
