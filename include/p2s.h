@@ -98,7 +98,7 @@ typedef struct {
                               * Exclusive with ar_alpha.  Default (0, 0). */
   int    slab_count;        /* G >= 2: the plan is rank slab_rank's share of ONE frame sharded
                                over G ranks (single-frame latency mode; see
-                               p2s_slab_*).  0 or 1: a normal plan.  White noise only. */
+                               p2s_slab_*).  0 or 1: a normal plan. */
   int    slab_rank;         /* 0 <= slab_rank < slab_count */
   unsigned int force;       /* kernel-selection overrides, P2S_FORCE_* bits; 0 = the production
                                dispatch.  For parity tests that pin one kernel variant against
@@ -354,7 +354,9 @@ int p2s_grid_size(int x);
  * bit-identical to p2s_simulate_frames of the unsharded frame (same kernels, same
  * per-pixel and per-bin arithmetic; the halo makes the mirror boundary exact).
  * The plan is created with opt->slab_count = G >= 2, opt->slab_rank = r and the GLOBAL
- * H, W; max_batch is 1.  ar_alpha and frozen flow must be 0.
+ * H, W; max_batch is 1.  White noise, frozen flow and AR(1) sequences (each rank keeps
+ * the AR state of its own spectral rows; a frame that does not continue the rank's previous
+ * call is replayed from frame 0, as in p2s_sample_zernike).
  *
  * Exchange buffers (dev float, complex values as interleaved pairs):
  *   send [G dest][rows_r][npairs][Ws(dest)] x 2 floats, recv [G src][rows_src][npairs][Ws(r)]

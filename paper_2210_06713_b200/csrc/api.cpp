@@ -584,8 +584,6 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
     const int G = o.slab_count, r = o.slab_rank;
     if (r < 0 || r >= G || G > 64)
       return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "slab_rank must be in [0, slab_count), slab_count <= 64");
-    if (o.ar_alpha != 0.f || o.flow_px_per_frame[0] != 0.f || o.flow_px_per_frame[1] != 0.f)
-      return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "slab mode samples white-noise frames only");
     const SlabGeom g = slab_geometry(W, T, p->P, G, r);
     for (int d = 0; d < G; ++d) {
       const SlabGeom gd = slab_geometry(W, T, p->P, G, d);
@@ -1177,9 +1175,12 @@ extern "C" p2s_status p2s_slab_rows(p2s_plan p, uint64_t seed, int64_t frame, fl
   if (!send) return set_error(P2S_ERR_INVALID_ARGUMENT, "send is NULL");
   DeviceGuard guard(p->device);
   cudaStream_t s = (cudaStream_t)stream;
+  // row pass of this rank's pairs: white noise, frozen flow or AR(1) (the rank keeps the
+  // state of its own rows; a frame that does not continue the previous call replays)
+  p2s_status st = run_step1(p, seed, frame, 1, s);
+  if (st != P2S_OK) return st;
   {
     StageScope sc(p, 0, s);
-    P2S_LAUNCH(launch_rows(p, seed, frame, 1, false, 1, frame, s), "k_rows (slab)");
     P2S_LAUNCH(launch_slab_pack(p, reinterpret_cast<float2*>(send), s), "k_slab_pack");
   }
   return P2S_OK;

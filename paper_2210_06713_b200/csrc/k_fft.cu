@@ -914,7 +914,11 @@ static RowVariant rows_variant(const p2s_plan_s* pl, bool ar, bool given, size_t
   for (int i = 0; i < pl->fq.nrad; ++i) one = one && (Q / pl->fq.rad[i]) * 2 <= 512;
   if (ar) {
     // 1: always k_rows_ar, 2: the 256/512-thread pair kernel (P2S_FORCE_AR_*)
-    const int ar_rows = (pl->force & P2S_FORCE_AR_ROW_KERNEL) ? 1 : (pl->force & P2S_FORCE_AR_PAIR_KERNEL) ? 2 : 0;
+    int ar_rows = (pl->force & P2S_FORCE_AR_ROW_KERNEL) ? 1 : (pl->force & P2S_FORCE_AR_PAIR_KERNEL) ? 2 : 0;
+    // slab mode: the row-pair kernels transform only this rank's pairs; the one-CTA-per-row
+    // kernel (still correct: every row, of which the pack takes this rank's) only if no
+    // pair kernel fits
+    if (pl->slab_G > 1 && ar_rows == 0 && Q > 512) ar_rows = 2;
     if (ar_rows == 0 && Q <= 512) {
       // short rows: 128-thread row-pair CTAs keep the grid's CTA count up where each CTA
       // runs a long frame sequence (cfg2, Q = 256, 100 frames: 1.57 -> 1.38 ms vs k_rows_ar;
@@ -977,8 +981,8 @@ size_t rows_smem_bytes(const p2s_plan_s* pl, bool ar, bool given_noise) {
 }
 
 template <int NT, int MB, int QN = 0, int R1 = 1, int R2 = 1, int R3 = 1>
-static int launch_rows_ar_pair(const RowArgs& a, int P, int npairs, size_t sm, cudaStream_t s) {
-  dim3 grid(P / 2 + 1, npairs);
+static int launch_rows_ar_pair(const RowArgs& a, int npr, int npairs, size_t sm, cudaStream_t s) {
+  dim3 grid(npr, npairs);  // Hermitian row pairs [a.ky0, a.ky0 + npr)
   P2S_SMEM_OPTIN((k_rows_ar_pair<NT, MB, QN, R1, R2, R3>), sm);
   k_rows_ar_pair<NT, MB, QN, R1, R2, R3><<<grid, NT, sm, s>>>(a);
   return (int)cudaGetLastError();
@@ -1021,19 +1025,21 @@ int launch_rows(const p2s_plan_s* pl, uint64_t seed, int64_t frame0, int F, bool
       P2S_SMEM_OPTIN((k_rows_pair<256, true>), sm);
       k_rows_pair<256, true><<<gpair, 256, sm, s>>>(a);
       break;
-    case RV_AR_PAIR_128: return launch_rows_ar_pair<128, 4>(a, pl->P, pl->npairs, sm, s);
-    case RV_AR_PAIR_256_1: return launch_rows_ar_pair<256, 1>(a, pl->P, pl->npairs, sm, s);
-    case RV_AR_PAIR_256_2: return launch_rows_ar_pair<256, 2>(a, pl->P, pl->npairs, sm, s);
-    case RV_AR_PAIR_256_4: return launch_rows_ar_pair<256, 4>(a, pl->P, pl->npairs, sm, s);
-    case RV_AR_PAIR_512_4: return launch_rows_ar_pair<512, 4>(a, pl->P, pl->npairs, sm, s);
-    case RV_AR_PAIR_512_8: return launch_rows_ar_pair<512, 8>(a, pl->P, pl->npairs, sm, s);
-    case RV_AR_PAIR_3840: return launch_rows_ar_pair<512, 8, 3840, 16, 16, 15>(a, pl->P, pl->npairs, sm, s);
-    case RV_AR_PAIR_1920: return launch_rows_ar_pair<512, 4, 1920, 16, 15, 8>(a, pl->P, pl->npairs, sm, s);
+    case RV_AR_PAIR_128: return launch_rows_ar_pair<128, 4>(a, npr, pl->npairs, sm, s);
+    case RV_AR_PAIR_256_1: return launch_rows_ar_pair<256, 1>(a, npr, pl->npairs, sm, s);
+    case RV_AR_PAIR_256_2: return launch_rows_ar_pair<256, 2>(a, npr, pl->npairs, sm, s);
+    case RV_AR_PAIR_256_4: return launch_rows_ar_pair<256, 4>(a, npr, pl->npairs, sm, s);
+    case RV_AR_PAIR_512_4: return launch_rows_ar_pair<512, 4>(a, npr, pl->npairs, sm, s);
+    case RV_AR_PAIR_512_8: return launch_rows_ar_pair<512, 8>(a, npr, pl->npairs, sm, s);
+    case RV_AR_PAIR_3840: return launch_rows_ar_pair<512, 8, 3840, 16, 16, 15>(a, npr, pl->npairs, sm, s);
+    case RV_AR_PAIR_1920: return launch_rows_ar_pair<512, 4, 1920, 16, 15, 8>(a, npr, pl->npairs, sm, s);
     case RV_AR_ROW_512:
+      a.ky0 = 0;  // one CTA per row over all P rows (slab mode: the pack takes this rank's)
       P2S_SMEM_OPTIN(k_rows_ar<512>, sm);
       k_rows_ar<512><<<grow, 512, sm, s>>>(a);
       break;
     case RV_AR_ROW_128:
+      a.ky0 = 0;
       P2S_SMEM_OPTIN(k_rows_ar<128>, sm);
       k_rows_ar<128><<<grow, 128, sm, s>>>(a);
       break;
