@@ -334,7 +334,7 @@ static size_t frame_bytes(const p2s_plan_s* p) {
   const size_t HW = (size_t)p->H * p->W, PQ = (size_t)p->P * p->Q;
   size_t b = 0;
   b += PQ * p->npairs * sizeof(float2);
-  b += (size_t)p->H * ((p->W + 127) / 128) * 128 * (size_t)std::max(p->nslots, p->Z - 3) * 2;
+  b += (size_t)p->H * ((p->W + 127) / 128) * 128 * (size_t)((std::max(p->nslots, p->Z - 3) + 1) & ~1) * 2;
   b += 2 * HW * 4;
   b += (size_t)p->C * HW * 2;
   b += (size_t)p->H * ((p->W + 127) / 128) * 128 * (size_t)p->mg_fold.n3 * 2;
@@ -354,7 +354,7 @@ static p2s_status alloc_workspace(p2s_plan_s* p) {
   };
   p->d_Z = reinterpret_cast<float2*>(take(mb * PQ * p->npairs * sizeof(float2)));
   p->d_X = reinterpret_cast<uint16_t*>(
-      take(mb * (size_t)p->H * ((p->W + 127) / 128) * 128 * (size_t)std::max(p->nslots, p->Z - 3) * 2));
+      take(mb * (size_t)p->H * ((p->W + 127) / 128) * 128 * (size_t)((std::max(p->nslots, p->Z - 3) + 1) & ~1) * 2));
   p->d_tilt = reinterpret_cast<float*>(take(mb * 2 * HW * 4));
   p->d_Iw = reinterpret_cast<uint16_t*>(take(mb * (size_t)p->C * HW * 2));
   p->ntx = (p->W + 127) / 128;
@@ -569,8 +569,8 @@ extern "C" p2s_status p2s_plan_create(p2s_plan* out, int H, int W, int C, double
   p->clamp01 = o.clamp01;
   p->device = dev;
   p->force = o.force;
-  if ((o.force & P2S_FORCE_X_PLANES) && (o.force & P2S_FORCE_X_TILES))
-    return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "P2S_FORCE_X_PLANES and _X_TILES are exclusive");
+  if (__builtin_popcount(o.force & (P2S_FORCE_X_PLANES | P2S_FORCE_X_TILES | P2S_FORCE_X_OCTETS)) > 1)
+    return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "P2S_FORCE_X_PLANES, _X_TILES and _X_OCTETS are exclusive");
   if ((o.force & P2S_FORCE_AR_ROW_KERNEL) && (o.force & P2S_FORCE_AR_PAIR_KERNEL))
     return delete p, set_error(P2S_ERR_INVALID_ARGUMENT, "P2S_FORCE_AR_ROW_KERNEL and _AR_PAIR_KERNEL are exclusive");
   p->P = grid_size(pad * H);

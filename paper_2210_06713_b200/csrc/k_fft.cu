@@ -869,14 +869,17 @@ static bool reg512(const AxisFFT& ax) {
 }
 
 // MLP input layout shared by its producers (k_cols*, k_zern_to_x) and k_mlp, decided once
-// at plan creation (p2s_plan_s::xtile).  Tile-major where the planes are far apart
-// (H W >= 4M pixels: 4K k_mlp 2.05 -> 1.36 ms, its 35 per-tile plane segments were 16.6 MB
-// apart); planes elsewhere (512^2: the column kernel's stores are 0.1 ms faster into planes,
-// k_mlp unchanged; 1080p: neutral).  P2S_FORCE_X_PLANES / _X_TILES force either.
+// at plan creation (p2s_plan_s::xtile).  Octet-pair tiles (x_index, xtile 2) from 2M pixels
+// per frame (1080p, 4K): k_mlp 1.38 -> 1.33 ms per launch at both (contiguous 9 KB tile
+// blocks, r1 measured 2.05 -> 1.36 at 4K for the tile-major layout against planes), the
+// long-column kernel's stores unchanged; planes at 512^2, where k_cols512 writes one column
+// per thread and the tiled addressing cost it 0.13 ms (k_mlp -0.05).  P2S_FORCE_X_PLANES /
+// _X_TILES / _X_OCTETS force a layout.
 int x_tile_layout(const p2s_plan_s* pl) {
   if (pl->force & P2S_FORCE_X_PLANES) return 0;
   if (pl->force & P2S_FORCE_X_TILES) return 1;
-  return (size_t)pl->H * pl->W >= ((size_t)4 << 20) ? 1 : 0;
+  if (pl->force & P2S_FORCE_X_OCTETS) return 2;
+  return (size_t)pl->H * pl->W >= ((size_t)2 << 20) ? 2 : 0;
 }
 
 // Row-pass kernel variants (one per dispatch outcome of rows_variant).
@@ -1161,9 +1164,9 @@ __global__ void __launch_bounds__(NT) k_cols(ColArgs a) {
       if (sb < a.nslots) z[(size_t)(sb + 1) * HW + pix] = v.y;
     } else {
       if (a.xtile) {  // tile-major (x_index); the plane path below keeps its cheaper addressing
-        uint16_t* Xt = a.X + x_index(1, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x);
+        uint16_t* Xt = a.X + x_index(a.xtile, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x);
         Xt[0] = f_to_bf16(v.x);
-        if (sb < a.nslots) Xt[128] = f_to_bf16(v.y);
+        if (sb < a.nslots) Xt[a.xtile == 2 ? 8 : 128] = f_to_bf16(v.y);
       } else {
         uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
         Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
@@ -1283,7 +1286,7 @@ __global__ void __launch_bounds__(NT, NT <= 512 ? 2 : 1) k_cols_ip(ColArgs a) {
     } else {
       uint16_t* Xa = a.X + x_index(a.xtile, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x0);
       // the second mode of the pair: the next plane (planes) or the next 128-pixel row of the tile
-      const size_t db = a.xtile ? 128 : HW;
+      const size_t db = a.xtile == 2 ? 8 : a.xtile ? 128 : HW;
       const bool hb = sb < a.nslots;
       if (vec) {
         uint32_t ua[TC / 2], ub[TC / 2];
@@ -1385,9 +1388,9 @@ __global__ void __launch_bounds__(NT) k_cols_p(ColArgs a) {
         if (sb < a.nslots) z[(size_t)(sb + 1) * HW + pix] = v.y;
       } else {
         if (a.xtile) {  // tile-major (x_index)
-          uint16_t* Xt = a.X + x_index(1, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x);
+          uint16_t* Xt = a.X + x_index(a.xtile, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x);
           Xt[0] = f_to_bf16(v.x);
-          if (sb < a.nslots) Xt[128] = f_to_bf16(v.y);
+          if (sb < a.nslots) Xt[a.xtile == 2 ? 8 : 128] = f_to_bf16(v.y);
         } else {
           uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
           Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);
@@ -1472,9 +1475,9 @@ __global__ void __launch_bounds__(512) k_cols512(ColArgs a) {
       if (sb < a.nslots) z[(size_t)(sb + 1) * HW + pix] = v.y;
     } else {
       if (a.xtile) {  // tile-major (x_index); the plane path below keeps its cheaper addressing
-        uint16_t* Xt = a.X + x_index(1, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x);
+        uint16_t* Xt = a.X + x_index(a.xtile, f, sa, a.nslots, a.H, a.W, a.ntx, yy, x);
         Xt[0] = f_to_bf16(v.x);
-        if (sb < a.nslots) Xt[128] = f_to_bf16(v.y);
+        if (sb < a.nslots) Xt[a.xtile == 2 ? 8 : 128] = f_to_bf16(v.y);
       } else {
         uint16_t* Xo = a.X + (size_t)f * a.nslots * HW;
         Xo[(size_t)sa * HW + pix] = f_to_bf16(v.x);

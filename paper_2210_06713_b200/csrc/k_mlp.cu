@@ -92,12 +92,16 @@ __device__ __forceinline__ void wg_sync(int wg) {  // named barrier of one 128-t
 __device__ __forceinline__ void load_a1(const MlpArgs& a, uint8_t* A1, int tile, int f, int pix0, int n, int ltid,
                                         bool async) {
   const uint16_t* Xf = a.X + (size_t)f * a.nin * a.HW;
-  const uint16_t* Xt = a.X + (size_t)tile * 128 * a.nin;  // tile-major: this tile's block
+  const int nin2 = a.xtile == 2 ? (a.nin + 1) & ~1 : a.nin;
+  const uint16_t* Xt = a.X + (size_t)tile * 128 * nin2;  // tile-major: this tile's block
   for (int idx = ltid; idx < a.nin * 16; idx += 128) {
     const int k = idx % a.nin, g = idx / a.nin;
     const int o = 8 * g;
-    // tile-major: plane k of this tile at k * 128 elements of its contiguous block
-    const uint16_t* src = a.xtile ? Xt + (size_t)k * 128 + o : Xf + (size_t)k * a.HW + pix0 + o;
+    // tile-major: plane k of this tile at k * 128 elements of its contiguous block; octet-pair
+    // layout (xtile 2): the chunk of mode k, octet g at ((k/2) 16 + g) 16 + (k%2) 8
+    const uint16_t* src = a.xtile == 2 ? Xt + (size_t)(((k >> 1) * 16 + g) * 16 + (k & 1) * 8)
+                        : a.xtile     ? Xt + (size_t)k * 128 + o
+                                      : Xf + (size_t)k * a.HW + pix0 + o;
     uint8_t* dst = A1 + g * (a.k1 * 16) + k * 16;
     if (async) {  // W % 8 == 0: whole 16-byte chunks, zero-filled past the row segment
       cp_async16(dst, o < n ? src : a.X, o < n ? 16u : 0u);

@@ -58,9 +58,18 @@ __device__ __forceinline__ float2 box_muller_fast(uint32_t a, uint32_t b) {
 // tile's inputs are one contiguous 256*nin-byte block, so k_mlp's 16-byte chunk loads stay
 // within a few pages; consecutive pixels stay adjacent, so the column kernels' stores keep
 // their full-sector runs); xtile = 0 -> planes [F][nin][H][W].
+// xtile = 2 -> per 128-pixel row tile, [F][H][ntx][nin/2 mode pairs][16 octets][2 modes][8 px]
+// (nin rounded up to even): the two modes of a pair for 8 adjacent pixels are one 32-byte
+// sector, so a long-column CTA writes a row of its block as one full-sector store, and each
+// (mode, octet) is still the 16-byte chunk of 8 pixels the MLP's A operand loads.
 __device__ __forceinline__ size_t x_index(int xtile, int f, int k, int nin, int H, int W, int ntx, int y, int x) {
   if (!xtile) return ((size_t)f * nin + k) * (size_t)H * W + (size_t)y * W + x;
   const int xt = x >> 7, px = x & 127;
+  if (xtile == 2) {
+    const int nin2 = (nin + 1) & ~1;
+    return (((size_t)f * H + y) * ntx + xt) * (size_t)(nin2 * 128) + (size_t)(((k >> 1) * 16 + (px >> 3)) * 16 +
+                                                                             (k & 1) * 8 + (px & 7));
+  }
   return ((((size_t)f * H + y) * ntx + xt) * nin + k) * 128 + px;
 }
 

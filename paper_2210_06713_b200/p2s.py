@@ -56,6 +56,7 @@ FORCE_NO_WARP_FUSION = 0x100
 FORCE_BLUR_SINGLE = 0x200
 FORCE_COLS_PERSISTENT = 0x400
 FORCE_WARP_GATHER = 0x800
+FORCE_X_OCTETS = 0x1000
 
 
 def _load():

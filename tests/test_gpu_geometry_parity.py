@@ -1,7 +1,7 @@
 """GPU parity against the fp64 oracle at BASELINE.json's own geometries and edge cases.
 
 * cfg5 (2160 x 3840 RGB, D/r0 = 5, K = 100, T = 33): the 4K kernels (rows 3840 = 16·16·15
-  in place, columns 2160 = 16·15·9 persistent, tile-major MLP inputs) against
+  in place, columns 2160 = 16·15·9 in place, octet-pair MLP inputs) against
   `pipeline.sample_zernike` on all 35 mode planes of a frame, and steps 1-5 on sampled
   pixels (corners and edges included) against Eq.9 evaluated pixel by pixel.
 * cfg4 / cfg5 as AR(0.95) sequences (reading Q18): fresh start, stored-state
@@ -111,7 +111,7 @@ def test_4k_fields_all_planes_and_sampled_output_vs_oracle():
 
 
 def test_4k_mlp_input_layouts_bit_identical():
-    """cfg5's default tile-major MLP inputs against the plane layout (P2S_FORCE_X_PLANES):
+    """cfg5's default octet-pair MLP inputs against the plane layout (P2S_FORCE_X_PLANES):
     the same values in another order, so the simulated frames are bit-identical."""
     from paper_2210_06713_b200 import FORCE_X_PLANES
     H, W, C = 2160, 3840, 3
@@ -152,30 +152,31 @@ def test_ar_long_rows_vs_oracle(H, W, dr0, force):
 
 # ------------------------------------------------------------------ MLP input layouts
 def test_1080p_mlp_input_layouts_bit_identical():
-    """k_cols_p writing tile-major MLP inputs (P2S_FORCE_X_TILES) against its default plane
-    layout at 1080p: bit-identical frames."""
-    from paper_2210_06713_b200 import FORCE_X_TILES
+    """The long-column kernel writing its default octet-pair MLP inputs, tile-major
+    (P2S_FORCE_X_TILES) and planes (P2S_FORCE_X_PLANES) at 1080p: bit-identical frames."""
+    from paper_2210_06713_b200 import FORCE_X_PLANES, FORCE_X_TILES
     H, W, C = 1080, 1920, 3
     img = torch.from_numpy(synth.image(H, W, C, seed=2)).cuda()
     outs = []
-    for force in (0, FORCE_X_TILES):
+    for force in (0, FORCE_X_TILES, FORCE_X_PLANES):
         plan, *_ = plan_for(H, W, C, 4.0, max_batch=3, force=force)
         o = torch.empty((3, C, H, W), device="cuda")
         plan.simulate_frames(img, 0, SEED, 0, 3, o)
         torch.cuda.synchronize()
         outs.append(o)
-    assert torch.equal(outs[0], outs[1])
+    for o in outs[1:]:
+        assert torch.equal(outs[0], o)
 
 
-def test_512_rgb_tile_layout_fused_warp_vs_oracle():
-    """512^2 RGB with tile-major MLP inputs forced: k_cols512 runs its fused warp and writes
-    the tile layout; sampled output pixels against the oracle."""
+@pytest.mark.parametrize("force", [0x080, 0x1000])
+def test_512_rgb_tile_layout_fused_warp_vs_oracle(force):
+    """512^2 RGB with tile-major / octet-pair MLP inputs forced: k_cols512 runs its fused
+    warp and writes the tiled layout; sampled output pixels against the oracle."""
     import bench
-    from paper_2210_06713_b200 import FORCE_X_TILES
     H = W = 512
     C, frame = 3, 9
     st5 = bench.STEP5
-    plan, basis, mlp, L = plan_for(H, W, C, 3.0, max_batch=4, force=FORCE_X_TILES, **st5)
+    plan, basis, mlp, L = plan_for(H, W, C, 3.0, max_batch=4, force=force, **st5)
     img = synth.image(H, W, C, seed=0)
     out = torch.empty((1, C, H, W), device="cuda")
     plan.simulate_frames(torch.from_numpy(img).cuda(), 0, SEED, frame, 1, out)

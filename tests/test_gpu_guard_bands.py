@@ -35,6 +35,7 @@ CASES = [
     (512, 64, 3, 100, 33, {}, 1),                         # 512-point columns, fused warp
     (48, 512, 1, 16, 17, {}, 2),                          # 512-point register rows
     (64, 160, 3, 16, 17, {"force": 0x080}, 2),            # tile-major MLP inputs
+    (64, 160, 3, 16, 17, {"force": 0x1000}, 2),           # octet-pair MLP inputs
     (1000, 40, 1, 16, 17, {}, 1),                         # persistent in-place columns
     (20, 2400, 1, 16, 17, {}, 1),                         # in-place long rows
     (20, 2400, 1, 16, 17, {"ar_alpha": 0.9}, 2),          # AR row pairs, long rows

@@ -332,7 +332,7 @@ def test_blur_single_basis_vs_oracle(H, W, K, T, k0):
     assert rel_l2(out.cpu().numpy()[0, 0], ref[0]) <= 1e-2
 
 
-@pytest.mark.parametrize("force", [0, 0x080])  # 0x080: force the tile-major MLP input layout
+@pytest.mark.parametrize("force", [0, 0x080, 0x1000])  # forced tile-major / octet-pair MLP input layouts
 @pytest.mark.parametrize("H,W,C,K,T", [(64, 64, 1, 16, 17), (96, 160, 3, 100, 33), (40, 90, 1, 16, 17)])
 def test_blur_api_vs_oracle(H, W, C, K, T, force):
     plan, basis, mlp, sq, L = make_plan(H, W, C, 3.0, K, T, force=force)
@@ -432,7 +432,7 @@ def test_oversized_mlp_is_unsupported():
     assert e.value.status == 5  # P2S_ERR_UNSUPPORTED
 
 
-@pytest.mark.parametrize("force", [0, 0x080])  # 0x080: force the tile-major MLP input layout
+@pytest.mark.parametrize("force", [0, 0x080, 0x1000])  # forced tile-major / octet-pair MLP input layouts
 def test_simulate_ar_sequence_vs_oracle(force):
     """Steps 1-5 on an AR(1) sequence (reading Q18): a fresh start and the stored-state
     continuation both follow the oracle's replayed sequence."""
