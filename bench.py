@@ -131,6 +131,9 @@ WORKLOADS = {
     # BASELINE.json configs[2]: the metric's 512x512 RGB headline, fits one GPU
     "cfg3_512": dict(H=512, W=512, C=3, F=64, d_over_r0=3.0, K=100, T=33, ar_alpha=0.0,
                      desc="512x512 RGB, batch of 64 frames/GPU, D/r0=3, Z=36, K=100 bases 33x33, MLP 33-100-100-100"),
+    # BASELINE.json configs[0]: the parity case (one 64x64 gray frame per call: launch latency)
+    "cfg1_64": dict(H=64, W=64, C=1, F=1, d_over_r0=2.0, K=16, T=17, ar_alpha=0.0,
+                    desc="64x64 gray, one frame per call, D/r0=2, Z=36, K=16 bases 17x17"),
     "cfg4_1080p": dict(H=1080, W=1920, C=3, F=8, d_over_r0=4.0, K=100, T=33, ar_alpha=0.0,
                        desc="1920x1080 RGB, 8 frames/GPU per step, D/r0=4, Z=36, K=100 bases 33x33"),
     # BASELINE.json configs[4]: the metric's 3840x2160 RGB half (the paper's ~60 s/frame case)

@@ -121,6 +121,7 @@ typedef struct {
 #define P2S_FORCE_COLS_PERSISTENT 0x400u /* long columns: persistent one-CTA-per-SM kernel     */
 #define P2S_FORCE_WARP_GATHER     0x800u /* step 2 gathering from global memory, no TMA window  */
 #define P2S_FORCE_X_OCTETS        0x1000u /* MLP inputs [F][H][ntx][slot/2][16][2][8 px]       */
+#define P2S_FORCE_ROWS_INPLACE    0x2000u /* 3840 / 1920 rows: in-place passes, not register-resident */
 
 /* Build a plan (P:312-330 generation setup; runs once, off the per-frame clock).
  *   H, W        image size in pixels (>= T, <= 8192)
@@ -161,7 +162,9 @@ p2s_status p2s_sample_zernike(p2s_plan p, uint64_t seed, int64_t frame0, int nfr
  * its conjugate, self-conjugate bins sqrt(PQ) g1).  Runs Y = sqrt(S_a) eta_a + i sqrt(S_b)
  * eta_b, the 2-D inverse DFT, the crop and the mixing a = L f exactly like
  * p2s_sample_zernike (each bin read as stored; no AR state, no frozen flow) into
- * zern (device float [nframes][Z][H][W]). */
+ * zern (device float [nframes][Z][H][W]).  Spectra that are not Hermitian are not rejected
+ * (checking would cost a pass): the result is then still f_a = Re y, f_b = Im y of the same
+ * inverse DFT, mixed -- well defined, but no longer two independent real fields. */
 p2s_status p2s_sample_zernike_from_noise(p2s_plan p, const float* eta, int nframes, float* zern, void* stream);
 
 /* Step 2: warped (dev float [nframes][C][H][W]) <- bilinear(img, x + kappa (a_2, a_3)).

@@ -626,3 +626,52 @@ def test_simulate_fused_warp_ragged_columns_vs_oracle():
     ref = pipeline.blur_at(Iw, w_at, basis, ys, xs)
     for c in range(C):
         assert rel_l2(got[c, ys, xs], ref[c]) <= 2e-2
+
+
+# ------------------------------------------------------------------ ABI misuse / edge paths
+def test_from_noise_non_hermitian_spectrum_is_the_re_im_split():
+    """p2s_sample_zernike_from_noise does not require Hermitian noise: for arbitrary complex
+    spectra it returns Re / Im of the same inverse DFT, mixed (documented in p2s.h) -- the
+    oracle's fields_from_noise computes exactly that for any input."""
+    H, W, F = 48, 40, 1
+    plan, _, _, sq, L = make_plan(H, W, 1, 2.0, 16, 17)
+    rng = np.random.default_rng(11)
+    eta = (rng.standard_normal((35, plan.P, plan.Q)) + 1j * rng.standard_normal((35, plan.P, plan.Q))) * 40.0
+    z = torch.empty((F, 36, H, W), device="cuda")
+    plan.sample_zernike_from_noise(torch.from_numpy(eta[None].astype(np.complex64)).cuda(), F, z)
+    torch.cuda.synchronize()
+    ref = pipeline.mix(pipeline.fields_from_noise(eta, sq, H, W), L)
+    got = z.cpu().numpy()[0]
+    assert max(rel_l2(got[j], ref[j]) for j in range(1, 36)) <= 1e-4
+
+
+def test_legacy_default_stream_and_side_stream():
+    """stream = NULL (the legacy default stream) and a caller-created stream give the same bits."""
+    H = W = 64
+    plan, *_ = make_plan(H, W, 1, 2.0, 16, 17)
+    img = cuda(synth.image(H, W, 1, seed=3))
+    a = torch.empty((2, 1, H, W), device="cuda")
+    b = torch.empty_like(a)
+    plan.simulate_frames(img, 0, SEED, 5, 2, a, stream=0)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        plan.simulate_frames(img, 0, SEED, 5, 2, b, stream=s)
+    s.synchronize()
+    assert torch.equal(a, b)
+
+
+def test_calls_on_a_destroyed_or_slab_plan_fail_loudly():
+    from paper_2210_06713_b200 import P2SError, Plan, PlanConfig
+    H = W = 64
+    p = Plan(PlanConfig(H=H, W=W, C=1, d_over_r0=2.0, K=16, taps=17, slab_count=2, slab_rank=0),
+             synth.basis(16, 17), synth.mlp_weights(16))
+    z = torch.empty((1, 36, H, W), device="cuda")
+    with pytest.raises(P2SError) as e:
+        p.sample_zernike(SEED, 0, 1, z)  # a slab plan runs only through p2s_slab_*
+    assert e.value.status == 1
+    q, *_ = make_plan(H, W, 1, 2.0, 16, 17)
+    q.close()
+    with pytest.raises(P2SError) as e:
+        q.sample_zernike(SEED, 0, 1, z)  # NULL plan after destroy
+    assert e.value.status == 1
