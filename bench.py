@@ -411,8 +411,16 @@ def measure_slab(args, rank, world, local, name="cfg5_4k"):
     from paper_2210_06713_b200 import Plan, PlanConfig, runner, slab_geometry
     w = dict(WORKLOADS[name])
     H, W, C, K, T = w["H"], w["W"], w["C"], w["K"], w["T"]
-    plan = Plan(PlanConfig(H=H, W=W, C=C, d_over_r0=w["d_over_r0"], K=K, taps=T, device=local, slab_count=world,
-                           slab_rank=rank, **STEP5), synth.basis(K, T, seed=0), synth.mlp_weights(K, seed=0))
+    err = None
+    try:
+        plan = Plan(PlanConfig(H=H, W=W, C=C, d_over_r0=w["d_over_r0"], K=K, taps=T, device=local,
+                               slab_count=world, slab_rank=rank, **STEP5), synth.basis(K, T, seed=0),
+                    synth.mlp_weights(K, seed=0))
+    except Exception as e:
+        err = e
+    # every rank must have a plan before any rank enters the all-to-all
+    if runner.sum_over_ranks(0.0 if err is None else 1.0) > 0:
+        raise RuntimeError(f"slab plan creation failed on some rank ({err})")
     dev = torch.device("cuda", local)
     img = torch.from_numpy(synth.image(H, W, C, seed=0)).to(dev)
     snd, rcv = plan.slab_counts()
@@ -541,7 +549,10 @@ def main():
                             "gpu_launches": r["gpu_launches"], "roofline": r["roofline"], "stages": r["stages"]}
 
     if world > 1 and not args.no_slab:
-        sl = measure_slab(args, rank, world, local)
+        try:
+            sl = measure_slab(args, rank, world, local)
+        except Exception as e:  # plan creation fails on every rank alike (checked below)
+            sl = {"error": f"{type(e).__name__}: {e}"}
         if rank == 0:
             extras["cfg5_4k_slab"] = sl
 
