@@ -80,3 +80,33 @@ def test_plan_create_without_gpu_fails_loudly():
     from paper_2210_06713_b200 import P2SError, Plan, PlanConfig
     with pytest.raises(P2SError):
         Plan(PlanConfig(H=64, W=64, C=1, d_over_r0=1.0, K=16, taps=17), synth.basis(16, 17), synth.mlp_weights(16))
+
+
+@pytest.mark.parametrize("H,W,T,G", [(2160, 3840, 33, 8), (1080, 1920, 33, 5), (96, 160, 17, 3), (75, 90, 9, 4)])
+def test_slab_geometry_partitions_columns_and_spectral_rows(H, W, T, G):
+    """p2s_slab_geometry (host only): the G output strips tile [0, W) contiguously, each halo is
+    the strip widened by T/2 and clipped to the frame, and the Hermitian row pairs of the G
+    ranks hold every spectral row of the P-point grid exactly once (pair {ky, P - ky}, the
+    self-mirrored rows 0 and P/2 once)."""
+    p2s = _lib()
+    geo = [p2s.slab_geometry(H, W, T, G, r) for r in range(G)]
+    assert geo[0]["x0"] == 0 and geo[-1]["x1"] == W
+    for a, b in zip(geo, geo[1:]):
+        assert a["x1"] == b["x0"] and a["kp1"] == b["kp0"]
+    P = geo[0]["P"]
+    rows = []
+    for g in geo:
+        assert g["hx0"] == max(0, g["x0"] - T // 2) and g["hx1"] == min(W, g["x1"] + T // 2)
+        mine = [kp for kp in range(g["kp0"], g["kp1"])] + [P - kp for kp in range(g["kp0"], g["kp1"])
+                                                              if kp != 0 and 2 * kp != P]
+        assert len(mine) == g["rows"]
+        rows += mine
+    assert sorted(rows) == list(range(P))
+
+
+def test_slab_geometry_rejects_bad_arguments():
+    p2s = _lib()
+    for args in [(64, 64, 17, 0, 0), (64, 64, 17, 2, 2), (64, 64, 17, 2, -1), (0, 64, 17, 1, 0)]:
+        with pytest.raises(p2s.P2SError) as e:
+            p2s.slab_geometry(*args)
+        assert e.value.status == 1
