@@ -116,7 +116,7 @@ typedef struct {
 #define P2S_FORCE_COLS_PER_BLOCK  0x020u /* long columns: one CTA per block, not persistent    */
 #define P2S_FORCE_X_PLANES        0x040u /* MLP inputs as [F][slot][H*W] planes                */
 #define P2S_FORCE_X_TILES         0x080u /* MLP inputs tile-major [F][H][ntx][slot][128]       */
-#define P2S_FORCE_NO_WARP_FUSION  0x100u /* step 2 as its own kernel, not in the column pass   */
+#define P2S_FORCE_WARP_FUSION     0x100u /* step 2 inside the 512-point column kernel          */
 #define P2S_FORCE_BLUR_SINGLE     0x200u /* blur on single CTAs (cta_group::1), not CTA pairs  */
 #define P2S_FORCE_COLS_PERSISTENT 0x400u /* long columns: persistent one-CTA-per-SM kernel     */
 #define P2S_FORCE_WARP_GATHER     0x800u /* step 2 gathering from global memory, no TMA window  */

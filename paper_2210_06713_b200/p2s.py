@@ -52,7 +52,7 @@ FORCE_ROWS_PINGPONG = 0x010
 FORCE_COLS_PER_BLOCK = 0x020
 FORCE_X_PLANES = 0x040
 FORCE_X_TILES = 0x080
-FORCE_NO_WARP_FUSION = 0x100
+FORCE_WARP_FUSION = 0x100
 FORCE_BLUR_SINGLE = 0x200
 FORCE_COLS_PERSISTENT = 0x400
 FORCE_WARP_GATHER = 0x800

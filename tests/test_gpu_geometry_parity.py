@@ -11,7 +11,7 @@
   invariant blur with the kernel sum_k w_k(0) h_k -- against scipy's mirror convolution.
 * Row length 4096 (16·16·16 in place; the AR pass falls back to the row kernel) and a row
   length no row kernel fits (4050: P2S_ERR_UNSUPPORTED at plan creation).
-* The MLP input layouts where each is used: tile-major at 512^2 (fused-warp k_cols512)
+* The MLP input layouts where each is used: tile-major at 512^2 (k_cols512 with step 2 fused)
   against the oracle, planes vs tiles at 1080p (k_cols_p) and 4K, bit for bit.
 
 Tolerances as everywhere (north_star): rel-L2 <= 1e-4 per mode plane (fp32 step 1),
@@ -176,7 +176,7 @@ def test_512_rgb_tile_layout_fused_warp_vs_oracle(force):
     H = W = 512
     C, frame = 3, 9
     st5 = bench.STEP5
-    plan, basis, mlp, L = plan_for(H, W, C, 3.0, max_batch=4, force=force, **st5)
+    plan, basis, mlp, L = plan_for(H, W, C, 3.0, max_batch=4, force=force | 0x100, **st5)
     img = synth.image(H, W, C, seed=0)
     out = torch.empty((1, C, H, W), device="cuda")
     plan.simulate_frames(torch.from_numpy(img).cuda(), 0, SEED, frame, 1, out)

@@ -32,7 +32,8 @@ def guards_intact(buf):
 CASES = [
     # (H, W, C, K, T, plan kwargs, F)
     (64, 96, 2, 16, 17, {}, 2),                           # generic FFTs, CTA-pair blur
-    (512, 64, 3, 100, 33, {}, 1),                         # 512-point columns, fused warp
+    (512, 64, 3, 100, 33, {}, 1),                         # 512-point columns, TMA warp
+    (512, 64, 3, 100, 33, {"force": 0x100}, 1),           # 512-point columns, fused warp
     (48, 512, 1, 16, 17, {}, 2),                          # 512-point register rows
     (64, 160, 3, 16, 17, {"force": 0x080}, 2),            # tile-major MLP inputs
     (64, 160, 3, 16, 17, {"force": 0x1000}, 2),           # octet-pair MLP inputs

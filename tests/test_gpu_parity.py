@@ -603,12 +603,13 @@ def test_frozen_flow_with_ar_is_rejected():
         make_plan(32, 32, 1, 2.0, 16, 17, flow=(1.0, 0.0), ar_alpha=0.5)
 
 
-def test_simulate_fused_warp_ragged_columns_vs_oracle():
-    """512-point columns with W not a multiple of the 16-column block: the fused step-2
-    path (mode-pair-0 column CTAs warp the image) and the ragged last block, checked
-    against the oracle on sampled pixels (full-frame Eq.9 is too slow at 512 rows)."""
+@pytest.mark.parametrize("force", [0, 0x100])  # 0x100: step 2 fused into the column kernel
+def test_simulate_fused_warp_ragged_columns_vs_oracle(force):
+    """512-point columns with W not a multiple of the 16-column block: the separate TMA
+    warp and the fused step-2 path (mode-pair-0 column CTAs warp the image), the ragged last
+    block, checked against the oracle on sampled pixels (full-frame Eq.9 is too slow)."""
     H, W, C, K, T, F = 512, 200, 3, 16, 17, 1
-    plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T)
+    plan, basis, mlp, sq, L = make_plan(H, W, C, 2.0, K, T, force=force)
     assert plan.P == 512
     img = synth.image(H, W, C, seed=4)
     out = torch.empty((F, C, H, W), device="cuda")

@@ -43,7 +43,7 @@ def simulate(p, F=2, frame0=0):
 
 CASES = {
     "generic_fft_blur_pair": lambda: simulate(plan(64, 96, C=2)),
-    "reg512_cols_fused_warp": lambda: simulate(plan(512, 64, C=3, K=100, T=33), F=1),
+    "reg512_cols_fused_warp": lambda: simulate(plan(512, 64, C=3, K=100, T=33, force=0x100), F=1),
     "reg512_rows": lambda: simulate(plan(48, 512), F=1),
     "reg512_generic_forced": lambda: simulate(plan(512, 512, force=FORCE_FFT_GENERIC), F=1),
     "x_tiles": lambda: simulate(plan(64, 160, C=3, force=FORCE_X_TILES)),
