@@ -198,7 +198,9 @@ p2s_status p2s_simulate_frames(p2s_plan p, const float* img, int64_t img_frame_s
  * out_host [nframes][C][H][W].  Copies in, runs, copies out, synchronises.  Internally the
  * frames run as tapered sub-batches on `stream` while a second (plan-owned) stream uploads
  * the images and downloads each finished sub-batch; pinned host memory gives full PCIe
- * overlap.  Results are bit-identical to p2s_simulate_frames. */
+ * overlap.  The image upload overlaps step 1 (only the warp waits for it), and a one-frame
+ * last sub-batch runs its blur in two row-band halves so the top half's download overlaps
+ * the bottom half.  Results are bit-identical to p2s_simulate_frames. */
 p2s_status p2s_simulate_frames_host(p2s_plan p, const float* img_host, int64_t img_frame_stride,
                                     uint64_t seed, int64_t frame0, int nframes, float* out_host,
                                     void* stream);
@@ -347,7 +349,9 @@ p2s_status p2s_host_tables(int P, int Q, double s_per_px, double d_over_r0, int 
 int p2s_grid_size(int x);
 
 /* ---------------------------------------------------------------------------------------
- * Single-frame latency mode: one frame sharded over G ranks.
+ * Single-frame latency mode: one frame sharded over G ranks -- for
+ * the large-frame case where one frame's latency matters (the paper's 3840x2160 frame,
+ * "about 60 seconds per frame" with split-step).
  * Step 1's first pass (noise + PSD + row IDFT) is split by Hermitian spectral
  * row pairs {ky, P-ky}: rank r transforms pairs kp in [kp0, kp1).  The second pass needs
  * whole columns, so the row-transformed spectrum is transposed across ranks by one
