@@ -76,7 +76,7 @@ def tensor_peak(peaks, clocks):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms over the warm-up and timed steps."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -320,13 +320,16 @@ def measure(name, args, rank, world, local, peaks):
             import torch.distributed as dist
             dist.barrier()
 
+    # the clock sampler (nvidia-smi, one process start ~0.1-0.3 s) runs from before the
+    # warm-up steps to the end of the timed region, so short timed regions (4K: ~0.15 s) are
+    # covered; every sample is under load
+    clk = ClockSampler(local)
+    clk.start()
     for s in range(args.warmup):
         plan.simulate_frames(img, 0, *frames(s), F, out)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    clk = ClockSampler(local)
-    clk.start()
     plan.stage_timing(True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)

@@ -15,7 +15,7 @@ python bench.py --workload cfg5_4k_f1 --extra cfg5_4k_ar,cfg4_1080p,cfg4_1080p_a
   > $O/${TAG}_workloads.json 2>> $O/${TAG}_bench.err
 CMD="python bench.py --steps 2 --warmup 1 --extra none --no-e2e --no-cpu-baseline"
 $CMD > $O/${TAG}_plain.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -s 4 -c 8 --csv --log-file $O/${TAG}_launches.csv $CMD \
+  ncu --metrics gpu__time_duration.sum --clock-control none -s 5 -c 10 --csv --log-file $O/${TAG}_launches.csv $CMD \
   > $O/${TAG}_ncu_launch.log 2>&1
 $CMD > $O/${TAG}_plain2.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:'k_rows|k_cols|k_mlp|k_blur' -s 4 -c 4 \
