@@ -256,3 +256,23 @@ def test_tma_window_warp_matches_gather_warp(H, W, C, img_frames):
         torch.cuda.synchronize()
         outs.append(o)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("W,force", [(2400, 0), (2400, 0x004), (1200, 0)])
+def test_ar_generic_long_rows_vs_oracle(W, force):
+    """AR(0.9) on long rows outside the compile-time plans: 2400 = 16·15·10 takes the generic
+    512-thread row-pair kernel (0x004: the one-CTA-per-row kernel), 1200 (512 < Q <= 1024 is
+    not it; 1200 > 1024) the pair kernel with four bins per thread -- fresh start, continuation
+    and replayed start against the oracle's recursion."""
+    H, alpha = 20, 0.9
+    plan, basis, mlp, L = plan_for(H, W, 1, 2.0, K=16, T=17, ar_alpha=alpha, force=force)
+    z = torch.empty((4, 36, H, W), device="cuda")
+    plan.sample_zernike(SEED, 0, 2, z[0:2])
+    plan.sample_zernike(SEED, 2, 1, z[2:3])
+    plan.sample_zernike(SEED, 1, 1, z[3:4])
+    torch.cuda.synchronize()
+    assert torch.equal(z[3], z[1])
+    zc = z.cpu().numpy()
+    sq = oracle_sqrtS(plan.P, plan.Q)
+    for t, eta in enumerate(pipeline.spectral_noise_sequence(SEED, 0, 3, plan.P, plan.Q, alpha)):
+        assert_planes(zc[t], fields_of(eta, sq, L, H, W))
