@@ -11,11 +11,11 @@ for step in "$@"; do
            echo "smoke exit $?" >> gpurun_out/smoke.log ;;
     bench) timeout -s KILL 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err;
            echo "bench exit $?" >> gpurun_out/bench.err ;;
-    sweep:*)  # sweep:VAR=a,b,c -> short bench per value (blur-focused tuning)
-      kv="${step#sweep:}"; var="${kv%%=*}"; vals="${kv#*=}"
+    force:*)  # force:0x100,0x800 -> short bench per p2s_options.force value (kernel variants)
+      vals="${step#force:}"
       for v in ${vals//,/ }; do
-        env "$var=$v" timeout -s KILL 600 python bench.py --steps 5 --warmup 2 --no-cpu-baseline --no-e2e \
-          > "gpurun_out/sweep_${var}_${v}.json" 2>&1
+        timeout -s KILL 600 python bench.py --steps 5 --warmup 3 --extra none --no-cpu-baseline --no-e2e --force "$v" \
+          > "gpurun_out/force_${v}.json" 2>&1
       done ;;
     bench_ref) timeout -s KILL 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1 ;;
     ncu_launches)

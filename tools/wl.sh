@@ -1,5 +1,5 @@
 #!/bin/bash
-# Short bench of named workloads (optionally with env overrides): tools/wl.sh cfg4_1080p cfg5_4k ...
+# Short bench of named workloads (TAG labels the lines): tools/wl.sh cfg4_1080p cfg5_4k ...
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 for W in "$@"; do
   timeout 600 python bench.py --workload "$W" --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null |
