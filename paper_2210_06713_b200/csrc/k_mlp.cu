@@ -89,13 +89,17 @@ __device__ __forceinline__ void wg_sync(int wg) {  // named barrier of one 128-t
 
 // A1 tile (nin planes x 128 pixels, MN-major, k linear at 16 B): pixels [pix0, pix0 + n) of
 // frame f (one row segment, n <= 128; the rest of the tile is zero).
+// NIN > 0: the input count at compile time (35 on the simulate path, 33 on the blur API
+// path), so the chunk index splits by constant division.
+template <int NIN>
 __device__ __forceinline__ void load_a1(const MlpArgs& a, uint8_t* A1, int tile, int f, int pix0, int n, int ltid,
                                         bool async) {
-  const uint16_t* Xf = a.X + (size_t)f * a.nin * a.HW;
-  const int nin2 = a.xtile == 2 ? (a.nin + 1) & ~1 : a.nin;
+  const int nin = NIN > 0 ? NIN : a.nin;
+  const uint16_t* Xf = a.X + (size_t)f * nin * a.HW;
+  const int nin2 = a.xtile == 2 ? (nin + 1) & ~1 : nin;
   const uint16_t* Xt = a.X + (size_t)tile * 128 * nin2;  // tile-major: this tile's block
-  for (int idx = ltid; idx < a.nin * 16; idx += 128) {
-    const int k = idx % a.nin, g = idx / a.nin;
+  for (int idx = ltid; idx < nin * 16; idx += 128) {
+    const int k = idx % nin, g = idx / nin;
     const int o = 8 * g;
     // tile-major: plane k of this tile at k * 128 elements of its contiguous block; octet-pair
     // layout (xtile 2): the chunk of mode k, octet g at ((k/2) 16 + g) 16 + (k%2) 8
@@ -136,6 +140,7 @@ constexpr int kMlpWG = 4;  // independent 128-pixel tile pipelines per CTA
 // kMlpWG warpgroups per CTA, each an independent tile pipeline (own A1, A2, 128 TMEM
 // columns, mbarrier), sharing one resident copy of the weight images; while one warpgroup
 // runs an epilogue the tensor core serves the others.
+template <int NIN>
 __global__ void __launch_bounds__(128 * kMlpWG, 1)
     k_mlp(const MlpArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -205,7 +210,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
   if (tile < ntiles) {
     int f, pix0, n;
     tile_pixels(a, tile, f, pix0, n);
-    load_a1(a, A1, tile, f, pix0, n, ltid, async);
+    load_a1<NIN>(a, A1, tile, f, pix0, n, ltid, async);
   }
   cp_async_commit();
   for (; tile < ntiles; tile += stride) {
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
       if (nxt < ntiles) {
         int fn, pn, nn;
         tile_pixels(a, nxt, fn, pn, nn);
-        load_a1(a, A1, nxt, fn, pn, nn, ltid, async);
+        load_a1<NIN>(a, A1, nxt, fn, pn, nn, ltid, async);
       }
       cp_async_commit();
     }
@@ -368,11 +373,12 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   int nwg = std::min(kMlpWG, 512 / cols_wg);
   while (nwg > 1 && blob_al + nwg * per_wg + 64 > 227 * 1024) --nwg;
   size_t sm = blob_al + nwg * per_wg + 64;
-  P2S_SMEM_OPTIN(k_mlp, sm);
+  auto kern = a.nin == 35 ? k_mlp<35> : a.nin == 33 ? k_mlp<33> : k_mlp<0>;
+  P2S_SMEM_OPTIN(kern, sm);
   const int ntiles = F * a.tiles_per_frame;
   int grid = p->num_sms;  // persistent: one CTA (nwg tile pipelines) per SM
   if (nwg * grid > ntiles) grid = (ntiles + nwg - 1) / nwg;
-  k_mlp<<<grid, 128 * nwg, sm, s>>>(a);
+  kern<<<grid, 128 * nwg, sm, s>>>(a);
   return (int)cudaGetLastError();
 }
 
