@@ -121,7 +121,6 @@ typedef struct {
 #define P2S_FORCE_COLS_PERSISTENT 0x400u /* long columns: persistent one-CTA-per-SM kernel     */
 #define P2S_FORCE_WARP_GATHER     0x800u /* step 2 gathering from global memory, no TMA window  */
 #define P2S_FORCE_X_OCTETS        0x1000u /* MLP inputs [F][H][ntx][slot/2][16][2][8 px]       */
-#define P2S_FORCE_ROWS_INPLACE    0x2000u /* 3840 / 1920 rows: in-place passes, not register-resident */
 
 /* Build a plan (P:312-330 generation setup; runs once, off the per-frame clock).
  *   H, W        image size in pixels (>= T, <= 8192)

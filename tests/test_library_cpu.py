@@ -110,3 +110,15 @@ def test_slab_geometry_rejects_bad_arguments():
         with pytest.raises(p2s.P2SError) as e:
             p2s.slab_geometry(*args)
         assert e.value.status == 1
+
+
+def test_force_bits_match_header():
+    """The Python FORCE_* constants are the header's P2S_FORCE_* bits (the kernel-selection
+    overrides of p2s_options.force)."""
+    p2s = _lib()
+    hdr = open(os.path.join(ROOT, "include", "p2s.h")).read()
+    bits = {m.group(1): int(m.group(2), 16) for m in re.finditer(r"#define P2S_FORCE_(\w+)\s+0x([0-9a-fA-F]+)u", hdr)}
+    assert bits and len(set(bits.values())) == len(bits)
+    for name, v in bits.items():
+        assert getattr(p2s, "FORCE_" + name) == v, name
+    assert {k[6:] for k in dir(p2s) if k.startswith("FORCE_")} == set(bits)
