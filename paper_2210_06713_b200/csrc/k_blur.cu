@@ -40,6 +40,7 @@ constexpr int kStepsPerStage = kBlurStepsPerStage;  // K-steps (B tiles) moved p
 constexpr int kEpiWarps = 16;      // four warps per TMEM lane quarter, each owning two 16-basis chunks
 constexpr int kBlurThreads = 64 + 32 * kEpiWarps;  // warp 0 TMA producer, warp 1 MMA issuer, epilogue
 constexpr int kAccStride = 128;    // TMEM columns per accumulator
+constexpr int kBlurLagStages = 1;  // B stages run for accumulator 0 alone at a row-group start (LAG)
 constexpr int kLoadRows = 4;       // source rows staged per warp by the tile loader
 constexpr int kSeg = 192;          // staged pixels per source row (>= 128 + T - 1 for T <= 63)
 
@@ -126,6 +127,11 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(trow_empty + kBlurTSlots);
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
+  // TMEM columns of accumulator a (= ch * RACC + r) of row group rg (see the MMA issuer)
+  constexpr bool LAG = C * RACC == 3;
+  auto acc_col = [](int rg, int ac) -> uint32_t {
+    return (uint32_t)((LAG ? ((3 * rg + ac) & 3) : ac) * kAccStride);
+  };
 
   const int x0 = blockIdx.x * 128, y0 = (a.band0 + (int)blockIdx.y) * a.RB, f = blockIdx.z;
   const int HW = a.H * a.W;
@@ -286,35 +292,28 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
   } else if (warp == 1 && leader) {
     // ---- MMA issuer (one elected lane): C x RACC accumulators per K-step, kStepsPerStage
     // K-steps per ring stage so the issuing thread stays ahead of the tensor pipe.
+    // LAG (3 accumulators, the 4th TMEM slot free): accumulator a of row group rg lives in
+    // slot (3 rg + a) mod 4, so accumulator 0 of the next row group starts in the free slot
+    // on the first kBlurLagStages B stages while the epilogue drains the previous group;
+    // accumulators 1-2 catch up on the same stages once it has released its slots.  The K
+    // order within each accumulator is unchanged (results are bit-identical to no lag).
+    // The epilogue's tcgen05.ld waits behind MMAs already in flight, so a longer lag delays
+    // the drain by as much as it hides (measured, DESIGN 6c): one stage.
     uint32_t stage = 0, phase = 0;
     const uint64_t ch_step = (uint64_t)(L.tile_bytes >> 4);
     const uint64_t b_desc_base = umma_desc(smem_u32(ring), 128, 256);
     if (tmem != 0) __trap();  // accumulators are addressed from column 0
-    uint64_t w_full = 0, w_tempty = 0, w_trow = 0;
+    uint64_t w_full = 0, w_tempty = 0, w_trow = 0, p_a = 0, p_b = 0, p_c = 0;
     const uint64_t t_mma0 = clk();
+    const int st_tr = a.nks_main / kStepsPerStage;  // first stage with a transposed K-step
     for (int rg = 0; rg < n_rg; ++rg) {
-      uint64_t t0c = clk();
-      mbar_wait(tempty, (rg & 1) ^ 1);
-      w_tempty += clk() - t0c;
-      tc_fence_after();
       const uint64_t a_row_desc = (uint64_t)(rg * RACC);  // start address += rows of this group
       const int slot = rg % kBlurTSlots;
       const uint64_t t_row_desc = (uint64_t)(slot * RACC * a.lr * a.nct);  // transposed rows of this group
       const uint64_t t_rstep = (uint64_t)(a.lr * a.nct);
-      const int st_tr = a.nks_main / kStepsPerStage;  // first stage with a transposed K-step
-      for (int st = 0; st < nst; ++st) {
-        const uint64_t t1c = clk();
-        mbar_wait(&full[stage], phase);
-        w_full += clk() - t1c;
-        if (st == st_tr && a.nks > a.nks_main) {
-          const uint64_t t2c = clk();
-          if (PAIR)
-            mbar_wait_cluster(&trow_full[slot], (rg / kBlurTSlots) & 1);
-          else
-            mbar_wait(&trow_full[slot], (rg / kBlurTSlots) & 1);
-          w_trow += clk() - t2c;
-        }
-        tc_fence_after();
+      const int nA = (LAG && rg > 0) ? min(kBlurLagStages, nst) : 0;  // lagged stages
+      // one ring stage: MMAs of accumulators [a0, a1) on its K-steps; optionally release it
+      auto issue_stage = [&](int st, int acc0, int acc1, bool release) {
         const uint64_t bdesc0 = b_desc_base + (uint64_t)((stage * kStepsPerStage * bbytes) >> 4);
         const int t0 = st * kStepsPerStage;
         if (elect_one()) {
@@ -328,29 +327,78 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
               const uint64_t rstep = tr ? t_rstep : 1ull;
               const uint32_t acc = t > 0 ? 1u : 0u;
 #pragma unroll
-              for (int ch = 0; ch < C; ++ch)
-#pragma unroll
-                for (int r = 0; r < RACC; ++r) {
-                  if (PAIR)
-                    umma_bf16_pair((uint32_t)((ch * RACC + r) * kAccStride), ad + ch * ch_step + r * rstep, bd,
-                                   a.idesc, acc);
-                  else
-                    umma_bf16((uint32_t)((ch * RACC + r) * kAccStride), ad + ch * ch_step + r * rstep, bd, a.idesc,
-                              acc);
-                }
+              for (int ac = 0; ac < C * RACC; ++ac) {
+                if (ac < acc0 || ac >= acc1) continue;
+                const int ch = ac / RACC, r = ac - ch * RACC;
+                const uint32_t d = acc_col(rg, ac);
+                if (PAIR)
+                  umma_bf16_pair(d, ad + ch * ch_step + r * rstep, bd, a.idesc, acc);
+                else
+                  umma_bf16(d, ad + ch * ch_step + r * rstep, bd, a.idesc, acc);
+              }
             }
           }
-          if (PAIR)
-            umma_commit_pair(&empty[stage]);
-          else
-            umma_commit(&empty[stage]);
+          if (release) {
+            if (PAIR)
+              umma_commit_pair(&empty[stage]);
+            else
+              umma_commit(&empty[stage]);
+          }
         }
         __syncwarp();
+      };
+      auto wait_stage = [&](int st) {
+        const uint64_t t1c = clk();
+        mbar_wait(&full[stage], phase);
+        w_full += clk() - t1c;
+        if (st == st_tr && a.nks > a.nks_main) {
+          const uint64_t t2c = clk();
+          if (PAIR)
+            mbar_wait_cluster(&trow_full[slot], (rg / kBlurTSlots) & 1);
+          else
+            mbar_wait(&trow_full[slot], (rg / kBlurTSlots) & 1);
+          w_trow += clk() - t2c;
+        }
+        tc_fence_after();
+      };
+      auto next_stage = [&]() {
         if (++stage == kBlurStages) {
           stage = 0;
           phase ^= 1;
         }
+      };
+      const uint32_t stage_a = stage, phase_a = phase;
+      const uint64_t ph0 = clk();
+      for (int st = 0; st < nA; ++st) {  // phase A: accumulator 0 alone, stages kept
+        wait_stage(st);
+        issue_stage(st, 0, 1, false);
+        next_stage();
       }
+      {
+        uint64_t t0c = clk();
+        mbar_wait(tempty, (rg & 1) ^ 1);  // the previous row group's slots are drained
+        w_tempty += clk() - t0c;
+        tc_fence_after();
+      }
+      const uint64_t ph1 = clk();
+      if (nA > 0) {  // phase B: the other accumulators on the same stages, then release them
+        stage = stage_a;
+        phase = phase_a;
+        for (int st = 0; st < nA; ++st) {
+          issue_stage(st, 1, C * RACC, true);
+          next_stage();
+        }
+      }
+      const uint64_t ph2 = clk();
+      for (int st = nA; st < nst; ++st) {
+        wait_stage(st);
+        issue_stage(st, 0, C * RACC, true);
+        next_stage();
+      }
+      const uint64_t ph3 = clk();
+      p_a += ph1 - ph0;
+      p_b += ph2 - ph1;
+      p_c += ph3 - ph2;
       if (elect_one()) {
         if (PAIR) {
           umma_commit_pair(tfull);
@@ -367,6 +415,9 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
       atomicAdd(&a.probe[2], (unsigned long long)w_tempty);
       atomicAdd(&a.probe[3], (unsigned long long)(clk() - t_mma0));
       atomicAdd(&a.probe[9], (unsigned long long)w_trow);
+      atomicAdd(&a.probe[12], (unsigned long long)p_a);
+      atomicAdd(&a.probe[13], (unsigned long long)p_b);
+      atomicAdd(&a.probe[14], (unsigned long long)p_c);
     }
   } else if (warp >= 2) {
     // ---- epilogue warps 2..17: TMEM lane quarter qd = warp % 4; part h = 0..3 owns the
@@ -447,7 +498,7 @@ __global__ void __launch_bounds__(kBlurThreads, 1)
           if (cb < nch) {
             uint32_t v[C][16];
 #pragma unroll
-            for (int ch = 0; ch < C; ++ch) tmem_ld16_issue(tl + (ch * RACC + r) * kAccStride + cb * 16, v[ch]);
+            for (int ch = 0; ch < C; ++ch) tmem_ld16_issue(tl + acc_col(rg, ch * RACC + r) + cb * 16, v[ch]);
             float wf[16];
             {
               const uint32_t* wp = reinterpret_cast<const uint32_t*>(&wc[r][c][0]);
@@ -609,8 +660,8 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
   const bool want_probe = false;
 #endif
   if (want_probe) {
-    if (!probe) cudaMalloc(&probe, 12 * sizeof(unsigned long long));
-    cudaMemsetAsync(probe, 0, 12 * sizeof(unsigned long long), s);
+    if (!probe) cudaMalloc(&probe, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(probe, 0, 16 * sizeof(unsigned long long), s);
     a.probe = probe;
   }
   const bool pair = g.pair;
@@ -634,16 +685,16 @@ int launch_blur(const p2s_plan_s* p, int F, const void* src, bool src_f32, uint6
     rc = src_f32 ? launch_blur_c<true, false>(p->C, a, p->tmap_b, grid, sm, s)
                  : launch_blur_c<false, false>(p->C, a, p->tmap_b, grid, sm, s);
   if (want_probe) {  // debug: per-CTA averages of the phase cycle counters
-    unsigned long long h[12];
+    unsigned long long h[16];
     cudaMemcpyAsync(h, probe, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     const double n = h[7] ? (double)h[7] : 1.0, nm = pair ? n / 2 : n;
     fprintf(stderr,
             "[blur probe] CTAs %llu  per CTA cycles: total %.0f prologue %.0f | MMA warp: loop %.0f wait_full %.0f "
             "wait_tmem %.0f wait_trow %.0f | epilogue warp 2: wait %.0f work %.0f (tfull to release %.0f) | "
-            "producer: trow fill %.0f ring wait %.0f\n",
+            "producer: trow fill %.0f ring wait %.0f | issuer phases A+wait %.0f B %.0f C %.0f\n",
             h[7], h[6] / n, h[0] / n, h[3] / nm, h[1] / nm, h[2] / nm, h[9] / nm, h[4] / n, h[5] / n, h[8] / n,
-            h[10] / n, h[11] / n);
+            h[10] / n, h[11] / n, h[12] / nm, h[13] / nm, h[14] / nm);
   }
   return rc;
 }

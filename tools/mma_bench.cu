@@ -218,5 +218,13 @@ int main() {
       run(name, c);
     }
   }
+  // accumulator chains: consecutive MMAs into 1..4 rotating accumulators (a run of MMAs into
+  // one accumulator waits on its own result)
+  for (int nacc : {1, 2, 3, 4}) {
+    Cfg c = {1, 0, 112, n, 128, 1232u, 128, 256, 16, 1, nacc, 0, 0, 3, 16, 1, 1, 40960};
+    char name[128];
+    snprintf(name, sizeof(name), "PAIR 3 tiles, %d accumulator(s)", nacc);
+    run(name, c);
+  }
   return 0;
 }
