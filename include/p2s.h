@@ -121,6 +121,7 @@ typedef struct {
 #define P2S_FORCE_COLS_PERSISTENT 0x400u /* long columns: persistent one-CTA-per-SM kernel     */
 #define P2S_FORCE_WARP_GATHER     0x800u /* step 2 gathering from global memory, no TMA window  */
 #define P2S_FORCE_X_OCTETS        0x1000u /* MLP inputs [F][H][ntx][slot/2][16][2][8 px]       */
+#define P2S_FORCE_MLP_A1_THREADS  0x2000u /* MLP inputs loaded by per-thread copies, no TMA box */
 
 /* Build a plan (P:312-330 generation setup; runs once, off the per-frame clock).
  *   H, W        image size in pixels (>= T, <= 8192)

@@ -25,7 +25,10 @@
 #include "p2s_dev.cuh"
 #include "p2s_internal.h"
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstring>
 
 namespace p2s {
 
@@ -38,6 +41,7 @@ struct MlpArgs {
   int HW, H, W, ntx, F, tiles_per_frame;
   int bias_folded;  // A1 column nin is the constant 1; biases live in the weight images
   int xtile;        // X layout (x_index): 1 = tile-major [F][H][ntx][nin][128]
+  int a1_tma;       // A1 tiles by TMA (tmap_x valid)
 };
 
 // Epilogue of a hidden layer: TMEM columns [0, ncols) of this thread's row -> +bias -> ReLU
@@ -142,7 +146,7 @@ constexpr int kMlpWG = 4;  // independent 128-pixel tile pipelines per CTA
 // runs an epilogue the tensor core serves the others.
 template <int NIN>
 __global__ void __launch_bounds__(128 * kMlpWG, 1)
-    k_mlp(const MlpArgs a) {
+    k_mlp(const __grid_constant__ MlpArgs a, const __grid_constant__ CUtensorMap tmap_x) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sw = smem;  // weight blob
   const uint32_t blob_al = (a.blob_bytes + 127) & ~127u;
@@ -157,8 +161,9 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
   uint8_t* A1 = sw + blob_al + wg * wg_bytes;
   uint8_t* A2 = A1 + a1_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sw + blob_al + nwg * wg_bytes);
-  uint64_t* bar = bars + wg;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + kMlpWG);
+  uint64_t* bar = bars + wg;                 // layer MMAs done
+  uint64_t* a1bar = bars + kMlpWG + wg;      // A1 bulk copy landed (xtile 3)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kMlpWG);
 
   for (uint32_t i = tid * 16; i < a.blob_bytes; i += blockDim.x * 16)
     *reinterpret_cast<uint4*>(sw + i) = __ldg(reinterpret_cast<const uint4*>(a.blob + i));
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     }
   }
   if (tid == 0) {
-    for (int i = 0; i < nwg; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 2 * kMlpWG; ++i) mbar_init(&bars[i], 1);
     mbar_fence_init();
   }
   const int wmax = na2;  // widest accumulator (n1, n2 or n3)
@@ -201,20 +206,48 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
   const uint32_t id1 = umma_idesc_bf16(128, a.n1, true, false);
   const uint32_t id2 = umma_idesc_bf16(128, a.n2, false, false);
   const uint32_t id3 = umma_idesc_bf16(128, a.n3, false, false);
-  uint32_t phase = 0;
+  uint32_t phase = 0, a1phase = 0;
   const int ntiles = a.F * a.tiles_per_frame;
   const bool async = (a.W % 8) == 0;
+  const bool bulk = a.a1_tma != 0;  // A1 by one TMA box per tile (tensor map over X)
   const int stride = nwg * gridDim.x;
+  auto fetch_a1 = [&](int t) {
+    if (bulk) {
+      if (ltid == 0) {
+        mbar_arrive_expect_tx(a1bar, a1_bytes);
+        if (a.xtile == 2) {
+          tma_load_5d(A1, &tmap_x, 0, 0, 0, 0, t, a1bar);
+        } else {
+          int f, pix0, n;
+          tile_pixels(a, t, f, pix0, n);
+          tma_load_4d(A1, &tmap_x, 0, 0, pix0 >> 3, f, a1bar);
+        }
+      }
+    } else {
+      int f, pix0, n;
+      tile_pixels(a, t, f, pix0, n);
+      load_a1<NIN>(a, A1, t, f, pix0, n, ltid, async);
+    }
+  };
 
   int tile = nwg * blockIdx.x + wg;
-  if (tile < ntiles) {
-    int f, pix0, n;
-    tile_pixels(a, tile, f, pix0, n);
-    load_a1<NIN>(a, A1, tile, f, pix0, n, ltid, async);
-  }
+  if (tile < ntiles) fetch_a1(tile);
   cp_async_commit();
   for (; tile < ntiles; tile += stride) {
-    cp_async_wait<0>();  // this tile's A1 (issued during the previous tile's layers 2-3)
+    if (bulk) {  // this tile's A1 (issued during the previous tile's layers 2-3); then the
+                 // padding planes [nin, k1): 0, the bias plane 1 (the box fills them with
+                 // zeros or, on octet-pair tiles, the odd plane of the last pair unwritten)
+      mbar_wait(a1bar, a1phase);
+      a1phase ^= 1;
+      const int npad = a.k1 - a.nin;
+      for (int idx = ltid; idx < npad * 16; idx += 128) {
+        const int k = a.nin + idx % npad, g = idx / npad;
+        const uint32_t one = (a.bias_folded && k == a.nin) ? 0x3F803F80u : 0u;
+        *reinterpret_cast<uint4*>(A1 + g * (a.k1 * 16) + k * 16) = make_uint4(one, one, one, one);
+      }
+    } else {
+      cp_async_wait<0>();  // this tile's A1 (issued during the previous tile's layers 2-3)
+    }
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
@@ -230,11 +263,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     tc_fence_after();
     {  // A1 is free once layer 1 has completed: prefetch the next tile's inputs
       const int nxt = tile + stride;
-      if (nxt < ntiles) {
-        int fn, pn, nn;
-        tile_pixels(a, nxt, fn, pn, nn);
-        load_a1<NIN>(a, A1, nxt, fn, pn, nn, ltid, async);
-      }
+      if (nxt < ntiles) fetch_a1(nxt);
       cp_async_commit();
     }
     if (a.bias_folded)
@@ -341,6 +370,45 @@ int launch_pack_weights(const p2s_plan_s* p, int F, const float* wts, cudaStream
   return (int)cudaGetLastError();
 }
 
+// Tensor map that delivers a 128-pixel tile's inputs as the A1 operand image
+// [16 octets][k1 planes][8 px] in one TMA box; the dimension order is the smem order, the
+// strides are X's layout (planes past nin are outside the map: zero-filled).
+//   planes (xtile 0) [F][nin][HW]: dims {8 px, nin, HW/8 octets, F}, box {8, k1, 16, 1}
+//   octet-pair tiles (xtile 2) [tiles][nin2/2][16][2][8]: dims {8 px, 2, nin2/2, 16 octets,
+//   tiles}, box {8, 2, k1/2, 16, 1}
+// Returns false when the layout / alignment does not allow it (k_mlp then loads A1 with
+// per-thread copies).
+static bool encode_x_map(CUtensorMap* m, const p2s_plan_s* p, const MlpArgs& a) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !encode)
+      return false;
+  }
+  if (((uintptr_t)a.X & 15) || a.k1 > 256) return false;
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  if (a.xtile == 0) {
+    if (a.W % 8 || a.HW % 8) return false;
+    cuuint64_t dims[4] = {8, (cuuint64_t)a.nin, (cuuint64_t)a.HW / 8, (cuuint64_t)a.F};
+    cuuint64_t strides[3] = {(cuuint64_t)a.HW * 2, 16, (cuuint64_t)a.nin * a.HW * 2};
+    cuuint32_t box[4] = {8, (cuuint32_t)a.k1, 16, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(a.X), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  if (a.xtile == 2) {
+    const int nin2 = (a.nin + 1) & ~1;
+    cuuint64_t dims[5] = {8, 2, (cuuint64_t)nin2 / 2, 16, (cuuint64_t)a.F * a.tiles_per_frame};
+    cuuint64_t strides[4] = {16, 512, 32, (cuuint64_t)nin2 * 256};
+    cuuint32_t box[5] = {8, 2, (cuuint32_t)a.k1 / 2, 16, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<uint16_t*>(a.X), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  return false;
+}
+
 int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   const MlpGeom& g = folded ? p->mg_fold : p->mg_plain;
   MlpArgs a;
@@ -371,14 +439,17 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   const size_t blob_al = (g.blob_bytes + 127) & ~(size_t)127;
   const size_t per_wg = 128 * g.k1 * 2 + 128 * nmax * 2;
   int nwg = std::min(kMlpWG, 512 / cols_wg);
-  while (nwg > 1 && blob_al + nwg * per_wg + 64 > 227 * 1024) --nwg;
-  size_t sm = blob_al + nwg * per_wg + 64;
+  while (nwg > 1 && blob_al + nwg * per_wg + 128 > 227 * 1024) --nwg;
+  size_t sm = blob_al + nwg * per_wg + 128;
   auto kern = a.nin == 35 ? k_mlp<35> : a.nin == 33 ? k_mlp<33> : k_mlp<0>;
   P2S_SMEM_OPTIN(kern, sm);
   const int ntiles = F * a.tiles_per_frame;
   int grid = p->num_sms;  // persistent: one CTA (nwg tile pipelines) per SM
   if (nwg * grid > ntiles) grid = (ntiles + nwg - 1) / nwg;
-  kern<<<grid, 128 * nwg, sm, s>>>(a);
+  CUtensorMap tmap_x;
+  std::memset(&tmap_x, 0, sizeof(tmap_x));
+  a.a1_tma = (p->force & P2S_FORCE_MLP_A1_THREADS) ? 0 : encode_x_map(&tmap_x, p, a) ? 1 : 0;
+  kern<<<grid, 128 * nwg, sm, s>>>(a, tmap_x);
   return (int)cudaGetLastError();
 }
 

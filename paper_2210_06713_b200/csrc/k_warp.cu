@@ -69,14 +69,6 @@ __global__ void __launch_bounds__(256) k_warp(WarpArgs a) {
 constexpr int kWarpTX = 64, kWarpTY = 32, kWarpM = 8;
 constexpr int kWarpBX = kWarpTX + 2 * kWarpM, kWarpBY = kWarpTY + 2 * kWarpM;
 
-__device__ __forceinline__ void tma_load_4d(void* sdst, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
-          smem_u32(sdst)),
-      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
-      : "memory");
-}
-
 template <int C>
 __global__ void __launch_bounds__(256) k_warp_tma(WarpArgs a, const __grid_constant__ CUtensorMap tmap_img, int img_frames) {
   extern __shared__ __align__(128) float win[];  // [C][kWarpBY][kWarpBX]

@@ -57,6 +57,7 @@ FORCE_BLUR_SINGLE = 0x200
 FORCE_COLS_PERSISTENT = 0x400
 FORCE_WARP_GATHER = 0x800
 FORCE_X_OCTETS = 0x1000
+FORCE_MLP_A1_THREADS = 0x2000
 
 
 def _load():

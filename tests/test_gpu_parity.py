@@ -332,7 +332,8 @@ def test_blur_single_basis_vs_oracle(H, W, K, T, k0):
     assert rel_l2(out.cpu().numpy()[0, 0], ref[0]) <= 1e-2
 
 
-@pytest.mark.parametrize("force", [0, 0x080, 0x1000])  # forced tile-major / octet-pair MLP input layouts
+# forced tile-major / octet-pair MLP input layouts; per-thread A1 copies instead of the TMA box
+@pytest.mark.parametrize("force", [0, 0x080, 0x1000, 0x2000, 0x3000])
 @pytest.mark.parametrize("H,W,C,K,T", [(64, 64, 1, 16, 17), (96, 160, 3, 100, 33), (40, 90, 1, 16, 17)])
 def test_blur_api_vs_oracle(H, W, C, K, T, force):
     plan, basis, mlp, sq, L = make_plan(H, W, C, 3.0, K, T, force=force)
@@ -432,7 +433,7 @@ def test_oversized_mlp_is_unsupported():
     assert e.value.status == 5  # P2S_ERR_UNSUPPORTED
 
 
-@pytest.mark.parametrize("force", [0, 0x080, 0x1000])  # forced tile-major / octet-pair MLP input layouts
+@pytest.mark.parametrize("force", [0, 0x080, 0x1000, 0x2000])  # MLP input layouts / A1 load paths
 def test_simulate_ar_sequence_vs_oracle(force):
     """Steps 1-5 on an AR(1) sequence (reading Q18): a fresh start and the stored-state
     continuation both follow the oracle's replayed sequence."""
@@ -676,3 +677,19 @@ def test_calls_on_a_destroyed_or_slab_plan_fail_loudly():
     with pytest.raises(P2SError) as e:
         q.sample_zernike(SEED, 0, 1, z)  # NULL plan after destroy
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("H,W", [(64, 160), (48, 200)])
+@pytest.mark.parametrize("layout", [0x040, 0x1000])
+def test_mlp_a1_tma_box_matches_thread_copies(H, W, layout):
+    """k_mlp's A1 operand by one TMA box per tile (the default for planes and octet-pair X)
+    equals the per-thread copies bit for bit, ragged last tile and partial rows included."""
+    outs = []
+    for extra in (0, 0x2000):
+        plan, basis, mlp, sq, L = make_plan(H, W, 3, 3.0, 16, 17, force=layout | extra)
+        img = synth.image(H, W, 3, seed=21)
+        out = torch.empty((2, 3, H, W), device="cuda")
+        plan.simulate_frames(cuda(img), 0, SEED, 0, 2, out)
+        torch.cuda.synchronize()
+        outs.append(out.cpu())
+    assert torch.equal(outs[0], outs[1])
