@@ -869,17 +869,19 @@ static bool reg512(const AxisFFT& ax) {
 }
 
 // MLP input layout shared by its producers (k_cols*, k_zern_to_x) and k_mlp, decided once
-// at plan creation (p2s_plan_s::xtile).  Octet-pair tiles (x_index, xtile 2) from 2M pixels
-// per frame (1080p, 4K): k_mlp 1.38 -> 1.33 ms per launch at both (contiguous 9 KB tile
-// blocks, r1 measured 2.05 -> 1.36 at 4K for the tile-major layout against planes), the
-// long-column kernel's stores unchanged; planes at 512^2, where k_cols512 writes one column
-// per thread and the tiled addressing cost it 0.13 ms (k_mlp -0.05).  P2S_FORCE_X_PLANES /
-// _X_TILES / _X_OCTETS force a layout.
+// at plan creation (p2s_plan_s::xtile).  Octet-pair tiles (x_index, xtile 2) from 1M pixels
+// per frame (1080p, 4K): contiguous 9 KB tile blocks (r1 measured 2.05 -> 1.36 ms at 4K for
+// the tile-major layout against planes), the long-column kernel's stores unchanged, and
+// k_mlp's TMA box over them (r2) 1.20 ms at 1080p against 1.45 for planes with per-thread
+// copies and 2.28 for planes by TMA (35 plane rows 4 MB apart per box); planes at 512^2
+// and below, where k_cols512 writes one column per thread and the tiled addressing cost it
+// 0.13 ms (octets + TMA at 512^2: k_mlp 1.24 vs 1.28, k_cols 1.24 vs 1.10).
+// P2S_FORCE_X_PLANES / _X_TILES / _X_OCTETS force a layout.
 int x_tile_layout(const p2s_plan_s* pl) {
   if (pl->force & P2S_FORCE_X_PLANES) return 0;
   if (pl->force & P2S_FORCE_X_TILES) return 1;
   if (pl->force & P2S_FORCE_X_OCTETS) return 2;
-  return (size_t)pl->H * pl->W >= ((size_t)2 << 20) ? 2 : 0;
+  return (size_t)pl->H * pl->W >= ((size_t)1 << 20) ? 2 : 0;
 }
 
 // Row-pass kernel variants (one per dispatch outcome of rows_variant).
