@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 
 namespace p2s {
@@ -42,6 +43,7 @@ struct MlpArgs {
   int bias_folded;  // A1 column nin is the constant 1; biases live in the weight images
   int xtile;        // X layout (x_index): 1 = tile-major [F][H][ntx][nin][128]
   int a1_tma;       // A1 tiles by TMA (tmap_x valid)
+  unsigned long long* probe;  // P2S_MLP_PROBE builds: [8] phase cycle sums, else null
 };
 
 // Epilogue of a hidden layer: TMEM columns [0, ncols) of this thread's row -> +bias -> ReLU
@@ -230,10 +232,24 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     }
   };
 
+#ifdef P2S_MLP_PROBE  // phase cycle counters of a tuning build (tools/blur_probe.py prints them)
+  unsigned long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  auto pclk = []() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    return t;
+  };
+#define MLP_T(i) const unsigned long long tt##i = pclk()
+#define MLP_ACC(i, a, b) pr[i] += tt##b - tt##a
+#else
+#define MLP_T(i)
+#define MLP_ACC(i, a, b)
+#endif
   int tile = nwg * blockIdx.x + wg;
   if (tile < ntiles) fetch_a1(tile);
   cp_async_commit();
   for (; tile < ntiles; tile += stride) {
+    MLP_T(0);
     if (bulk) {  // this tile's A1 (issued during the previous tile's layers 2-3); then the
                  // padding planes [nin, k1): 0, the bias plane 1 (the box fills them with
                  // zeros or, on octet-pair tiles, the odd plane of the last pair unwritten)
@@ -251,6 +267,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
+    MLP_T(1);
     // ---- layer 1
     if (ltid == 0) {
       tma_store_wait_read();  // the previous tile's w store has finished reading A2
@@ -261,6 +278,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
+    MLP_T(2);
     {  // A1 is free once layer 1 has completed: prefetch the next tile's inputs
       const int nxt = tile + stride;
       if (nxt < ntiles) fetch_a1(nxt);
@@ -270,9 +288,11 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
       mlp_hidden_epilogue<false>(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m);
     else
       mlp_hidden_epilogue<true>(taddr, a.n1, b1, A2, (a.n1 / 8) * 128, m);
+    MLP_T(3);
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
+    MLP_T(4);
     // ---- layer 2
     if (ltid == 0) {
       tc_fence_after();
@@ -282,10 +302,12 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
+    MLP_T(5);
     if (a.bias_folded)
       mlp_hidden_epilogue<false>(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m);
     else
       mlp_hidden_epilogue<true>(taddr, a.n2, b2, A2, (a.n2 / 8) * 128, m);
+    MLP_T(6);
     fence_async_smem();
     tc_fence_before();
     wg_sync(wg);
@@ -298,6 +320,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
+    MLP_T(7);
     // w tile -> A2 as [n3/8][128 px][8] bf16 (16-byte stores, consecutive lanes adjacent),
     // then one bulk copy of the whole tile.
     {
@@ -325,7 +348,20 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
     wg_sync(wg);
     // tile index == (f * H + y) * ntx + xt: the output block of this row tile
     if (ltid == 0) bulk_s2g(a.wout + (size_t)tile * a.n3 * 128, A2, (uint32_t)a.n3 * 256);
+    MLP_T(8);
+    MLP_ACC(0, 0, 1);  // A1 wait (+ padding planes) + group sync
+    MLP_ACC(1, 1, 2);  // layer 1 (after the previous w store has read A2)
+    MLP_ACC(2, 2, 3);  // next tile's A1 prefetch issue + epilogue 1
+    MLP_ACC(3, 3, 4);  // sync
+    MLP_ACC(4, 4, 5);  // layer 2
+    MLP_ACC(5, 5, 6);  // epilogue 2
+    MLP_ACC(6, 6, 7);  // sync + layer 3
+    MLP_ACC(7, 7, 8);  // output epilogue + sync + store issue
   }
+#ifdef P2S_MLP_PROBE
+  if (ltid == 0 && a.probe)
+    for (int i = 0; i < 8; ++i) atomicAdd(&a.probe[i], pr[i]);
+#endif
   if (ltid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
@@ -453,7 +489,27 @@ int launch_mlp(const p2s_plan_s* p, int F, bool folded, cudaStream_t s) {
   CUtensorMap tmap_x;
   std::memset(&tmap_x, 0, sizeof(tmap_x));
   a.a1_tma = (p->force & P2S_FORCE_MLP_A1_THREADS) ? 0 : encode_x_map(&tmap_x, p, a) ? 1 : 0;
+  a.probe = nullptr;
+#ifdef P2S_MLP_PROBE
+  static unsigned long long* probe = nullptr;
+  if (!probe) cudaMalloc(&probe, 8 * sizeof(unsigned long long));
+  cudaMemsetAsync(probe, 0, 8 * sizeof(unsigned long long), s);
+  a.probe = probe;
+#endif
   kern<<<grid, 128 * nwg, sm, s>>>(a, tmap_x);
+#ifdef P2S_MLP_PROBE
+  {
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, probe, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const double nt = (double)ntiles;
+    fprintf(stderr,
+            "[mlp probe] tiles %.0f A1 %s | per tile cycles: A1 wait %.0f | L1 %.0f | prefetch+epi1 %.0f | sync %.0f | "
+            "L2 %.0f | epi2 %.0f | sync+L3 %.0f | epi3+store %.0f\n",
+            nt, a.a1_tma ? "TMA" : "threads", h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt,
+            h[6] / nt, h[7] / nt);
+  }
+#endif
   return (int)cudaGetLastError();
 }
 

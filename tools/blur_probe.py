@@ -1,9 +1,10 @@
 #!/usr/bin/env python
-"""k_blur phase cycle counters (development tool): run with libp2s built with
-EXTRA=-DP2S_BLUR_PROBE; each blur launch prints per-CTA phase averages to stderr.
+"""k_blur / k_mlp phase cycle counters (development tool): run with libp2s built with
+EXTRA=-DP2S_BLUR_PROBE and/or -DP2S_MLP_PROBE; each blur / MLP launch prints per-CTA
+(blur) or per-tile (MLP) phase averages to stderr.
 
     make -C paper_2210_06713_b200/csrc clean && make -C paper_2210_06713_b200/csrc EXTRA=-DP2S_BLUR_PROBE
-    python tools/blur_probe.py [--workload cfg3_512] [--reps 3]
+    python tools/blur_probe.py [--workload cfg3_512] [--reps 3] [--force 0x2000]
 """
 import argparse
 import os
