@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(128 * kMlpWG, 1)
   const int stride = nwg * gridDim.x;
   auto fetch_a1 = [&](int t) {
     if (bulk) {
-      if (ltid == 0) {
+      if (ltid == 32) {  // warp 1: warp 0 already issues the layer MMAs and waits on the w store
         mbar_arrive_expect_tx(a1bar, a1_bytes);
         if (a.xtile == 2) {
           tma_load_5d(A1, &tmap_x, 0, 0, 0, 0, t, a1bar);
