@@ -49,36 +49,30 @@ struct MlpArgs {
 // Epilogue of a hidden layer: TMEM columns [0, ncols) of this thread's row -> +bias -> ReLU
 // -> bf16 -> the next layer's K-major A operand (row m of a [128 x ncols] SWIZZLE_NONE
 // image, core matrices of 8 rows x 16 B, k-chunks at 128 B, 8-row groups at sbo).
-// TMEM loads are issued 32 columns at a time before one wait.
+// One 16-column TMEM load per wait (measured: 32 or 64 columns per wait are slower).
 template <bool BIAS>
 __device__ __forceinline__ void mlp_hidden_epilogue(uint32_t taddr, int ncols, const float* bias, uint8_t* a_smem,
                                                     uint32_t sbo, int m) {
   uint8_t* rowbase = a_smem + (m & 7) * 16 + (m >> 3) * sbo;
-  for (int c0 = 0; c0 < ncols; c0 += 32) {
-    uint32_t r[32];
+  for (int c0 = 0; c0 < ncols; c0 += 16) {  // 16 columns per TMEM wait
+    uint32_t r[16];
     tmem_ld16_issue(taddr + c0, r);
-    const bool two = c0 + 16 < ncols;
-    if (two) tmem_ld16_issue(taddr + c0 + 16, r + 16);
     tmem_wait_ld();
+    uint32_t pk[8];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (h == 1 && !two) break;
-      uint32_t pk[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float x0 = __uint_as_float(r[16 * h + 2 * i]), x1 = __uint_as_float(r[16 * h + 2 * i + 1]);
-        if (BIAS) {
-          x0 += bias[c0 + 16 * h + 2 * i];
-          x1 += bias[c0 + 16 * h + 2 * i + 1];
-        }
-        x0 = fmaxf(x0, 0.f);
-        x1 = fmaxf(x1, 0.f);
-        pk[i] = pack_bf16x2(x0, x1);
+    for (int i = 0; i < 8; ++i) {
+      float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+      if (BIAS) {
+        x0 += bias[c0 + 2 * i];
+        x1 += bias[c0 + 2 * i + 1];
       }
-      uint8_t* base = rowbase + ((c0 + 16 * h) / 8) * 128;
-      *reinterpret_cast<uint4*>(base) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-      *reinterpret_cast<uint4*>(base + 128) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      x0 = fmaxf(x0, 0.f);
+      x1 = fmaxf(x1, 0.f);
+      pk[i] = pack_bf16x2(x0, x1);
     }
+    uint8_t* base = rowbase + (c0 / 8) * 128;
+    *reinterpret_cast<uint4*>(base) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    *reinterpret_cast<uint4*>(base + 128) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
   }
 }
 
